@@ -1,0 +1,177 @@
+/*
+ * hsb200.h — C ABI of the B200-native hybrid sparse+dense inner-product search
+ * (the hot path of arXiv 1903.08690's `hybridsearch` reference package).
+ *
+ * Plain pointers and sizes only: no torch / Python types cross this boundary.
+ * Every entry point returns an hs_status; hs_last_error() gives the message of
+ * the calling thread's last failure.  Host-pointer entry points copy inputs to
+ * the device inside the call (borrowed for the duration of the call) and copy
+ * results back into caller-allocated host buffers.  `_dev` entry points take
+ * device pointers and a cudaStream_t (as void*), and enqueue without syncing.
+ *
+ * Reference interfaces replaced (paths relative to /root/reference/pkg/src/hybridsearch):
+ *   hs_index_create      <- the HybridIndex a search consumes      pipeline.py:92-116
+ *                           (InvertedIndex sparse.py:172-200, PQCodes dense.py:183-209,
+ *                            Codebooks dense.py:25-54, ScalarQuantResidual dense.py:361-378,
+ *                            WhiteningTransform dense.py:320-330, HybridDataset data.py:118-162)
+ *   hs_search_batch      <- search_batch / search_topk             pipeline.py:282-300, 226-279
+ *   hs_search_batch_dev  <- same, device-resident queries/results  (no reference counterpart)
+ *   hs_adc_table         <- adc_table                              dense.py:212-220
+ *   hs_quantize_lut      <- quantize_lut + QuantizedLUT.bias_total dense.py:248-260, 243-245
+ *   hs_lut16_scan        <- lut16_scan / lut16_scan_reference      dense.py:297-317, 263-281
+ *   hs_sparse_scan       <- sparse_scan (Accumulator scores)       sparse.py:268-284
+ *   hs_stage1_scores     <- _stage1_scores                         pipeline.py:192-203
+ *   hs_select_topk       <- select_topk                            pipeline.py:165-189
+ *   hs_exact_topk        <- brute_force_topk (_exact_scores)       harness.py:25-35, pipeline.py:313-322
+ *   hs_shard_merge_dev   <- (new) top-h merge of per-shard results; no reference counterpart
+ */
+#ifndef HSB200_H
+#define HSB200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  HS_OK = 0,
+  HS_EINVAL = 1,       /* -> ValueError   (pipeline.py:235-245, dense.py:251-252, dense.py:304-305) */
+  HS_ENOMEM = 2,       /* -> MemoryError */
+  HS_ECUDA = 3,        /* -> RuntimeError */
+  HS_ENCCL = 4,        /* -> RuntimeError */
+  HS_EUNSUPPORTED = 5  /* -> ValueError (e.g. 256-center codes in lut16_scan, dense.py:304-305) */
+} hs_status;
+
+typedef struct hs_index* hs_index_t;
+
+/* Borrowed host arrays describing one immutable hybrid index.  All sparse
+ * dimension ids are uint32 (d_sparse < 2^32); row pointers are int64. */
+typedef struct {
+  int64_t n;             /* points */
+  int64_t d_sparse;      /* sparse dimensionality */
+  int64_t d_dense;       /* dense dimensionality (0 = no dense part) */
+  const int64_t* order;  /* [n] layout slot -> original id (pipeline.py:102) */
+
+  /* pruned scan index: posting lists of the active dims, ascending dims,
+   * ids strictly ascending within a list (sparse.py:219-235) */
+  int64_t n_active;
+  const uint32_t* post_dims;  /* [n_active] */
+  const int64_t* post_ptr;    /* [n_active+1] */
+  const uint32_t* post_ids;   /* [nnz] layout slots */
+  const float* post_w;        /* [nnz] */
+
+  /* forward sparse residual, rows in layout order (pipeline.py:137-138) */
+  const int64_t* res_indptr;  /* [n+1] or NULL when empty */
+  const uint32_t* res_indices;
+  const float* res_data;
+
+  /* dense PQ part (present iff d_dense > 0) */
+  int32_t n_subspaces;        /* K */
+  int32_t n_centers;          /* l: 16 for the LUT16 scan, 256 is rejected at search */
+  const int32_t* subdims;     /* [K] widths, contiguous subspaces (dense.py:57-62) */
+  const float* centers;       /* concatenation over k of centers[k] (l x subdims[k]) row-major */
+  const uint8_t* packed;      /* [(K+1)/2][n] pair-major 4-bit codes (dense.py:156-170) */
+  int32_t has_sq;             /* scalar-quant residual present (dense.py:361-378) */
+  const float* sq_lo;         /* [d_dense] */
+  const float* sq_step;       /* [d_dense] */
+  const uint8_t* sq_codes;    /* [n][d_dense] layout order */
+  int32_t has_whitening;      /* query-side whitening (dense.py:351-357) */
+  const double* wh_mean;      /* [d_dense] */
+  const double* wh_inverse_t; /* [d_dense][d_dense] */
+
+  /* raw dataset for exact rerank / ground truth (optional; original id order) */
+  int32_t has_dataset;
+  const float* ds_dense;      /* [n][d_dense] */
+  const int64_t* ds_indptr;   /* [n+1] */
+  const uint32_t* ds_indices;
+  const float* ds_data;
+
+  /* query-time weights from HybridIndexConfig (pipeline.py:51-52) */
+  double sparse_weight;
+  double dense_weight;
+  /* added to every returned original id (multi-GPU id-range shards) */
+  int64_t id_offset;
+} hs_index_desc;
+
+/* A batch of queries: CSR sparse parts (ascending dims per row) + dense rows. */
+typedef struct {
+  int64_t nq;
+  const int64_t* sp_indptr;   /* [nq+1] */
+  const uint32_t* sp_dims;    /* [nnz] */
+  const float* sp_vals;       /* [nnz] */
+  const float* dense;         /* [nq][d_dense] (may be NULL when d_dense == 0) */
+  /* optional hints for the _dev entry points (<= 0: derived with a D2H copy) */
+  int64_t nnz;                /* sp_indptr[nq] - sp_indptr[0] */
+  int32_t max_row_nnz;        /* max over rows of the row length */
+} hs_query_batch;
+
+/* Per-call search knobs; resolved by the caller from HybridIndexConfig and
+ * the call overrides (pipeline.py:233-245). */
+typedef struct {
+  int32_t h;
+  double overfetch;           /* alpha: k1 = min(n, ceil(alpha*h)) */
+  double retain;              /* beta:  k2 = min(k1, ceil(beta*h)) */
+  int32_t exact_final_rerank;
+} hs_search_params;
+
+const char* hs_last_error(void);
+const char* hs_version(void);
+
+/* ---- index lifetime ---- */
+int hs_index_create(const hs_index_desc* desc, int device, hs_index_t* out);
+void hs_index_destroy(hs_index_t index);
+int hs_index_memory_bytes(hs_index_t index, int64_t* bytes);
+
+/* Result slots per query = kh = min(h, k2); counts[3] = {k1, k2, kh}.
+ * stage_seconds[3] receives device time per stage summed over the batch. */
+int hs_result_sizes(hs_index_t index, const hs_search_params* p, int64_t counts[3]);
+
+/* ---- the hot path ---- */
+int hs_search_batch(hs_index_t index, const hs_query_batch* queries,
+                    const hs_search_params* params, int64_t* out_ids,
+                    double* out_scores, double* stage_seconds);
+
+/* Device-resident variant: every pointer in `queries` and the outputs are
+ * device pointers; enqueued on `stream` (cudaStream_t), no host sync. */
+int hs_search_batch_dev(hs_index_t index, const hs_query_batch* queries,
+                        const hs_search_params* params, int64_t* d_out_ids,
+                        double* d_out_scores, void* stream);
+
+/* ---- unit entry points (parity tests; each mirrors one reference function) ---- */
+/* T[q][k][c] = <centers[k][c], qw[q][slice k]> in f64. */
+int hs_adc_table(const float* centers, const int32_t* subdims, int32_t K, int32_t l,
+                 const double* qw, int64_t nq, int64_t d, double* T);
+/* u8 table, per-row bias, shared scale, numpy-pairwise bias_total. */
+int hs_quantize_lut(const double* T, int64_t nq, int32_t K, int32_t l, uint8_t* table,
+                    double* bias, double* scale, double* bias_total);
+/* integer totals and bias_total + scale*total for nq LUTs over n points. */
+int hs_lut16_scan(const uint8_t* packed, int64_t n, int32_t K, const uint8_t* qtable,
+                  const double* bias_total, const double* scale, int64_t nq,
+                  int32_t* totals, double* scores);
+/* f64 accumulator in layout order, weights NOT applied (sparse.py:268-284). */
+int hs_sparse_scan(hs_index_t index, const hs_query_batch* queries, double* acc);
+/* stage-1 scores in layout order with the index's weights (pipeline.py:192-203). */
+int hs_stage1_scores(hs_index_t index, const hs_query_batch* queries, double* scores);
+/* top-k positions per row by (score desc, tie asc); tie_ids NULL = positions. */
+int hs_select_topk(const double* scores, int64_t nq, int64_t n, int64_t k,
+                   const int64_t* tie_ids, int64_t* out);
+/* exact top-h (brute force over the raw dataset), ids original. */
+int hs_exact_topk(hs_index_t index, const hs_query_batch* queries, int32_t h,
+                  int64_t* out_ids, double* out_scores);
+
+/* Merge G gathered per-shard results (ids/scores [G][nq][kh], device) into
+ * the top-h per query by (score desc, id asc). */
+int hs_shard_merge_dev(const int64_t* d_ids, const double* d_scores, int64_t G,
+                       int64_t nq, int64_t kh, int32_t h, int64_t* d_out_ids,
+                       double* d_out_scores, void* stream);
+
+/* Timing of the last search on this index: per-kernel CUDA-event averages
+ * (used by bench.py for the roofline). names joined by ';'. */
+int hs_last_kernel_times(hs_index_t index, double* ms, int32_t max_entries,
+                         int32_t* n_entries, char* names, int32_t names_cap);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HSB200_H */

@@ -1,0 +1,825 @@
+// api.cu — the C ABI (include/hsb200.h): index upload, the batched
+// three-stage search driver and the unit entry points.
+//
+// Search driver (replaces search_topk / search_batch, reference
+// pipeline.py:226-300): queries are processed in chunks; per chunk
+//   map_dims -> lut_build -> stage1 (fused scan + per-tile top-k) ->
+//   select (merge tiles to the top k1) -> stage2 -> stage3 -> outputs,
+// all enqueued on the index's stream with no host round trip between stages.
+#include <algorithm>
+#include <cstring>
+#include <memory>
+#include <vector>
+
+#include "kernels.cuh"
+
+namespace hs {
+
+static thread_local std::string g_err;
+void set_error(const std::string& msg) { g_err = msg; }
+const char* last_error() { return g_err.c_str(); }
+
+namespace {
+
+template <typename T>
+int dalloc(DeviceIndex& ix, T** p, size_t count) {
+  *p = nullptr;
+  if (count == 0) return HS_OK;
+  HS_CUDA(cudaMalloc(reinterpret_cast<void**>(p), sizeof(T) * count));
+  ix.bytes += (int64_t)(sizeof(T) * count);
+  return HS_OK;
+}
+
+template <typename T>
+int dupload(DeviceIndex& ix, T** p, const T* src, size_t count) {
+  HS_CHECK(dalloc(ix, p, count));
+  if (count) HS_CUDA(cudaMemcpy(*p, src, sizeof(T) * count, cudaMemcpyHostToDevice));
+  return HS_OK;
+}
+
+__global__ void k_interleave(const uint32_t* ids, const float* w, int64_t n, uint2* out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = make_uint2(ids[i], __float_as_uint(w[i]));
+}
+
+__global__ void k_order_u32(const int64_t* in, int64_t n, uint32_t* out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = (uint32_t)in[i];
+}
+
+void free_device_arrays(DeviceIndex* ix) {
+  if (!ix) return;
+  cudaSetDevice(ix->device);
+  void* ptrs[] = {ix->order,    ix->post_dims,  ix->post_ptr, ix->post,       ix->res_indptr,
+                  ix->res_indices, ix->res_data, ix->subdims,  ix->dim_off,    ix->cen_off,
+                  ix->centers,  ix->packed,     ix->sq_lo,    ix->sq_step,    ix->sq_codes,
+                  ix->wh_mean,  ix->wh_inv_t,   ix->ds_dense, ix->ds_indptr,  ix->ds_indices,
+                  ix->ds_data,  ix->scratch};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  if (ix->stream) cudaStreamDestroy(ix->stream);
+}
+
+int ensure_scratch(DeviceIndex& ix, size_t bytes) {
+  if (bytes <= ix.scratch_bytes) return HS_OK;
+  if (ix.scratch) {
+    HS_CUDA(cudaStreamSynchronize(ix.stream));
+    cudaFree(ix.scratch);
+    ix.scratch = nullptr;
+    ix.scratch_bytes = 0;
+  }
+  const size_t want = bytes + bytes / 4;
+  HS_CUDA(cudaMalloc(&ix.scratch, want));
+  ix.scratch_bytes = want;
+  return HS_OK;
+}
+
+struct Arena {
+  char* base;
+  size_t off = 0;
+  template <typename T>
+  T* take(size_t count) {
+    off = (off + 255) & ~size_t(255);
+    T* p = reinterpret_cast<T*>(base + off);
+    off += sizeof(T) * count;
+    return p;
+  }
+};
+
+struct Sizes {
+  int64_t k1 = 0, k2 = 0, kh = 0;
+};
+
+int resolve_sizes(const DeviceIndex& ix, const hs_search_params* p, Sizes* s) {
+  if (!p) HS_FAIL(HS_EINVAL, "null search params");
+  if (p->h < 1) HS_FAIL(HS_EINVAL, "h must be >= 1");
+  if (!(p->overfetch >= p->retain && p->retain >= 1.0))
+    HS_FAIL(HS_EINVAL, "need overfetch >= retain >= 1");
+  // k1 = min(n, ceil(alpha*h)); k2 = min(k1, ceil(beta*h)) (pipeline.py:251, 261)
+  const double a = std::ceil(p->overfetch * (double)p->h);
+  const double b = std::ceil(p->retain * (double)p->h);
+  s->k1 = (int64_t)std::min<double>((double)ix.n, a);
+  s->k2 = (int64_t)std::min<double>((double)s->k1, b);
+  s->kh = std::min<int64_t>(p->h, s->k2);
+  return HS_OK;
+}
+
+constexpr int64_t kMaxRerank = 8192;  // k1/k2 held in shared memory for stages 2-3
+
+// time accumulation helpers
+struct Timer {
+  DeviceIndex* ix;
+  cudaStream_t st;
+  std::vector<cudaEvent_t> evs;
+  std::vector<std::string> names;
+  bool on;
+  Timer(DeviceIndex* ix_, cudaStream_t st_, bool on_) : ix(ix_), st(st_), on(on_) {}
+  void mark(const char* name) {
+    if (!on) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, st);
+    evs.push_back(e);
+    names.push_back(name ? name : "");
+  }
+  // names[i] labels the interval (evs[i-1], evs[i])
+  void finish(double* stage_seconds) {
+    if (!on || evs.empty()) return;
+    cudaEventSynchronize(evs.back());
+    ix->tnames.clear();
+    ix->tms.clear();
+    double st3[3] = {0, 0, 0};
+    for (size_t i = 1; i < evs.size(); ++i) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, evs[i - 1], evs[i]);
+      const std::string& nm = names[i];
+      auto it = std::find(ix->tnames.begin(), ix->tnames.end(), nm);
+      if (it == ix->tnames.end()) {
+        ix->tnames.push_back(nm);
+        ix->tms.push_back(ms);
+      } else {
+        ix->tms[it - ix->tnames.begin()] += ms;
+      }
+      if (nm == "map_dims" || nm == "lut_build" || nm == "stage1" || nm == "merge") st3[0] += ms;
+      else if (nm == "stage2") st3[1] += ms;
+      else if (nm == "stage3") st3[2] += ms;
+    }
+    if (stage_seconds)
+      for (int i = 0; i < 3; ++i) stage_seconds[i] = st3[i] * 1e-3;
+    for (auto e : evs) cudaEventDestroy(e);
+    evs.clear();
+  }
+};
+
+// Full search for a device-resident query batch.  `max_qnnz`/`nnz` known.
+int run_search(DeviceIndex& ix, const hs_query_batch& qb, int64_t nnz, int max_qnnz,
+               const hs_search_params* params, int64_t* d_ids, double* d_scores, cudaStream_t st,
+               Timer* tm, bool check_lut = false) {
+  Sizes sz;
+  HS_CHECK(resolve_sizes(ix, params, &sz));
+  const int64_t nq = qb.nq;
+  if (nq <= 0 || sz.kh <= 0) return HS_OK;
+  if (ix.d_dense > 0 && ix.l != 16) HS_FAIL(HS_EUNSUPPORTED, "lut16_scan requires 16-center codes");
+  if (params->exact_final_rerank && !ix.has_ds)
+    HS_FAIL(HS_EINVAL, "exact_final_rerank requires the original dataset");
+  if (sz.k1 > kMaxRerank)
+    HS_FAIL(HS_EUNSUPPORTED, "overfetch*h above 8192 candidates is not supported");
+  if (max_qnnz > 8192) HS_FAIL(HS_EUNSUPPORTED, "queries with more than 8192 sparse nonzeros");
+
+  // query-chunk size bounded by scratch for the stage-1 per-tile outputs
+  int64_t QB = std::min<int64_t>(nq, 2048);
+  int64_t s1_entries = 0;
+  for (;;) {
+    const Stage1Plan p0 = plan_stage1(ix, QB, sz.k1, max_qnnz, S1_SELECT);
+    s1_entries = QB * p0.ntiles * p0.out_per_tile;
+    const int64_t last = nq % QB;
+    if (last) {
+      const Stage1Plan p1 = plan_stage1(ix, last, sz.k1, max_qnnz, S1_SELECT);
+      s1_entries = std::max<int64_t>(s1_entries, last * p1.ntiles * p1.out_per_tile);
+    }
+    if ((double)s1_entries * sizeof(Cand) <= 1.0e9 || QB == 1) break;
+    QB = (QB + 1) / 2;
+  }
+  const int64_t d = ix.d_dense;
+  const int Kp16 = ix.Kp * 16;
+  size_t need = 0;
+  {
+    Arena a{nullptr};
+    a.take<uint32_t>(nnz + 1);
+    a.take<uint32_t>(nnz + 1);
+    a.take<double>(nnz + 1);
+    a.take<double>(QB * d + 1);
+    a.take<double>(QB * d + 1);
+    a.take<uint8_t>(QB * Kp16 + 16);
+    a.take<double>(QB);
+    a.take<double>(QB);
+    a.take<double>(QB);
+    a.take<int>(QB);
+    a.take<Cand>((size_t)s1_entries + 1);
+    a.take<Cand>(QB * sz.k1 + 1);
+    a.take<Cand>(QB * sz.k2 + 1);
+    need = a.off + 1024;
+  }
+  HS_CHECK(ensure_scratch(ix, need));
+  Arena a{static_cast<char*>(ix.scratch)};
+  uint32_t* lbeg = a.take<uint32_t>(nnz + 1);
+  uint32_t* lend = a.take<uint32_t>(nnz + 1);
+  double* qv = a.take<double>(nnz + 1);
+  double* qd = a.take<double>(QB * d + 1);
+  double* qw = a.take<double>(QB * d + 1);
+  uint8_t* luts = a.take<uint8_t>(QB * Kp16 + 16);
+  double* btot = a.take<double>(QB);
+  double* scl = a.take<double>(QB);
+  double* off = a.take<double>(QB);
+  int* bad = a.take<int>(QB);
+  Cand* s1out = a.take<Cand>((size_t)s1_entries + 1);
+  Cand* cand1 = a.take<Cand>(QB * sz.k1 + 1);
+  Cand* cand2 = a.take<Cand>(QB * sz.k2 + 1);
+
+  if (tm) tm->mark("begin");
+  QueryView all;
+  all.nq = nq;
+  all.sp_indptr = qb.sp_indptr;
+  all.sp_dims = qb.sp_dims;
+  all.sp_vals = qb.sp_vals;
+  all.dense = qb.dense;
+  launch_map_dims(ix, all, nnz, true, lbeg, lend, qv, st);
+  if (tm) tm->mark("map_dims");
+  if (d > 0) HS_CUDA(cudaMemsetAsync(bad, 0, sizeof(int) * QB, st));
+
+  for (int64_t q0 = 0; q0 < nq; q0 += QB) {
+    const int64_t nqc = std::min(QB, nq - q0);
+    QueryView qc;
+    qc.nq = nqc;
+    qc.sp_indptr = qb.sp_indptr + q0;
+    qc.sp_dims = qb.sp_dims;
+    qc.sp_vals = qb.sp_vals;
+    qc.dense = qb.dense ? qb.dense + q0 * d : nullptr;
+    Stage1Plan pc = plan_stage1(ix, nqc, sz.k1, max_qnnz, S1_SELECT);
+    if (d > 0) {
+      launch_lut_build(ix, qc.dense, nqc, qd, qw, luts, btot, scl, off, bad, st);
+      HS_CUDA(cudaGetLastError());
+      if (tm) tm->mark("lut_build");
+    } else if (params->exact_final_rerank) {
+      // no dense part: qd unused
+    }
+    HS_CHECK(launch_stage1(ix, qc, pc, lbeg, lend, qv, luts, btot, scl, off, s1out, nullptr, st));
+    if (tm) tm->mark("stage1");
+    HS_CHECK(launch_select_topk(s1out, nqc, (int64_t)pc.ntiles * pc.out_per_tile, sz.k1, cand1, st));
+    if (tm) tm->mark("merge");
+    launch_stage2(ix, cand1, nqc, (int)sz.k1, (int)sz.k2, qw, cand2, st);
+    HS_CUDA(cudaGetLastError());
+    if (tm) tm->mark("stage2");
+    launch_stage3(ix, qc, cand2, nqc, (int)sz.k2, (int)sz.kh, params->exact_final_rerank ? 1 : 0,
+                  max_qnnz, qd, d_ids + q0 * sz.kh, d_scores + q0 * sz.kh, st);
+    HS_CUDA(cudaGetLastError());
+    if (tm) tm->mark("stage3");
+  }
+  if (check_lut && d > 0) {
+    std::vector<int> hb(QB);
+    HS_CUDA(cudaMemcpyAsync(hb.data(), bad, sizeof(int) * QB, cudaMemcpyDeviceToHost, st));
+    HS_CUDA(cudaStreamSynchronize(st));
+    for (int v : hb)
+      if (v) HS_FAIL(HS_EINVAL, "lookup table contains non-finite values");
+  }
+  return HS_OK;
+}
+
+// host query batch -> device copies (owned by the returned holder)
+struct DevQueries {
+  hs_query_batch b{};
+  std::vector<void*> bufs;
+  int64_t nnz = 0;
+  int max_row = 0;
+  ~DevQueries() {
+    for (void* p : bufs) cudaFree(p);
+  }
+};
+
+int upload_queries(const DeviceIndex& ix, const hs_query_batch* q, DevQueries* out, bool check) {
+  if (!q || q->nq < 0) HS_FAIL(HS_EINVAL, "bad query batch");
+  const int64_t nq = q->nq;
+  const int64_t base = nq ? q->sp_indptr[0] : 0;
+  const int64_t nnz = nq ? q->sp_indptr[nq] - base : 0;
+  int max_row = 0;
+  std::vector<int64_t> ptr(nq + 1);
+  for (int64_t i = 0; i <= nq; ++i) ptr[i] = q->sp_indptr[i] - base;
+  for (int64_t i = 0; i < nq; ++i) {
+    const int64_t len = ptr[i + 1] - ptr[i];
+    if (len < 0) HS_FAIL(HS_EINVAL, "query indptr not monotone");
+    max_row = std::max<int64_t>(max_row, len);
+  }
+  if (check)
+    for (int64_t i = 0; i < nnz; ++i)
+      if ((int64_t)q->sp_dims[base + i] >= ix.d_sparse)
+        HS_FAIL(HS_EINVAL, "query sparse dimension out of range");
+  auto up = [&](const void* src, size_t bytes, void** dst) -> int {
+    *dst = nullptr;
+    HS_CUDA(cudaMalloc(dst, bytes ? bytes : 16));
+    out->bufs.push_back(*dst);
+    if (bytes) HS_CUDA(cudaMemcpyAsync(*dst, src, bytes, cudaMemcpyHostToDevice, ix.stream));
+    return HS_OK;
+  };
+  void *dptr, *ddims, *dvals, *ddense = nullptr;
+  HS_CHECK(up(ptr.data(), sizeof(int64_t) * (nq + 1), &dptr));
+  HS_CHECK(up(q->sp_dims + base, sizeof(uint32_t) * nnz, &ddims));
+  HS_CHECK(up(q->sp_vals + base, sizeof(float) * nnz, &dvals));
+  if (ix.d_dense > 0) {
+    if (!q->dense) HS_FAIL(HS_EINVAL, "query dense dimension mismatch");
+    HS_CHECK(up(q->dense, sizeof(float) * nq * ix.d_dense, &ddense));
+  }
+  HS_CUDA(cudaStreamSynchronize(ix.stream));  // ptr vector goes out of scope
+  out->b.nq = nq;
+  out->b.sp_indptr = static_cast<int64_t*>(dptr);
+  out->b.sp_dims = static_cast<uint32_t*>(ddims);
+  out->b.sp_vals = static_cast<float*>(dvals);
+  out->b.dense = static_cast<float*>(ddense);
+  out->b.nnz = nnz;
+  out->b.max_row_nnz = max_row;
+  out->nnz = nnz;
+  out->max_row = max_row;
+  return HS_OK;
+}
+
+int derive_hints(DeviceIndex& ix, const hs_query_batch* q, int64_t* nnz, int* max_row,
+                 cudaStream_t st) {
+  if (q->nnz > 0 && q->max_row_nnz > 0) {
+    *nnz = q->nnz;
+    *max_row = q->max_row_nnz;
+    return HS_OK;
+  }
+  std::vector<int64_t> ptr(q->nq + 1);
+  HS_CUDA(cudaMemcpyAsync(ptr.data(), q->sp_indptr, sizeof(int64_t) * (q->nq + 1),
+                          cudaMemcpyDeviceToHost, st));
+  HS_CUDA(cudaStreamSynchronize(st));
+  *nnz = ptr[q->nq] - ptr[0];
+  int m = 0;
+  for (int64_t i = 0; i < q->nq; ++i) m = std::max<int64_t>(m, ptr[i + 1] - ptr[i]);
+  *max_row = m;
+  (void)ix;
+  return HS_OK;
+}
+
+}  // namespace
+}  // namespace hs
+
+using namespace hs;
+
+struct hs_index : public hs::DeviceIndex {};
+
+namespace hs {
+static void free_index(hs_index* ix) {
+  if (!ix) return;
+  free_device_arrays(ix);
+  delete ix;
+}
+}  // namespace hs
+
+extern "C" {
+
+const char* hs_last_error(void) { return hs::last_error(); }
+const char* hs_version(void) { return "hsb200 0.1.0 (sm_100a)"; }
+
+int hs_index_create(const hs_index_desc* ds, int device, hs_index_t* out) {
+  if (!ds || !out) HS_FAIL(HS_EINVAL, "null argument");
+  *out = nullptr;
+  if (ds->n < 0 || ds->n >= (int64_t)0xFFFFFFFFLL) HS_FAIL(HS_EINVAL, "n out of range (< 2^32)");
+  if (ds->d_sparse < 0 || ds->d_sparse > (int64_t)0xFFFFFFFFLL)
+    HS_FAIL(HS_EINVAL, "d_sparse must be < 2^32");
+  const int64_t nnz_post = ds->n_active ? ds->post_ptr[ds->n_active] : 0;
+  if (nnz_post >= (int64_t)0xFFFFFFFFLL) HS_FAIL(HS_EINVAL, "more than 2^32 postings");
+  HS_CUDA(cudaSetDevice(device));
+  std::unique_ptr<hs_index, void (*)(hs_index*)> ix(new hs_index(), [](hs_index* p) {
+    hs::free_index(p);
+  });
+  ix->device = device;
+  ix->n = ds->n;
+  ix->d_sparse = ds->d_sparse;
+  ix->d_dense = ds->d_dense;
+  ix->id_offset = ds->id_offset;
+  ix->sparse_weight = ds->sparse_weight;
+  ix->dense_weight = ds->dense_weight;
+  HS_CUDA(cudaStreamCreateWithFlags(&ix->stream, cudaStreamNonBlocking));
+  const int64_t n = ds->n;
+  const int T = 256;
+
+  // order (u32 on device)
+  {
+    int64_t* tmp = nullptr;
+    HS_CUDA(cudaMalloc(&tmp, sizeof(int64_t) * std::max<int64_t>(n, 1)));
+    if (n) HS_CUDA(cudaMemcpy(tmp, ds->order, sizeof(int64_t) * n, cudaMemcpyHostToDevice));
+    HS_CHECK(dalloc(*ix, &ix->order, std::max<int64_t>(n, 1)));
+    if (n) k_order_u32<<<(unsigned)ceil_div(n, T), T>>>(tmp, n, ix->order);
+    HS_CUDA(cudaDeviceSynchronize());
+    cudaFree(tmp);
+  }
+  // postings
+  ix->n_active = ds->n_active;
+  ix->nnz_post = nnz_post;
+  {
+    std::vector<uint32_t> ptr32(ds->n_active + 1);
+    for (int64_t i = 0; i <= ds->n_active; ++i) ptr32[i] = (uint32_t)(ds->n_active ? ds->post_ptr[i] : 0);
+    HS_CHECK(dupload(*ix, &ix->post_dims, ds->post_dims, ds->n_active));
+    HS_CHECK(dupload(*ix, &ix->post_ptr, ptr32.data(), ds->n_active + 1));
+    if (nnz_post) {
+      uint32_t* tid = nullptr;
+      float* tw = nullptr;
+      HS_CUDA(cudaMalloc(&tid, sizeof(uint32_t) * nnz_post));
+      HS_CUDA(cudaMalloc(&tw, sizeof(float) * nnz_post));
+      HS_CUDA(cudaMemcpy(tid, ds->post_ids, sizeof(uint32_t) * nnz_post, cudaMemcpyHostToDevice));
+      HS_CUDA(cudaMemcpy(tw, ds->post_w, sizeof(float) * nnz_post, cudaMemcpyHostToDevice));
+      HS_CHECK(dalloc(*ix, &ix->post, nnz_post));
+      k_interleave<<<(unsigned)ceil_div(nnz_post, T), T>>>(tid, tw, nnz_post, ix->post);
+      HS_CUDA(cudaDeviceSynchronize());
+      cudaFree(tid);
+      cudaFree(tw);
+    } else {
+      HS_CHECK(dalloc(*ix, &ix->post, 1));
+    }
+  }
+  // sparse residual
+  if (ds->res_indptr && n) {
+    ix->res_nnz = ds->res_indptr[n] - ds->res_indptr[0];
+    HS_CHECK(dupload(*ix, &ix->res_indptr, ds->res_indptr, n + 1));
+    HS_CHECK(dupload(*ix, &ix->res_indices, ds->res_indices, ix->res_nnz));
+    HS_CHECK(dupload(*ix, &ix->res_data, ds->res_data, ix->res_nnz));
+  }
+  // dense
+  if (ds->d_dense > 0) {
+    const int K = ds->n_subspaces;
+    if (K <= 0) HS_FAIL(HS_EINVAL, "dense part without subspaces");
+    ix->K = K;
+    ix->l = ds->n_centers;
+    ix->Kp = (K + 1) & ~1;
+    ix->npairs = (K + 1) / 2;
+    std::vector<int32_t> doff(K), coff(K);
+    int64_t dsum = 0, csum = 0;
+    for (int k = 0; k < K; ++k) {
+      doff[k] = (int32_t)dsum;
+      coff[k] = (int32_t)csum;
+      dsum += ds->subdims[k];
+      csum += (int64_t)ds->subdims[k] * ds->n_centers;
+      ix->max_width = std::max(ix->max_width, ds->subdims[k]);
+    }
+    if (dsum != ds->d_dense) HS_FAIL(HS_EINVAL, "subspace widths do not sum to d_dense");
+    HS_CHECK(dupload(*ix, &ix->subdims, ds->subdims, K));
+    HS_CHECK(dupload(*ix, &ix->dim_off, doff.data(), K));
+    HS_CHECK(dupload(*ix, &ix->cen_off, coff.data(), K));
+    HS_CHECK(dupload(*ix, &ix->centers, ds->centers, csum));
+    if (ds->n_centers == 16) {
+      ix->pstride = ((n + 15) / 16) * 16 + 16;
+      HS_CHECK(dalloc(*ix, &ix->packed, (size_t)ix->npairs * ix->pstride));
+      HS_CUDA(cudaMemset(ix->packed, 0, (size_t)ix->npairs * ix->pstride));
+      if (n)
+        HS_CUDA(cudaMemcpy2D(ix->packed, ix->pstride, ds->packed, n, n, ix->npairs,
+                             cudaMemcpyHostToDevice));
+    }
+    ix->has_sq = ds->has_sq;
+    if (ds->has_sq) {
+      HS_CHECK(dupload(*ix, &ix->sq_lo, ds->sq_lo, ds->d_dense));
+      HS_CHECK(dupload(*ix, &ix->sq_step, ds->sq_step, ds->d_dense));
+      HS_CHECK(dupload(*ix, &ix->sq_codes, ds->sq_codes, (size_t)n * ds->d_dense));
+    }
+    ix->has_wh = ds->has_whitening;
+    if (ds->has_whitening) {
+      HS_CHECK(dupload(*ix, &ix->wh_mean, ds->wh_mean, ds->d_dense));
+      HS_CHECK(dupload(*ix, &ix->wh_inv_t, ds->wh_inverse_t, (size_t)ds->d_dense * ds->d_dense));
+    }
+  }
+  // raw dataset
+  ix->has_ds = ds->has_dataset;
+  if (ds->has_dataset) {
+    if (ds->d_dense > 0) HS_CHECK(dupload(*ix, &ix->ds_dense, ds->ds_dense, (size_t)n * ds->d_dense));
+    ix->ds_nnz = n ? ds->ds_indptr[n] - ds->ds_indptr[0] : 0;
+    HS_CHECK(dupload(*ix, &ix->ds_indptr, ds->ds_indptr, n + 1));
+    HS_CHECK(dupload(*ix, &ix->ds_indices, ds->ds_indices, ix->ds_nnz));
+    HS_CHECK(dupload(*ix, &ix->ds_data, ds->ds_data, ix->ds_nnz));
+  }
+  HS_CUDA(cudaDeviceSynchronize());
+  *out = ix.release();
+  return HS_OK;
+}
+
+void hs_index_destroy(hs_index_t index) { hs::free_index(index); }
+
+int hs_index_memory_bytes(hs_index_t index, int64_t* bytes) {
+  if (!index || !bytes) HS_FAIL(HS_EINVAL, "null argument");
+  *bytes = index->bytes;
+  return HS_OK;
+}
+
+int hs_result_sizes(hs_index_t index, const hs_search_params* p, int64_t counts[3]) {
+  if (!index) HS_FAIL(HS_EINVAL, "null index");
+  Sizes s;
+  HS_CHECK(resolve_sizes(*index, p, &s));
+  counts[0] = s.k1;
+  counts[1] = s.k2;
+  counts[2] = s.kh;
+  return HS_OK;
+}
+
+int hs_search_batch(hs_index_t index, const hs_query_batch* queries,
+                    const hs_search_params* params, int64_t* out_ids, double* out_scores,
+                    double* stage_seconds) {
+  if (!index) HS_FAIL(HS_EINVAL, "null index");
+  std::lock_guard<std::mutex> lock(index->mu);
+  HS_CUDA(cudaSetDevice(index->device));
+  Sizes sz;
+  HS_CHECK(resolve_sizes(*index, params, &sz));
+  DevQueries dq;
+  HS_CHECK(upload_queries(*index, queries, &dq, true));
+  const int64_t nq = queries->nq;
+  const int64_t total = nq * sz.kh;
+  int64_t* d_ids = nullptr;
+  double* d_sc = nullptr;
+  HS_CUDA(cudaMalloc(&d_ids, sizeof(int64_t) * std::max<int64_t>(total, 1)));
+  HS_CUDA(cudaMalloc(&d_sc, sizeof(double) * std::max<int64_t>(total, 1)));
+  Timer tm(index, index->stream, index->timing);
+  int rc = run_search(*index, dq.b, dq.nnz, dq.max_row, params, d_ids, d_sc, index->stream, &tm,
+                      true);
+  if (rc == HS_OK && total) {
+    cudaMemcpyAsync(out_ids, d_ids, sizeof(int64_t) * total, cudaMemcpyDeviceToHost, index->stream);
+    cudaMemcpyAsync(out_scores, d_sc, sizeof(double) * total, cudaMemcpyDeviceToHost,
+                    index->stream);
+  }
+  cudaError_t e = cudaStreamSynchronize(index->stream);
+  tm.finish(stage_seconds);
+  cudaFree(d_ids);
+  cudaFree(d_sc);
+  if (rc != HS_OK) return rc;
+  if (e != cudaSuccess) HS_FAIL(HS_ECUDA, std::string("CUDA error: ") + cudaGetErrorString(e));
+  return HS_OK;
+}
+
+int hs_search_batch_dev(hs_index_t index, const hs_query_batch* queries,
+                        const hs_search_params* params, int64_t* d_out_ids,
+                        double* d_out_scores, void* stream) {
+  if (!index || !queries) HS_FAIL(HS_EINVAL, "null argument");
+  std::lock_guard<std::mutex> lock(index->mu);
+  HS_CUDA(cudaSetDevice(index->device));
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : index->stream;
+  int64_t nnz = 0;
+  int max_row = 0;
+  HS_CHECK(derive_hints(*index, queries, &nnz, &max_row, st));
+  return run_search(*index, *queries, nnz, max_row, params, d_out_ids, d_out_scores, st, nullptr);
+}
+
+int hs_adc_table(const float* centers, const int32_t* subdims, int32_t K, int32_t l,
+                 const double* qw, int64_t nq, int64_t d, double* T) {
+  if (K <= 0 || l <= 0 || nq < 0) HS_FAIL(HS_EINVAL, "bad shape");
+  std::vector<int32_t> doff(K), coff(K);
+  int64_t ds = 0, cs = 0;
+  for (int k = 0; k < K; ++k) {
+    doff[k] = (int32_t)ds;
+    coff[k] = (int32_t)cs;
+    ds += subdims[k];
+    cs += (int64_t)subdims[k] * l;
+  }
+  if (ds != d) HS_FAIL(HS_EINVAL, "query dense dimension mismatch");
+  DeviceIndex tmp;
+  float* dc;
+  int32_t *dsd, *ddo, *dco;
+  double *dq, *dT;
+  HS_CHECK(dupload(tmp, &dc, centers, cs));
+  HS_CHECK(dupload(tmp, &dsd, subdims, K));
+  HS_CHECK(dupload(tmp, &ddo, doff.data(), K));
+  HS_CHECK(dupload(tmp, &dco, coff.data(), K));
+  HS_CHECK(dupload(tmp, &dq, qw, nq * d));
+  HS_CHECK(dalloc(tmp, &dT, nq * K * l));
+  launch_adc_table(dc, dsd, ddo, dco, K, l, dq, nq, d, dT, 0);
+  HS_CUDA(cudaGetLastError());
+  HS_CUDA(cudaMemcpy(T, dT, sizeof(double) * nq * K * l, cudaMemcpyDeviceToHost));
+  cudaFree(dc); cudaFree(dsd); cudaFree(ddo); cudaFree(dco); cudaFree(dq); cudaFree(dT);
+  return HS_OK;
+}
+
+int hs_quantize_lut(const double* T, int64_t nq, int32_t K, int32_t l, uint8_t* table,
+                    double* bias, double* scale, double* bias_total) {
+  if (K < 0 || l <= 0 || nq < 0) HS_FAIL(HS_EINVAL, "bad shape");
+  if (nq == 0) return HS_OK;
+  DeviceIndex tmp;
+  double *dT, *db, *ds, *dbt;
+  uint8_t* dt;
+  int* dbad;
+  HS_CHECK(dupload(tmp, &dT, T, nq * K * l));
+  HS_CHECK(dalloc(tmp, &dt, nq * K * l + 1));
+  HS_CHECK(dalloc(tmp, &db, nq * K + 1));
+  HS_CHECK(dalloc(tmp, &ds, nq));
+  HS_CHECK(dalloc(tmp, &dbt, nq));
+  HS_CHECK(dalloc(tmp, &dbad, nq));
+  HS_CUDA(cudaMemset(dbad, 0, sizeof(int) * nq));
+  launch_quantize(dT, nq, K, l, K, dt, db, ds, dbt, dbad, 0);
+  HS_CUDA(cudaGetLastError());
+  std::vector<int> hbad(nq);
+  HS_CUDA(cudaMemcpy(hbad.data(), dbad, sizeof(int) * nq, cudaMemcpyDeviceToHost));
+  if (K * l) HS_CUDA(cudaMemcpy(table, dt, nq * K * l, cudaMemcpyDeviceToHost));
+  if (K) HS_CUDA(cudaMemcpy(bias, db, sizeof(double) * nq * K, cudaMemcpyDeviceToHost));
+  HS_CUDA(cudaMemcpy(scale, ds, sizeof(double) * nq, cudaMemcpyDeviceToHost));
+  HS_CUDA(cudaMemcpy(bias_total, dbt, sizeof(double) * nq, cudaMemcpyDeviceToHost));
+  cudaFree(dT); cudaFree(dt); cudaFree(db); cudaFree(ds); cudaFree(dbt); cudaFree(dbad);
+  for (int64_t i = 0; i < nq; ++i)
+    if (hbad[i]) HS_FAIL(HS_EINVAL, "lookup table contains non-finite values");
+  return HS_OK;
+}
+
+int hs_lut16_scan(const uint8_t* packed, int64_t n, int32_t K, const uint8_t* qtable,
+                  const double* bias_total, const double* scale, int64_t nq, int32_t* totals,
+                  double* scores) {
+  if (K <= 0 || n < 0 || nq < 0) HS_FAIL(HS_EINVAL, "bad shape");
+  if (n == 0 || nq == 0) return HS_OK;
+  // a dense-only temporary index view over the caller's codes
+  hs_index_desc dsc;
+  std::memset(&dsc, 0, sizeof(dsc));
+  std::vector<int64_t> order(n);
+  for (int64_t i = 0; i < n; ++i) order[i] = i;
+  std::vector<int32_t> sub(K, 1);
+  std::vector<float> cen((size_t)K * 16, 0.f);
+  int64_t zero_ptr = 0;
+  dsc.n = n;
+  dsc.d_sparse = 0;
+  dsc.d_dense = K;
+  dsc.order = order.data();
+  dsc.n_active = 0;
+  dsc.post_ptr = &zero_ptr;
+  dsc.n_subspaces = K;
+  dsc.n_centers = 16;
+  dsc.subdims = sub.data();
+  dsc.centers = cen.data();
+  dsc.packed = packed;
+  dsc.sparse_weight = 1.0;
+  dsc.dense_weight = 1.0;
+  int dev = 0;
+  HS_CUDA(cudaGetDevice(&dev));
+  hs_index_t ix = nullptr;
+  HS_CHECK(hs_index_create(&dsc, dev, &ix));
+  std::unique_ptr<hs_index, void (*)(hs_index*)> guard(ix, [](hs_index* p) { hs::free_index(p); });
+  const int Kp = ix->Kp;
+  // padded LUTs [nq][Kp][16]
+  std::vector<uint8_t> lp((size_t)nq * Kp * 16, 0);
+  for (int64_t q = 0; q < nq; ++q)
+    std::memcpy(&lp[(size_t)q * Kp * 16], qtable + (size_t)q * K * 16, (size_t)K * 16);
+  DeviceIndex tmp;
+  uint8_t* dl;
+  double *dbt, *dsc2, *dout;
+  uint32_t* dtot;
+  int64_t* dptr;
+  HS_CHECK(dupload(tmp, &dl, lp.data(), lp.size()));
+  HS_CHECK(dupload(tmp, &dbt, bias_total, nq));
+  HS_CHECK(dupload(tmp, &dsc2, scale, nq));
+  HS_CHECK(dalloc(tmp, &dout, nq * n));
+  HS_CHECK(dalloc(tmp, &dtot, nq * n));
+  std::vector<int64_t> qp(nq + 1, 0);
+  HS_CHECK(dupload(tmp, &dptr, qp.data(), nq + 1));
+  QueryView qv;
+  qv.nq = nq;
+  qv.sp_indptr = dptr;
+  Stage1Plan p = plan_stage1(*ix, nq, 1, 1, S1_DUMP);
+  HS_CHECK(launch_stage1(*ix, qv, p, nullptr, nullptr, nullptr, dl, dbt, dsc2, nullptr, nullptr,
+                         dout, ix->stream, dtot, true));
+  HS_CUDA(cudaStreamSynchronize(ix->stream));
+  HS_CUDA(cudaMemcpy(scores, dout, sizeof(double) * nq * n, cudaMemcpyDeviceToHost));
+  HS_CUDA(cudaMemcpy(totals, dtot, sizeof(uint32_t) * nq * n, cudaMemcpyDeviceToHost));
+  cudaFree(dl); cudaFree(dbt); cudaFree(dsc2); cudaFree(dout); cudaFree(dtot); cudaFree(dptr);
+  return HS_OK;
+}
+
+static int stage1_dump(hs_index_t index, const hs_query_batch* queries, double* out, bool raw_acc) {
+  if (!index) HS_FAIL(HS_EINVAL, "null index");
+  std::lock_guard<std::mutex> lock(index->mu);
+  HS_CUDA(cudaSetDevice(index->device));
+  DevQueries dq;
+  HS_CHECK(upload_queries(*index, queries, &dq, true));
+  const int64_t nq = queries->nq, n = index->n, d = index->d_dense;
+  if (nq == 0 || n == 0) return HS_OK;
+  if (!raw_acc && d > 0 && index->l != 16)
+    HS_FAIL(HS_EUNSUPPORTED, "lut16_scan requires 16-center codes");
+  DeviceIndex tmp;
+  uint32_t *lb, *le;
+  double *qv, *qd, *qw, *bt, *sc, *of, *dump;
+  uint8_t* luts;
+  int* bad;
+  HS_CHECK(dalloc(tmp, &lb, dq.nnz + 1));
+  HS_CHECK(dalloc(tmp, &le, dq.nnz + 1));
+  HS_CHECK(dalloc(tmp, &qv, dq.nnz + 1));
+  HS_CHECK(dalloc(tmp, &qd, nq * d + 1));
+  HS_CHECK(dalloc(tmp, &qw, nq * d + 1));
+  HS_CHECK(dalloc(tmp, &luts, nq * index->Kp * 16 + 16));
+  HS_CHECK(dalloc(tmp, &bt, nq));
+  HS_CHECK(dalloc(tmp, &sc, nq));
+  HS_CHECK(dalloc(tmp, &of, nq));
+  HS_CHECK(dalloc(tmp, &bad, nq));
+  HS_CHECK(dalloc(tmp, &dump, nq * n));
+  HS_CUDA(cudaMemsetAsync(bad, 0, sizeof(int) * nq, index->stream));
+  QueryView qvw;
+  qvw.nq = nq;
+  qvw.sp_indptr = dq.b.sp_indptr;
+  qvw.sp_dims = dq.b.sp_dims;
+  qvw.sp_vals = dq.b.sp_vals;
+  qvw.dense = dq.b.dense;
+  launch_map_dims(*index, qvw, dq.nnz, !raw_acc, lb, le, qv, index->stream);
+  if (!raw_acc && d > 0)
+    launch_lut_build(*index, qvw.dense, nq, qd, qw, luts, bt, sc, of, bad, index->stream);
+  Stage1Plan p = plan_stage1(*index, nq, 1, dq.max_row, S1_DUMP);
+  p.sparse_only_acc = raw_acc;
+  HS_CHECK(launch_stage1(*index, qvw, p, lb, le, qv, luts, bt, sc, of, nullptr, dump,
+                         index->stream));
+  HS_CUDA(cudaStreamSynchronize(index->stream));
+  std::vector<int> hbad(nq);
+  HS_CUDA(cudaMemcpy(hbad.data(), bad, sizeof(int) * nq, cudaMemcpyDeviceToHost));
+  HS_CUDA(cudaMemcpy(out, dump, sizeof(double) * nq * n, cudaMemcpyDeviceToHost));
+  cudaFree(lb); cudaFree(le); cudaFree(qv); cudaFree(qd); cudaFree(qw); cudaFree(luts);
+  cudaFree(bt); cudaFree(sc); cudaFree(of); cudaFree(bad); cudaFree(dump);
+  for (int64_t i = 0; i < nq; ++i)
+    if (hbad[i]) HS_FAIL(HS_EINVAL, "lookup table contains non-finite values");
+  return HS_OK;
+}
+
+int hs_sparse_scan(hs_index_t index, const hs_query_batch* queries, double* acc) {
+  return stage1_dump(index, queries, acc, true);
+}
+
+int hs_stage1_scores(hs_index_t index, const hs_query_batch* queries, double* scores) {
+  return stage1_dump(index, queries, scores, false);
+}
+
+int hs_select_topk(const double* scores, int64_t nq, int64_t n, int64_t k,
+                   const int64_t* tie_ids, int64_t* out) {
+  if (nq < 0 || n < 0) HS_FAIL(HS_EINVAL, "bad shape");
+  k = std::min(k, n);
+  if (k <= 0 || nq == 0) return HS_OK;
+  if (tie_ids)
+    for (int64_t i = 0; i < n; ++i)
+      if (tie_ids[i] < 0 || tie_ids[i] >= (int64_t)0xFFFFFFFFLL)
+        HS_FAIL(HS_EUNSUPPORTED, "tie ids must lie in [0, 2^32-1)");
+  DeviceIndex tmp;
+  double* ds;
+  int64_t *dt = nullptr, *dout;
+  Cand *c, *co;
+  HS_CHECK(dupload(tmp, &ds, scores, nq * n));
+  if (tie_ids) HS_CHECK(dupload(tmp, &dt, tie_ids, n));
+  HS_CHECK(dalloc(tmp, &c, nq * n));
+  HS_CHECK(dalloc(tmp, &co, nq * k));
+  HS_CHECK(dalloc(tmp, &dout, nq * k));
+  launch_scores_to_cands(ds, dt, nq, n, c, 0);
+  HS_CHECK(launch_select_topk(c, nq, n, k, co, 0));
+  launch_cands_to_positions(co, nq, k, dout, 0);
+  HS_CUDA(cudaGetLastError());
+  HS_CUDA(cudaMemcpy(out, dout, sizeof(int64_t) * nq * k, cudaMemcpyDeviceToHost));
+  cudaFree(ds); if (dt) cudaFree(dt); cudaFree(c); cudaFree(co); cudaFree(dout);
+  return HS_OK;
+}
+
+int hs_exact_topk(hs_index_t index, const hs_query_batch* queries, int32_t h, int64_t* out_ids,
+                  double* out_scores) {
+  if (!index) HS_FAIL(HS_EINVAL, "null index");
+  if (!index->has_ds) HS_FAIL(HS_EINVAL, "exact scoring requires the original dataset");
+  if (h < 1) HS_FAIL(HS_EINVAL, "h must be >= 1");
+  std::lock_guard<std::mutex> lock(index->mu);
+  HS_CUDA(cudaSetDevice(index->device));
+  DevQueries dq;
+  HS_CHECK(upload_queries(*index, queries, &dq, true));
+  const int64_t nq = queries->nq, n = index->n, d = index->d_dense;
+  const int64_t kh = std::min<int64_t>(h, n);
+  if (nq == 0 || kh == 0) return HS_OK;
+  // chunk queries so the per-point candidate array stays below ~2 GB
+  int64_t QB = std::max<int64_t>(1, std::min<int64_t>(nq, (int64_t)(2.0e9 / (16.0 * n))));
+  DeviceIndex tmp;
+  Cand *all, *top;
+  double* qd;
+  int64_t* dids;
+  double* dsc;
+  HS_CHECK(dalloc(tmp, &all, QB * n));
+  HS_CHECK(dalloc(tmp, &top, QB * kh));
+  HS_CHECK(dalloc(tmp, &qd, nq * d + 1));
+  HS_CHECK(dalloc(tmp, &dids, nq * kh));
+  HS_CHECK(dalloc(tmp, &dsc, nq * kh));
+  cudaStream_t st = index->stream;
+  if (d > 0) launch_query_qd(dq.b.dense, nq, d, index->dense_weight, qd, st);
+  for (int64_t q0 = 0; q0 < nq; q0 += QB) {
+    const int64_t nqc = std::min(QB, nq - q0);
+    QueryView qc;
+    qc.nq = nqc;
+    qc.sp_indptr = dq.b.sp_indptr + q0;
+    qc.sp_dims = dq.b.sp_dims;
+    qc.sp_vals = dq.b.sp_vals;
+    launch_exact_scores(*index, qc, dq.max_row, qd + q0 * d, all, st);
+    HS_CHECK(launch_select_topk(all, nqc, n, kh, top, st));
+    launch_cands_to_ids(top, nqc * kh, index->id_offset, dids + q0 * kh, dsc + q0 * kh, st);
+  }
+  HS_CUDA(cudaStreamSynchronize(st));
+  HS_CUDA(cudaMemcpy(out_ids, dids, sizeof(int64_t) * nq * kh, cudaMemcpyDeviceToHost));
+  HS_CUDA(cudaMemcpy(out_scores, dsc, sizeof(double) * nq * kh, cudaMemcpyDeviceToHost));
+  cudaFree(all); cudaFree(top); cudaFree(qd); cudaFree(dids); cudaFree(dsc);
+  return HS_OK;
+}
+
+int hs_shard_merge_dev(const int64_t* d_ids, const double* d_scores, int64_t G, int64_t nq,
+                       int64_t kh, int32_t h, int64_t* d_out_ids, double* d_out_scores,
+                       void* stream) {
+  if (G <= 0 || nq < 0 || kh < 0 || h < 1) HS_FAIL(HS_EINVAL, "bad shape");
+  if (G * kh > 8192) HS_FAIL(HS_EUNSUPPORTED, "G*kh above 8192");
+  launch_shard_merge(d_ids, d_scores, G, nq, kh, h, d_out_ids, d_out_scores,
+                     static_cast<cudaStream_t>(stream));
+  HS_CUDA(cudaGetLastError());
+  return HS_OK;
+}
+
+int hs_last_kernel_times(hs_index_t index, double* ms, int32_t max_entries, int32_t* n_entries,
+                         char* names, int32_t names_cap) {
+  if (!index) HS_FAIL(HS_EINVAL, "null index");
+  const int32_t n = (int32_t)std::min<size_t>(index->tms.size(), (size_t)max_entries);
+  std::string joined;
+  for (int32_t i = 0; i < n; ++i) {
+    ms[i] = index->tms[i];
+    if (i) joined += ";";
+    joined += index->tnames[i];
+  }
+  *n_entries = n;
+  if (names && names_cap > 0) {
+    std::strncpy(names, joined.c_str(), names_cap - 1);
+    names[names_cap - 1] = 0;
+  }
+  return HS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,137 @@
+// kernels.cuh — device index layout and the kernel launchers shared by the
+// translation units of libhsb200.so.
+#pragma once
+
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+namespace hs {
+
+// Immutable device copy of one hybrid index (the C-ABI handle).
+struct DeviceIndex {
+  int device = 0;
+  int64_t n = 0, d_sparse = 0, d_dense = 0, id_offset = 0;
+  double sparse_weight = 1.0, dense_weight = 1.0;
+
+  uint32_t* order = nullptr;  // [n] slot -> original id (u32)
+
+  // pruned scan index: interleaved (id, w-bits) postings, CSR over active dims
+  int64_t n_active = 0, nnz_post = 0;
+  uint32_t* post_dims = nullptr;  // [n_active]
+  uint32_t* post_ptr = nullptr;   // [n_active+1] (nnz_post < 2^32)
+  uint2* post = nullptr;          // [nnz_post] {id, __float_as_uint(w)}
+
+  // forward sparse residual (layout order)
+  int64_t res_nnz = 0;
+  int64_t* res_indptr = nullptr;
+  uint32_t* res_indices = nullptr;
+  float* res_data = nullptr;
+
+  // dense PQ part
+  int K = 0, l = 0, Kp = 0, npairs = 0, max_width = 0;
+  int32_t* subdims = nullptr;  // [K]
+  int32_t* dim_off = nullptr;  // [K] first dense dim of subspace k
+  int32_t* cen_off = nullptr;  // [K] offset of centers[k] in `centers`
+  float* centers = nullptr;
+  uint8_t* packed = nullptr;  // [npairs][pstride]
+  int64_t pstride = 0;
+  int has_sq = 0;
+  float *sq_lo = nullptr, *sq_step = nullptr;
+  uint8_t* sq_codes = nullptr;  // [n][d_dense]
+  int has_wh = 0;
+  double *wh_mean = nullptr, *wh_inv_t = nullptr;
+
+  // raw dataset (original order) for exact rerank / ground truth
+  int has_ds = 0;
+  float* ds_dense = nullptr;
+  int64_t* ds_indptr = nullptr;
+  uint32_t* ds_indices = nullptr;
+  float* ds_data = nullptr;
+  int64_t ds_nnz = 0;
+
+  int64_t bytes = 0;
+  cudaStream_t stream = nullptr;
+  std::mutex mu;
+
+  // scratch arena (grown on demand, owned by the handle)
+  void* scratch = nullptr;
+  size_t scratch_bytes = 0;
+
+  // per-kernel timing of the last batch (CUDA events; bench roofline)
+  bool timing = true;
+  std::vector<std::string> tnames;
+  std::vector<double> tms;
+};
+
+// ---- per-batch device views of a query chunk ----
+struct QueryView {
+  int64_t nq = 0;
+  const int64_t* sp_indptr = nullptr;  // device [nq+1], absolute offsets
+  const uint32_t* sp_dims = nullptr;
+  const float* sp_vals = nullptr;
+  const float* dense = nullptr;  // [nq][d]
+};
+
+// lut.cu
+void launch_lut_build(const DeviceIndex& ix, const float* qdense, int64_t nq, double* qd_out,
+                      double* qw_out, uint8_t* luts, double* bias_total, double* scale,
+                      double* offset, int* bad, cudaStream_t st);
+void launch_adc_table(const float* centers, const int32_t* subdims, const int32_t* dim_off,
+                      const int32_t* cen_off, int K, int l, const double* qw, int64_t nq,
+                      int64_t d, double* T, cudaStream_t st);
+void launch_quantize(const double* T, int64_t nq, int K, int l, int Kp, uint8_t* table,
+                     double* bias, double* scale, double* bias_total, int* bad,
+                     cudaStream_t st);
+
+// stage1.cu
+enum Stage1Mode { S1_SELECT = 0, S1_EMIT_ALL = 1, S1_DUMP = 2 };
+struct Stage1Plan {
+  int mode = S1_SELECT;
+  int ntiles = 1;
+  int64_t tile_pts = 0;   // multiple of the chunk size
+  int k = 0;              // per-tile keep (SELECT)
+  int cap = 0;            // candidate buffer entries (pow2, >= k + chunk)
+  int64_t out_per_tile = 0;
+  int max_qnnz = 0;
+  bool use_dense = true;  // DUMP: include the dense part
+  bool sparse_only_acc = false;  // DUMP: raw accumulator (no weights, no dense)
+};
+int stage1_chunk_points();
+Stage1Plan plan_stage1(const DeviceIndex& ix, int64_t nq, int64_t k, int max_qnnz, int mode);
+size_t stage1_smem_bytes(const DeviceIndex& ix, const Stage1Plan& p);
+void launch_map_dims(const DeviceIndex& ix, const QueryView& q, int64_t nnz, bool use_weight,
+                     uint32_t* lbeg, uint32_t* lend, double* qv, cudaStream_t st);
+int launch_stage1(const DeviceIndex& ix, const QueryView& q, const Stage1Plan& p,
+                  const uint32_t* lbeg, const uint32_t* lend, const double* qv,
+                  const uint8_t* luts, const double* bias_total, const double* scale,
+                  const double* offset, Cand* out, double* dump, cudaStream_t st,
+                  uint32_t* dump_tot = nullptr, bool raw_dense = false);
+
+// select.cu
+int launch_select_topk(const Cand* in, int64_t nq, int64_t m, int64_t k, Cand* out,
+                       cudaStream_t st);
+void launch_scores_to_cands(const double* scores, const int64_t* tie_ids, int64_t nq,
+                            int64_t n, Cand* out, cudaStream_t st);
+void launch_cands_to_positions(const Cand* c, int64_t nq, int64_t k, int64_t* out,
+                               cudaStream_t st);
+void launch_shard_merge(const int64_t* ids, const double* scores, int64_t G, int64_t nq,
+                        int64_t kh, int h, int64_t* out_ids, double* out_scores,
+                        cudaStream_t st);
+
+// rerank.cu
+void launch_stage2(const DeviceIndex& ix, const Cand* cand1, int64_t nq, int k1, int k2,
+                   const double* qw, Cand* cand2, cudaStream_t st);
+void launch_stage3(const DeviceIndex& ix, const QueryView& q, const Cand* cand2, int64_t nq,
+                   int k2, int kh, int exact, int max_qnnz, const double* qd, int64_t* out_ids,
+                   double* out_scores, cudaStream_t st);
+void launch_query_qd(const float* qdense, int64_t nq, int64_t d, double w, double* qd,
+                     cudaStream_t st);
+void launch_exact_scores(const DeviceIndex& ix, const QueryView& q, int max_qnnz,
+                         const double* qd, Cand* out, cudaStream_t st);
+void launch_cands_to_ids(const Cand* c, int64_t total, int64_t id_offset, int64_t* ids,
+                         double* scores, cudaStream_t st);
+
+}  // namespace hs

@@ -1,0 +1,184 @@
+// select.cu — K4 top-k selection and K7 shard merge.
+//
+// Exact top-k by (score desc, tie id asc), the ordering of select_topk
+// (reference pipeline.py:165-189).  Candidates are 16-byte {score, tie, slot}
+// entries.  One CTA per query sorts up to kCap entries in shared memory with
+// a bitonic network; longer inputs are streamed through the same buffer
+// (keep the best k, refill, re-sort).  Inputs with k > kCap/2 fall back to a
+// global-memory bitonic sort (only reachable from exhaustive test settings).
+#include "kernels.cuh"
+
+namespace hs {
+
+namespace {
+
+constexpr int kSelThreads = 512;
+constexpr int kCap = 8192;  // 128 KB of candidates in shared memory
+
+__global__ void __launch_bounds__(kSelThreads) k_select_smem(const Cand* __restrict__ in,
+                                                             int64_t m, int k,
+                                                             Cand* __restrict__ out) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Cand* buf = reinterpret_cast<Cand*>(smem_raw);
+  const int64_t q = blockIdx.x;
+  const Cand* src = in + q * m;
+  int have = 0;
+  int64_t pos = 0;
+  do {
+    const int64_t take = min((int64_t)(kCap - have), m - pos);
+    const int tot = have + (int)take;
+    int P = 1;
+    while (P < tot) P <<= 1;
+    for (int i = threadIdx.x; i < P - have; i += blockDim.x)
+      buf[have + i] = (i < take) ? src[pos + i] : worst_cand();
+    __syncthreads();
+    bitonic_sort_block(buf, P);
+    pos += take;
+    have = tot < k ? tot : k;
+  } while (pos < m);
+  for (int i = threadIdx.x; i < k; i += blockDim.x) out[q * k + i] = i < have ? buf[i] : worst_cand();
+}
+
+__global__ void k_pad_copy(const Cand* __restrict__ in, int64_t m, int64_t P, int64_t nq,
+                           Cand* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nq * P) return;
+  const int64_t q = i / P, j = i % P;
+  out[i] = j < m ? in[q * m + j] : worst_cand();
+}
+
+__global__ void k_bitonic_step(Cand* a, int64_t P, int64_t nq, int64_t kk, int64_t jj) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t half = P >> 1;
+  if (t >= nq * half) return;
+  const int64_t q = t / half, i = t % half;
+  const int64_t lo = ((i & ~(jj - 1)) << 1) | (i & (jj - 1));
+  const int64_t hi = lo + jj;
+  Cand* s = a + q * P;
+  const bool up = (lo & kk) == 0;
+  Cand x = s[lo], y = s[hi];
+  if (up ? better(y, x) : better(x, y)) {
+    s[lo] = y;
+    s[hi] = x;
+  }
+}
+
+__global__ void k_take_prefix(const Cand* __restrict__ a, int64_t P, int64_t nq, int64_t k,
+                              Cand* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nq * k) return;
+  out[i] = a[(i / k) * P + (i % k)];
+}
+
+__global__ void k_scores_to_cands(const double* __restrict__ s, const int64_t* __restrict__ tie,
+                                  int64_t nq, int64_t n, Cand* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nq * n) return;
+  const int64_t j = i % n;
+  Cand c;
+  c.s = s[i];
+  c.tie = tie ? (uint32_t)tie[j] : (uint32_t)j;
+  c.slot = (uint32_t)j;
+  out[i] = c;
+}
+
+__global__ void k_cands_to_positions(const Cand* __restrict__ c, int64_t total,
+                                     int64_t* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < total) out[i] = (int64_t)c[i].slot;
+}
+
+// K7: per query, best h of the G*kh gathered (id, score) pairs by
+// (score desc, id asc).  Shards own disjoint id ranges, so ids are unique.
+__global__ void __launch_bounds__(kSelThreads) k_shard_merge(
+    const int64_t* __restrict__ ids, const double* __restrict__ scores, int64_t G, int64_t nq,
+    int64_t kh, int h, int64_t* __restrict__ out_ids, double* __restrict__ out_scores) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Cand* buf = reinterpret_cast<Cand*>(smem_raw);
+  const int64_t q = blockIdx.x;
+  const int64_t m = G * kh;
+  int P = 1;
+  while (P < m) P <<= 1;
+  for (int64_t i = threadIdx.x; i < P; i += blockDim.x) {
+    Cand c = worst_cand();
+    if (i < m) {
+      const int64_t g = i / kh, j = i % kh;
+      const int64_t src = (g * nq + q) * kh + j;
+      const int64_t id = ids[src];
+      if (id >= 0) {
+        c.s = scores[src];
+        c.tie = (uint32_t)id;
+        c.slot = (uint32_t)i;
+      }
+    }
+    buf[i] = c;
+  }
+  __syncthreads();
+  bitonic_sort_block(buf, P);
+  for (int i = threadIdx.x; i < h; i += blockDim.x) {
+    const Cand c = buf[i];
+    const bool ok = c.slot != 0xFFFFFFFFu;
+    int64_t id = -1;
+    if (ok) {
+      const int64_t g = c.slot / kh, j = c.slot % kh;
+      id = ids[(g * nq + q) * kh + j];
+    }
+    out_ids[q * h + i] = id;
+    out_scores[q * h + i] = ok ? c.s : -INFINITY;
+  }
+}
+
+}  // namespace
+
+int launch_select_topk(const Cand* in, int64_t nq, int64_t m, int64_t k, Cand* out,
+                       cudaStream_t st) {
+  if (nq <= 0 || k <= 0) return HS_OK;
+  if (k <= kCap / 2) {
+    const size_t smem = sizeof(Cand) * kCap;
+    HS_CUDA(cudaFuncSetAttribute(k_select_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem));
+    k_select_smem<<<(unsigned)nq, kSelThreads, smem, st>>>(in, m, (int)k, out);
+    HS_CUDA(cudaGetLastError());
+    return HS_OK;
+  }
+  // global bitonic fallback
+  const int64_t P = next_pow2(m);
+  Cand* tmp = nullptr;
+  HS_CUDA(cudaMallocAsync(&tmp, sizeof(Cand) * nq * P, st));
+  const int T = 256;
+  k_pad_copy<<<(unsigned)ceil_div(nq * P, T), T, 0, st>>>(in, m, P, nq, tmp);
+  for (int64_t kk = 2; kk <= P; kk <<= 1)
+    for (int64_t jj = kk >> 1; jj > 0; jj >>= 1)
+      k_bitonic_step<<<(unsigned)ceil_div(nq * (P >> 1), T), T, 0, st>>>(tmp, P, nq, kk, jj);
+  k_take_prefix<<<(unsigned)ceil_div(nq * k, T), T, 0, st>>>(tmp, P, nq, k, out);
+  HS_CUDA(cudaFreeAsync(tmp, st));
+  HS_CUDA(cudaGetLastError());
+  return HS_OK;
+}
+
+void launch_scores_to_cands(const double* scores, const int64_t* tie_ids, int64_t nq, int64_t n,
+                            Cand* out, cudaStream_t st) {
+  if (nq * n <= 0) return;
+  const int T = 256;
+  k_scores_to_cands<<<(unsigned)ceil_div(nq * n, T), T, 0, st>>>(scores, tie_ids, nq, n, out);
+}
+
+void launch_cands_to_positions(const Cand* c, int64_t nq, int64_t k, int64_t* out,
+                               cudaStream_t st) {
+  if (nq * k <= 0) return;
+  const int T = 256;
+  k_cands_to_positions<<<(unsigned)ceil_div(nq * k, T), T, 0, st>>>(c, nq * k, out);
+}
+
+void launch_shard_merge(const int64_t* ids, const double* scores, int64_t G, int64_t nq,
+                        int64_t kh, int h, int64_t* out_ids, double* out_scores,
+                        cudaStream_t st) {
+  if (nq <= 0) return;
+  const int64_t P = next_pow2(G * kh);
+  const size_t smem = sizeof(Cand) * P;
+  cudaFuncSetAttribute(k_shard_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_shard_merge<<<(unsigned)nq, kSelThreads, smem, st>>>(ids, scores, G, nq, kh, h, out_ids,
+                                                          out_scores);
+}
+
+}  // namespace hs

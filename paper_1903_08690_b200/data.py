@@ -1,0 +1,5 @@
+"""Import-path alias for `hybridsearch.data` users (reference data.py)."""
+from .types import (  # noqa: F401
+    BadMagicError, BadVersionError, FormatError, HybridDataset, HybridVector, SparseVector,
+    TruncatedFileError,
+)

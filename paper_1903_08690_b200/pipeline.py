@@ -1,0 +1,4 @@
+"""Import-path alias for `hybridsearch.pipeline` users (reference pipeline.py)."""
+from .builder import build_index  # noqa: F401
+from .search import search_batch, search_topk, select_topk, stage1_scores  # noqa: F401
+from .types import HybridIndex, HybridIndexConfig, SearchResult, StageStats  # noqa: F401
