@@ -159,6 +159,7 @@ int run_search(DeviceIndex& ix, const hs_query_batch& qb, int64_t nnz, int max_q
   HS_CHECK(resolve_sizes(ix, params, &sz));
   const int64_t nq = qb.nq;
   if (nq <= 0 || sz.kh <= 0) return HS_OK;
+  if (ix.d_dense > 0 && ix.K == 0) HS_FAIL(HS_EINVAL, "index has no dense PQ codes");
   if (ix.d_dense > 0 && ix.l != 16) HS_FAIL(HS_EUNSUPPORTED, "lut16_scan requires 16-center codes");
   if (params->exact_final_rerank && !ix.has_ds)
     HS_FAIL(HS_EINVAL, "exact_final_rerank requires the original dataset");
@@ -425,9 +426,8 @@ int hs_index_create(const hs_index_desc* ds, int device, hs_index_t* out) {
     HS_CHECK(dupload(*ix, &ix->res_data, ds->res_data, ix->res_nnz));
   }
   // dense
-  if (ds->d_dense > 0) {
+  if (ds->d_dense > 0 && ds->n_subspaces > 0) {
     const int K = ds->n_subspaces;
-    if (K <= 0) HS_FAIL(HS_EINVAL, "dense part without subspaces");
     ix->K = K;
     ix->l = ds->n_centers;
     ix->Kp = (K + 1) & ~1;
@@ -671,6 +671,7 @@ static int stage1_dump(hs_index_t index, const hs_query_batch* queries, double* 
   HS_CHECK(upload_queries(*index, queries, &dq, true));
   const int64_t nq = queries->nq, n = index->n, d = index->d_dense;
   if (nq == 0 || n == 0) return HS_OK;
+  if (!raw_acc && d > 0 && index->K == 0) HS_FAIL(HS_EINVAL, "index has no dense PQ codes");
   if (!raw_acc && d > 0 && index->l != 16)
     HS_FAIL(HS_EUNSUPPORTED, "lut16_scan requires 16-center codes");
   DeviceIndex tmp;

@@ -170,7 +170,7 @@ __global__ void __launch_bounds__(kThreads) k_stage1(Stage1Args a) {
   if (a.has_dense) {
     btot = a.bias_total[q];
     scl = a.scale[q];
-    off = a.offset[q];
+    off = a.offset ? a.offset[q] : 0.0;
   }
   __syncthreads();
 
