@@ -166,6 +166,12 @@ int hs_shard_merge_dev(const int64_t* d_ids, const double* d_scores, int64_t G,
                        int64_t nq, int64_t kh, int32_t h, int64_t* d_out_ids,
                        double* d_out_scores, void* stream);
 
+/* Per-kernel CUDA-event timing of search calls (on by default for the host
+ * entry point; enables it for the _dev entry point too, which then syncs). */
+int hs_set_timing(hs_index_t index, int on);
+/* Cumulative number of kernels this index's search calls have launched. */
+int hs_index_launches(hs_index_t index, int64_t* launches);
+
 /* Timing of the last search on this index: per-kernel CUDA-event averages
  * (used by bench.py for the roofline). names joined by ';'. */
 int hs_last_kernel_times(hs_index_t index, double* ms, int32_t max_entries,

@@ -74,7 +74,7 @@ def build_cuda(verbose=False, force=False):
 def build_host(force=False):
     src = os.path.join(CSRC, "hostbuild.cpp")
     if force or _stale(LIB_HOST, [src]):
-        _run(["g++", "-O3", "-march=x86-64-v2", "-fopenmp", "-fPIC", "-shared", "-std=c++17",
+        _run(["g++", "-O3", "-march=x86-64-v3", "-ffp-contract=off", "-fopenmp", "-fPIC", "-shared", "-std=c++17",
               "-o", LIB_HOST, src])
     return LIB_HOST
 

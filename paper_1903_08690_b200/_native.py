@@ -81,6 +81,8 @@ def lib():
         L.hs_select_topk.argtypes = [P, i64, i64, i64, P, P]
         L.hs_exact_topk.argtypes = [P, ctypes.POINTER(QueryBatch), i32, P, P]
         L.hs_shard_merge_dev.argtypes = [P, P, i64, i64, i64, i32, P, P, P]
+        L.hs_set_timing.argtypes = [P, ctypes.c_int]
+        L.hs_index_launches.argtypes = [P, ctypes.POINTER(i64)]
         L.hs_last_kernel_times.argtypes = [P, P, i32, ctypes.POINTER(i32), ctypes.c_char_p, i32]
         _LIB = L
     return _LIB

@@ -60,6 +60,14 @@ def _hostlib():
         lib.hsb_gen_hybrid.argtypes = [i64, i64, i64, ctypes.c_double, ctypes.c_double,
                                        ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64,
                                        ctypes.c_int, P, P, P, P]
+        lib.hsb_top_t_thresholds_csr.argtypes = [i64, i64, P, P, P, i64, P]
+        lib.hsb_prune_split.argtypes = [i64, P, P, P, P, P, P, P, P, P, P, P]
+        lib.hsb_rank_rows.argtypes = [i64, P, P, P, P]
+        lib.hsb_inverted_counts.argtypes = [i64, i64, P, P, P, P]
+        lib.hsb_inverted_fill.argtypes = [i64, i64, P, P, P, P, P, P, P]
+        lib.hsb_pq_encode.argtypes = [i64, i64, P, ctypes.c_int32, P, P, ctypes.c_int32, P]
+        lib.hsb_sq_residual.argtypes = [i64, i64, P, P, P, ctypes.c_int32, P, P, ctypes.c_int32,
+                                        P, P, P]
         _HOST = lib
     return _HOST
 
@@ -81,12 +89,22 @@ def top_t_thresholds(csc: sp.csc_matrix, t: int) -> np.ndarray:
     return eta
 
 
+def _csr_parts(m):
+    return (np.ascontiguousarray(m.indptr, dtype=np.int64),
+            np.ascontiguousarray(m.indices, dtype=np.int32),
+            np.ascontiguousarray(m.data, dtype=np.float32))
+
+
 def resolve_thresholds(th: PruneThresholds, matrix: sp.spmatrix):
     d = matrix.shape[1]
     if th.data_min is not None:
         eta = np.broadcast_to(np.asarray(th.data_min, dtype=np.float64), (d,)).copy()
     else:
-        eta = top_t_thresholds(matrix.tocsc(), th.top_t)
+        m = sp.csr_matrix(matrix)
+        ip, ix, dt = _csr_parts(m)
+        eta = np.zeros(d, dtype=np.float64)
+        _hostlib().hsb_top_t_thresholds_csr(m.shape[0], d, _ptr(ip), _ptr(ix), _ptr(dt),
+                                            int(th.top_t), _ptr(eta))
     eps = np.broadcast_to(np.asarray(th.residual_min, dtype=np.float64), (d,)).copy()
     if np.any(eps > eta):
         raise ValueError("residual_min must be <= data_min in every dimension")
@@ -101,14 +119,31 @@ def _mask_csr(m: sp.csr_matrix, keep: np.ndarray) -> sp.csr_matrix:
     return sp.csr_matrix((m.data[keep], m.indices[keep], indptr), shape=m.shape)
 
 
-def prune_split(matrix, thresholds: PruneThresholds):
+def prune_split(matrix, thresholds: PruneThresholds, with_discarded: bool = True):
     """(data, residual, discarded) entry-disjoint CSR parts (sparse.py:83-103)."""
     m = sp.csr_matrix(matrix)
     eta, eps = resolve_thresholds(thresholds, m)
-    a = np.abs(m.data.astype(np.float64))
-    in_data = a >= eta[m.indices]
-    in_res = ~in_data & (a >= eps[m.indices])
-    return _mask_csr(m, in_data), _mask_csr(m, in_res), _mask_csr(m, ~in_data & ~in_res)
+    n = m.shape[0]
+    ip, ix, dt = _csr_parts(m)
+    dptr = np.zeros(n + 1, dtype=np.int64)
+    rptr = np.zeros(n + 1, dtype=np.int64)
+    L = _hostlib()
+    L.hsb_prune_split(n, _ptr(ip), _ptr(ix), _ptr(dt), _ptr(eta), _ptr(eps), _ptr(dptr), None,
+                      None, _ptr(rptr), None, None)
+    di = np.empty(max(int(dptr[-1]), 1), dtype=np.int32)
+    dd = np.empty(max(int(dptr[-1]), 1), dtype=np.float32)
+    ri = np.empty(max(int(rptr[-1]), 1), dtype=np.int32)
+    rd = np.empty(max(int(rptr[-1]), 1), dtype=np.float32)
+    L.hsb_prune_split(n, _ptr(ip), _ptr(ix), _ptr(dt), _ptr(eta), _ptr(eps), _ptr(dptr), _ptr(di),
+                      _ptr(dd), _ptr(rptr), _ptr(ri), _ptr(rd))
+    data_part = sp.csr_matrix((dd[:dptr[-1]], di[:dptr[-1]], dptr), shape=m.shape)
+    res_part = sp.csr_matrix((rd[:rptr[-1]], ri[:rptr[-1]], rptr), shape=m.shape)
+    disc = None
+    if with_discarded:
+        a = np.abs(m.data.astype(np.float64))
+        in_data = a >= eta[m.indices]
+        disc = _mask_csr(m, ~in_data & ~(a >= eps[m.indices]))
+    return data_part, res_part, disc
 
 
 def cache_sort(matrix) -> np.ndarray:
@@ -116,17 +151,15 @@ def cache_sort(matrix) -> np.ndarray:
     m = sp.csr_matrix(matrix)
     n, d = m.shape
     nnz = np.bincount(m.indices, minlength=d)
-    ranked = np.lexsort((np.arange(d), -nnz))
+    ranked = np.argsort(-nnz, kind="stable")  # nnz desc, ties to the lower dim
     ranked = ranked[nnz[ranked] > 0]
     if n == 0 or len(ranked) == 0:
         return np.arange(n, dtype=np.int64)
-    rank_of = np.full(d, -1, dtype=np.int64)
-    rank_of[ranked] = np.arange(len(ranked))
-    r = rank_of[m.indices].astype(np.int32)
-    rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(m.indptr))
-    o = np.lexsort((r, rows))  # each row's ranks ascending
-    r = np.ascontiguousarray(r[o])
-    indptr = np.ascontiguousarray(m.indptr, dtype=np.int64)
+    rank_of = np.full(d, -1, dtype=np.int32)
+    rank_of[ranked] = np.arange(len(ranked), dtype=np.int32)
+    indptr, ix, _ = _csr_parts(m)
+    r = np.empty(max(len(ix), 1), dtype=np.int32)
+    _hostlib().hsb_rank_rows(n, _ptr(indptr), _ptr(ix), _ptr(rank_of), _ptr(r))
     order = np.empty(n, dtype=np.int64)
     _hostlib().hsb_cache_sort(n, _ptr(indptr), _ptr(r), _ptr(order))
     return order
@@ -138,17 +171,20 @@ def build_inverted(matrix, order) -> InvertedIndex:
     n, d = m.shape
     order = np.asarray(order, dtype=np.int64)
     pos = invert_permutation(order)
-    rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(m.indptr))
-    keep = m.data != 0
-    cols = m.indices[keep].astype(np.int64)
-    pids = pos[rows[keep]]
-    w = m.data[keep]
-    o = np.lexsort((pids, cols))
-    cols, pids, w = cols[o], pids[o], w[o]
-    dims, counts = np.unique(cols, return_counts=True)
-    ptr = np.concatenate(([0], np.cumsum(counts))).astype(np.int64)
-    return InvertedIndex(n, d, order, dims=dims.astype(np.int64), ptr=ptr,
-                         ids=pids.astype(np.uint32), w=w.astype(np.float32))
+    ip, ix, dt = _csr_parts(m)
+    L = _hostlib()
+    counts = np.zeros(d, dtype=np.int64)
+    L.hsb_inverted_counts(n, d, _ptr(ip), _ptr(ix), _ptr(dt), _ptr(counts))
+    colptr = np.zeros(d + 1, dtype=np.int64)
+    np.cumsum(counts, out=colptr[1:])
+    nnz = int(colptr[-1])
+    ids = np.empty(max(nnz, 1), dtype=np.uint32)
+    w = np.empty(max(nnz, 1), dtype=np.float32)
+    L.hsb_inverted_fill(n, d, _ptr(ip), _ptr(ix), _ptr(dt), _ptr(pos), _ptr(colptr), _ptr(ids),
+                        _ptr(w))
+    dims = np.flatnonzero(counts).astype(np.int64)
+    ptr = np.concatenate((colptr[dims], [nnz])).astype(np.int64)
+    return InvertedIndex(n, d, order, dims=dims, ptr=ptr, ids=ids[:nnz], w=w[:nnz])
 
 
 # ----------------------------------------------------------------------------
@@ -181,12 +217,21 @@ def _sqdist(x, sq, c):
 
 
 def _kmeans(x, k, iters, rng):
+    """Lloyd iterations with farthest-point repair (dense.py:84-105).
+
+    Same arithmetic as the reference; two exact shortcuts: each iteration's
+    objective reuses the next iteration's argmin (min == value at argmin), and
+    cluster members are gathered through one stable argsort instead of k
+    boolean masks (same rows, same ascending order).
+    """
     c = _seed_centers(x, k, rng)
     sq = np.sum(x ** 2, axis=1)
     hist = []
+    rows = np.arange(x.shape[0])
     d2 = _sqdist(x, sq, c)
+    a_next = np.argmin(d2, axis=1)
     for _ in range(iters):
-        a = np.argmin(d2, axis=1)
+        a = a_next
         cnt = np.bincount(a, minlength=k)
         for e in np.flatnonzero(cnt == 0):  # farthest-point repair
             big = int(np.argmax(cnt))
@@ -195,11 +240,14 @@ def _kmeans(x, k, iters, rng):
             a[far] = e
             cnt[big] -= 1
             cnt[e] = 1
+        grp = np.argsort(a, kind="stable")
+        ends = np.cumsum(cnt)
         for j in range(k):
             if cnt[j]:
-                c[j] = x[a == j].mean(axis=0)
+                c[j] = x[grp[ends[j] - cnt[j]:ends[j]]].mean(axis=0)
         d2 = _sqdist(x, sq, c)
-        hist.append(float(np.maximum(d2.min(axis=1), 0.0).mean()))
+        a_next = np.argmin(d2, axis=1)
+        hist.append(float(np.maximum(d2[rows, a_next], 0.0).mean()))
     return c, np.asarray(hist)
 
 
@@ -216,13 +264,28 @@ def train_codebooks(dense, n_subspaces, n_centers=LUT16_CENTERS, n_iters=25, see
         rs = np.random.default_rng(seqs[0])
         x = x[np.sort(rs.choice(n, size=sample, replace=False))]
     edges = np.concatenate(([0], np.cumsum(widths)))
-    centers, hist = [], []
-    for k in range(n_subspaces):
-        c, h = _kmeans(x[:, edges[k]:edges[k + 1]], n_centers, n_iters,
+
+    def one(k):
+        # each subspace owns its RNG stream, so the pool order cannot change results
+        c, h = _kmeans(np.ascontiguousarray(x[:, edges[k]:edges[k + 1]]), n_centers, n_iters,
                        np.random.default_rng(seqs[1 + k]))
-        centers.append(c.astype(np.float32))
-        hist.append(h)
-    return Codebooks(subdims=widths, centers=centers, objective_history=hist)
+        return c.astype(np.float32), h
+
+    res = _pool_map(one, range(n_subspaces))
+    return Codebooks(subdims=widths, centers=[r[0] for r in res],
+                     objective_history=[r[1] for r in res])
+
+
+def _pool_map(fn, items):
+    """Thread pool over independent per-subspace work (numpy releases the GIL)."""
+    items = list(items)
+    workers = min(len(items), os.cpu_count() or 1)
+    if workers <= 1:
+        return [fn(i) for i in items]
+    from concurrent.futures import ThreadPoolExecutor
+
+    with ThreadPoolExecutor(max_workers=workers) as ex:
+        return list(ex.map(fn, items))
 
 
 def pq_encode(dense, codebooks: Codebooks) -> np.ndarray:
@@ -231,12 +294,25 @@ def pq_encode(dense, codebooks: Codebooks) -> np.ndarray:
     if x.shape[1] != codebooks.d_dense:
         raise ValueError("dense dimension mismatch with codebooks")
     out = np.empty((x.shape[0], codebooks.n_subspaces), dtype=np.uint8)
-    for k, sl in enumerate(codebooks.slices()):
-        sub = x[:, sl]
+    if int(np.max(codebooks.subdims)) <= 2:
+        xc = np.ascontiguousarray(x)
+        sub = np.ascontiguousarray(codebooks.subdims, dtype=np.int64)
+        cen = np.ascontiguousarray(np.concatenate([c.reshape(-1) for c in codebooks.centers]),
+                                   dtype=np.float32)
+        rc = _hostlib().hsb_pq_encode(xc.shape[0], xc.shape[1], _ptr(xc), codebooks.n_subspaces,
+                                      _ptr(sub), _ptr(cen), codebooks.n_centers, _ptr(out))
+        if rc == 0:
+            return out
+    slices = codebooks.slices()
+
+    def one(k):
+        sub = x[:, slices[k]]
         c = codebooks.centers[k].astype(np.float64)
         d2 = (np.sum(sub ** 2, axis=1)[:, None] - 2.0 * (sub @ c.T)
               + np.sum(c ** 2, axis=1)[None, :])
         out[:, k] = np.argmin(d2, axis=1)
+
+    _pool_map(one, range(codebooks.n_subspaces))
     return out
 
 
@@ -297,6 +373,23 @@ def sq_encode(dense) -> ScalarQuantResidual:
     return ScalarQuantResidual(lo=lo.astype(np.float32), step=step.astype(np.float32), codes=codes)
 
 
+def sq_residual(vec, order, codes, cb: Codebooks) -> ScalarQuantResidual:
+    """sq_encode(vec[order] - reconstruct(codes)) without the n x d temporaries."""
+    x = np.ascontiguousarray(vec, dtype=np.float64)
+    n, d = x.shape
+    lo = np.empty(d, dtype=np.float32)
+    step = np.empty(d, dtype=np.float32)
+    q = np.empty((n, d), dtype=np.uint8)
+    sub = np.ascontiguousarray(cb.subdims, dtype=np.int64)
+    cen = np.ascontiguousarray(np.concatenate([c.reshape(-1) for c in cb.centers]),
+                               dtype=np.float32)
+    _hostlib().hsb_sq_residual(n, d, _ptr(x), _ptr(np.ascontiguousarray(order, dtype=np.int64)),
+                               _ptr(np.ascontiguousarray(codes, dtype=np.uint8)),
+                               cb.n_subspaces, _ptr(sub), _ptr(cen), cb.n_centers, _ptr(lo),
+                               _ptr(step), _ptr(q))
+    return ScalarQuantResidual(lo=lo, step=step, codes=q)
+
+
 # ----------------------------------------------------------------------------
 # build_index
 # ----------------------------------------------------------------------------
@@ -304,7 +397,8 @@ def build_index(dataset: HybridDataset, config: HybridIndexConfig | None = None,
                 keep_dataset: bool = True, order_fn=None) -> HybridIndex:
     """Full hybrid index; deterministic for a fixed config seed (pipeline.py:119-162)."""
     config = config or HybridIndexConfig()
-    data_part, residual_part, _ = prune_split(dataset.sparse, config.prune_thresholds())
+    data_part, residual_part, _ = prune_split(dataset.sparse, config.prune_thresholds(),
+                                              with_discarded=False)
     order = np.asarray((order_fn or cache_sort)(data_part), dtype=np.int64)
     if order.shape != (dataset.n,) or not np.array_equal(np.sort(order), np.arange(dataset.n)):
         raise ValueError("layout ordering is not a permutation of [0, n)")
@@ -322,11 +416,8 @@ def build_index(dataset: HybridDataset, config: HybridIndexConfig | None = None,
         cb = train_codebooks(vec, K, n_centers=config.pq_centers, n_iters=config.kmeans_iters,
                              seed=config.seed, sample=config.train_sample)
         codes = pq_encode(vec, cb)[order]
-        vo = vec[order]
-        del vec
-        resid = vo - cb.reconstruct(codes)
         dense_index = DenseIndex(codebooks=cb, codes=PQCodes.from_codes(codes, config.pq_centers),
-                                 residual=sq_encode(resid), whitening=wt)
+                                 residual=sq_residual(vec, order, codes, cb), whitening=wt)
     return HybridIndex(config=config, n=dataset.n, d_sparse=dataset.d_sparse,
                        d_dense=dataset.d_dense, order=order, sparse_index=sidx,
                        sparse_residual=res, dense_index=dense_index,

@@ -225,6 +225,7 @@ int run_search(DeviceIndex& ix, const hs_query_batch& qb, int64_t nnz, int max_q
   all.sp_vals = qb.sp_vals;
   all.dense = qb.dense;
   launch_map_dims(ix, all, nnz, true, lbeg, lend, qv, st);
+  ix.launches += nnz > 0 ? 1 : 0;
   if (tm) tm->mark("map_dims");
   if (d > 0) HS_CUDA(cudaMemsetAsync(bad, 0, sizeof(int) * QB, st));
 
@@ -244,6 +245,7 @@ int run_search(DeviceIndex& ix, const hs_query_batch& qb, int64_t nnz, int max_q
     } else if (params->exact_final_rerank) {
       // no dense part: qd unused
     }
+    ix.launches += (d > 0 ? 1 : 0) + 4;  // lut_build, stage1, merge, stage2, stage3
     HS_CHECK(launch_stage1(ix, qc, pc, lbeg, lend, qv, luts, btot, scl, off, s1out, nullptr, st));
     if (tm) tm->mark("stage1");
     HS_CHECK(launch_select_topk(s1out, nqc, (int64_t)pc.ntiles * pc.out_per_tile, sz.k1, cand1, st));
@@ -541,7 +543,26 @@ int hs_search_batch_dev(hs_index_t index, const hs_query_batch* queries,
   int64_t nnz = 0;
   int max_row = 0;
   HS_CHECK(derive_hints(*index, queries, &nnz, &max_row, st));
-  return run_search(*index, *queries, nnz, max_row, params, d_out_ids, d_out_scores, st, nullptr);
+  if (!index->timing_dev)
+    return run_search(*index, *queries, nnz, max_row, params, d_out_ids, d_out_scores, st,
+                      nullptr);
+  Timer tm(index, st, true);
+  const int rc =
+      run_search(*index, *queries, nnz, max_row, params, d_out_ids, d_out_scores, st, &tm);
+  tm.finish(nullptr);
+  return rc;
+}
+
+int hs_set_timing(hs_index_t index, int on) {
+  if (!index) HS_FAIL(HS_EINVAL, "null index");
+  index->timing_dev = on != 0;
+  return HS_OK;
+}
+
+int hs_index_launches(hs_index_t index, int64_t* launches) {
+  if (!index || !launches) HS_FAIL(HS_EINVAL, "null argument");
+  *launches = index->launches;
+  return HS_OK;
 }
 
 int hs_adc_table(const float* centers, const int32_t* subdims, int32_t K, int32_t l,

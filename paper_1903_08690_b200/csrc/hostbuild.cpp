@@ -259,6 +259,266 @@ int hsb_top_t_thresholds(int64_t d, const int64_t* indptr, const float* data, in
   return 0;
 }
 
+
+// ---------------------------------------------------------------------------
+// prune_split (sparse.py:83-103): per-column thresholds from a CSR matrix and
+// the three-way split.  Thresholds: eta[j] = t-th largest |v| in column j
+// when nnz_j > t (np.partition semantics), 0 otherwise; t == 0 -> +inf.
+// ---------------------------------------------------------------------------
+int hsb_top_t_thresholds_csr(int64_t n, int64_t d, const int64_t* indptr,
+                             const int32_t* indices, const float* data, int64_t t,
+                             double* eta) {
+  if (t == 0) {
+    for (int64_t j = 0; j < d; ++j) eta[j] = INFINITY;
+    return 0;
+  }
+  std::vector<int64_t> cnt(d + 1, 0);
+  const int64_t nnz = indptr[n];
+  for (int64_t e = 0; e < nnz; ++e) cnt[indices[e] + 1]++;
+  for (int64_t j = 0; j < d; ++j) cnt[j + 1] += cnt[j];
+  std::vector<float> vals(nnz);
+  std::vector<int64_t> cur(cnt.begin(), cnt.end() - 1);
+  for (int64_t e = 0; e < nnz; ++e) vals[cur[indices[e]]++] = std::fabs(data[e]);
+#pragma omp parallel for schedule(dynamic, 4096)
+  for (int64_t j = 0; j < d; ++j) {
+    const int64_t lo = cnt[j], m = cnt[j + 1] - lo;
+    if (m <= t) {
+      eta[j] = 0.0;
+      continue;
+    }
+    std::nth_element(vals.begin() + lo, vals.begin() + lo + (m - t), vals.begin() + lo + m);
+    eta[j] = (double)vals[lo + (m - t)];
+  }
+  return 0;
+}
+
+// Two-call protocol: with d_indices == NULL fills d_indptr / r_indptr
+// (cumulative); then fills both parts.  Entries with v == 0 are dropped
+// (eliminate_zeros, sparse.py:99-101).
+int hsb_prune_split(int64_t n, const int64_t* indptr, const int32_t* indices, const float* data,
+                    const double* eta, const double* eps, int64_t* d_indptr, int32_t* d_indices,
+                    float* d_data, int64_t* r_indptr, int32_t* r_indices, float* r_data) {
+  auto cls = [&](int64_t e) -> int {  // 0 data, 1 residual, 2 discard
+    const float v = data[e];
+    if (v == 0.0f) return 2;
+    const double a = std::fabs((double)v);
+    const int32_t j = indices[e];
+    if (a >= eta[j]) return 0;
+    if (a >= eps[j]) return 1;
+    return 2;
+  };
+  if (!d_indices) {
+    d_indptr[0] = 0;
+    r_indptr[0] = 0;
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < n; ++i) {
+      int64_t a = 0, b = 0;
+      for (int64_t e = indptr[i]; e < indptr[i + 1]; ++e) {
+        const int c = cls(e);
+        a += c == 0;
+        b += c == 1;
+      }
+      d_indptr[i + 1] = a;
+      r_indptr[i + 1] = b;
+    }
+    for (int64_t i = 0; i < n; ++i) {
+      d_indptr[i + 1] += d_indptr[i];
+      r_indptr[i + 1] += r_indptr[i];
+    }
+    return 0;
+  }
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < n; ++i) {
+    int64_t a = d_indptr[i], b = r_indptr[i];
+    for (int64_t e = indptr[i]; e < indptr[i + 1]; ++e) {
+      const int c = cls(e);
+      if (c == 0) {
+        d_indices[a] = indices[e];
+        d_data[a++] = data[e];
+      } else if (c == 1) {
+        r_indices[b] = indices[e];
+        r_data[b++] = data[e];
+      }
+    }
+  }
+  return 0;
+}
+
+// Per-row ascending ranks (rank_of maps dim -> rank) for cache_sort.
+int hsb_rank_rows(int64_t n, const int64_t* indptr, const int32_t* indices,
+                  const int32_t* rank_of, int32_t* ranks) {
+#pragma omp parallel for schedule(dynamic, 4096)
+  for (int64_t i = 0; i < n; ++i) {
+    for (int64_t e = indptr[i]; e < indptr[i + 1]; ++e) ranks[e] = rank_of[indices[e]];
+    std::sort(ranks + indptr[i], ranks + indptr[i + 1]);
+  }
+  return 0;
+}
+
+// build_inverted (sparse.py:219-235): counts per column, then fill the
+// posting lists (slot ids ascending within each list).
+int hsb_inverted_counts(int64_t n, int64_t d, const int64_t* indptr, const int32_t* indices,
+                        const float* data, int64_t* counts) {
+  for (int64_t j = 0; j < d; ++j) counts[j] = 0;
+  const int64_t nnz = indptr[n];
+  for (int64_t e = 0; e < nnz; ++e)
+    if (data[e] != 0.0f) counts[indices[e]]++;
+  return 0;
+}
+
+int hsb_inverted_fill(int64_t n, int64_t d, const int64_t* indptr, const int32_t* indices,
+                      const float* data, const int64_t* pos, const int64_t* colptr,
+                      uint32_t* ids, float* w) {
+  std::vector<int64_t> cur(colptr, colptr + d);
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t e = indptr[i]; e < indptr[i + 1]; ++e) {
+      if (data[e] == 0.0f) continue;
+      const int64_t at = cur[indices[e]]++;
+      ids[at] = (uint32_t)pos[i];
+      w[at] = data[e];
+    }
+#pragma omp parallel
+  {
+    std::vector<std::pair<uint32_t, float>> tmp;
+#pragma omp for schedule(dynamic, 4096)
+    for (int64_t j = 0; j < d; ++j) {
+      const int64_t lo = colptr[j], hi = colptr[j + 1];
+      if (hi - lo < 2) continue;
+      tmp.resize(hi - lo);
+      for (int64_t k = lo; k < hi; ++k) tmp[k - lo] = {ids[k], w[k]};
+      std::sort(tmp.begin(), tmp.end(),
+                [](const std::pair<uint32_t, float>& a, const std::pair<uint32_t, float>& b) {
+                  return a.first < b.first;
+                });
+      for (int64_t k = lo; k < hi; ++k) {
+        ids[k] = tmp[k - lo].first;
+        w[k] = tmp[k - lo].second;
+      }
+    }
+  }
+  return 0;
+}
+
+// pq_encode (dense.py:138-153) for subspaces of width <= 2, reproducing
+// numpy's arithmetic: |x|^2 summed from 0, the 2-wide BLAS product
+// fma(x1, c1, x0*c0), d2 = (|x|^2 - 2*dot) + |c|^2, first minimum wins.
+// Returns 1 if a subspace is wider than 2 (caller falls back).
+int hsb_pq_encode(int64_t n, int64_t d, const double* x, int32_t K, const int64_t* subdims,
+                  const float* centers, int32_t l, uint8_t* codes) {
+  std::vector<int64_t> off(K), coff(K);
+  int64_t o = 0, co = 0;
+  for (int32_t k = 0; k < K; ++k) {
+    if (subdims[k] > 2 || subdims[k] < 1) return 1;
+    off[k] = o;
+    coff[k] = co;
+    o += subdims[k];
+    co += subdims[k] * l;
+  }
+  std::vector<double> csq((size_t)K * l);
+  for (int32_t k = 0; k < K; ++k)
+    for (int32_t c = 0; c < l; ++c) {
+      const float* cc = centers + coff[k] + (int64_t)c * subdims[k];
+      double s = 0.0;
+      for (int64_t t = 0; t < subdims[k]; ++t) {
+        const double v = (double)cc[t];
+        s = s + v * v;
+      }
+      csq[(size_t)k * l + c] = s;
+    }
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < n; ++i) {
+    const double* xi = x + i * d;
+    for (int32_t k = 0; k < K; ++k) {
+      const double* s = xi + off[k];
+      const float* cb = centers + coff[k];
+      int best = 0;
+      double bd = 0.0;
+      if (subdims[k] == 2) {
+        const double sq = (0.0 + s[0] * s[0]) + s[1] * s[1];
+        for (int32_t c = 0; c < l; ++c) {
+          const double c0 = cb[2 * c], c1 = cb[2 * c + 1];
+          const double dot = std::fma(s[1], c1, s[0] * c0);
+          const double d2 = (sq - 2.0 * dot) + csq[(size_t)k * l + c];
+          if (c == 0 || d2 < bd) {
+            bd = d2;
+            best = c;
+          }
+        }
+      } else {
+        const double sq = 0.0 + s[0] * s[0];
+        for (int32_t c = 0; c < l; ++c) {
+          const double dot = s[0] * (double)cb[c];
+          const double d2 = (sq - 2.0 * dot) + csq[(size_t)k * l + c];
+          if (c == 0 || d2 < bd) {
+            bd = d2;
+            best = c;
+          }
+        }
+      }
+      codes[i * K + k] = (uint8_t)best;
+    }
+  }
+  return 0;
+}
+
+// Scalar-quantised dense residual (pipeline.py:158-160, dense.py:381-390):
+// r = vec[order[i]] - center(code) in f64; per-dim lo/hi; step = (hi-lo)/256;
+// code = clip(floor((r - lo) / (step > 0 ? step : 1)), 0, 255).
+int hsb_sq_residual(int64_t n, int64_t d, const double* vec, const int64_t* order,
+                    const uint8_t* codes, int32_t K, const int64_t* subdims, const float* centers,
+                    int32_t l, float* lo_out, float* step_out, uint8_t* sq) {
+  std::vector<int64_t> dimk(d), dimt(d), coff(K);
+  int64_t o = 0, co = 0;
+  for (int32_t k = 0; k < K; ++k) {
+    coff[k] = co;
+    for (int64_t t = 0; t < subdims[k]; ++t) {
+      dimk[o] = k;
+      dimt[o] = t;
+      ++o;
+    }
+    co += subdims[k] * l;
+  }
+  auto resid = [&](int64_t i, int64_t j) -> double {
+    const int64_t k = dimk[j];
+    const int c = codes[i * K + k];
+    return vec[order[i] * d + j] - (double)centers[coff[k] + (int64_t)c * subdims[k] + dimt[j]];
+  };
+  std::vector<double> lo(d, INFINITY), hi(d, -INFINITY);
+#pragma omp parallel
+  {
+    std::vector<double> tlo(d, INFINITY), thi(d, -INFINITY);
+#pragma omp for schedule(static)
+    for (int64_t i = 0; i < n; ++i)
+      for (int64_t j = 0; j < d; ++j) {
+        const double r = resid(i, j);
+        if (r < tlo[j]) tlo[j] = r;
+        if (r > thi[j]) thi[j] = r;
+      }
+#pragma omp critical
+    for (int64_t j = 0; j < d; ++j) {
+      if (tlo[j] < lo[j]) lo[j] = tlo[j];
+      if (thi[j] > hi[j]) hi[j] = thi[j];
+    }
+  }
+  std::vector<double> step(d), safe(d);
+  for (int64_t j = 0; j < d; ++j) {
+    if (n == 0) lo[j] = hi[j] = 0.0;
+    step[j] = (hi[j] - lo[j]) / 256.0;
+    safe[j] = step[j] > 0 ? step[j] : 1.0;
+    lo_out[j] = (float)lo[j];
+    step_out[j] = (float)step[j];
+  }
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t j = 0; j < d; ++j) {
+      double q = std::floor((resid(i, j) - lo[j]) / safe[j]);
+      if (q < 0) q = 0;
+      if (q > 255) q = 255;
+      sq[i * d + j] = (uint8_t)q;
+    }
+  return 0;
+}
+
 int hsb_num_threads(void) {
 #ifdef _OPENMP
   return omp_get_max_threads();

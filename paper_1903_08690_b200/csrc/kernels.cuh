@@ -61,7 +61,9 @@ struct DeviceIndex {
   size_t scratch_bytes = 0;
 
   // per-kernel timing of the last batch (CUDA events; bench roofline)
-  bool timing = true;
+  bool timing = true;      // host entry point
+  bool timing_dev = false;  // _dev entry point (adds a sync)
+  int64_t launches = 0;
   std::vector<std::string> tnames;
   std::vector<double> tms;
 };

@@ -155,6 +155,21 @@ class DeviceIndex:
         keys = names.value.decode().split(";") if cnt.value else []
         return {k: float(ms[i]) for i, k in enumerate(keys)}
 
+    def set_timing(self, on: bool):
+        nat.check(nat.lib().hs_set_timing(self._h, int(bool(on))))
+
+    def launches(self) -> int:
+        v = ctypes.c_int64()
+        nat.check(nat.lib().hs_index_launches(self._h, ctypes.byref(v)))
+        return int(v.value)
+
+    def search_dev(self, qb, params, out_ids_ptr: int, out_scores_ptr: int, stream: int = 0):
+        """Device-resident batch: qb fields are device pointers (see hs_search_batch_dev)."""
+        nat.check(nat.lib().hs_search_batch_dev(self._h, ctypes.byref(qb), ctypes.byref(params),
+                                                ctypes.c_void_p(out_ids_ptr),
+                                                ctypes.c_void_p(out_scores_ptr),
+                                                ctypes.c_void_p(stream)))
+
     def close(self):
         if getattr(self, "_h", None) is not None and self._h.value:
             nat.lib().hs_index_destroy(self._h)
@@ -250,6 +265,11 @@ def _validate_queries(q: QueryArrays, d_sparse: int, d_dense: int):
 # ----------------------------------------------------------------------------
 # the hot path
 # ----------------------------------------------------------------------------
+def resolve_params(index, h=None, overfetch=None, retain=None, exact_final_rerank=None):
+    """hs_search_params for an index + overrides (validated like the reference)."""
+    return _resolve(index, h, overfetch, retain, exact_final_rerank)
+
+
 def _resolve(index, h, overfetch, retain, exact_final_rerank):
     cfg = index.config
     h = cfg.h if h is None else int(h)
