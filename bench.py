@@ -271,7 +271,9 @@ def main():
         m_ids = torch.empty((nq, h), dtype=torch.int64, device=dev)
         m_sc = torch.empty((nq, h), dtype=torch.float64, device=dev)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
-    stream = torch.cuda.current_stream(dev)
+    torch.cuda.synchronize()
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
 
     def step():
         dev_index.search_dev(qb, params, out_ids.data_ptr(), out_sc.data_ptr(),

@@ -133,7 +133,8 @@ int hs_search_batch(hs_index_t index, const hs_query_batch* queries,
                     double* out_scores, double* stage_seconds);
 
 /* Device-resident variant: every pointer in `queries` and the outputs are
- * device pointers; enqueued on `stream` (cudaStream_t), no host sync. */
+ * device pointers; enqueued on `stream` (cudaStream_t; NULL = the legacy
+ * default stream), no host sync.  sp_indptr[0] must be 0. */
 int hs_search_batch_dev(hs_index_t index, const hs_query_batch* queries,
                         const hs_search_params* params, int64_t* d_out_ids,
                         double* d_out_scores, void* stream);

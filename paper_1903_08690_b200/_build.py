@@ -15,8 +15,10 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 REPO = os.path.dirname(HERE)
-OBJ = os.path.join(REPO, "build", "obj")
-LIB_CUDA = os.path.join(HERE, "libhsb200.so")
+OBJ = os.path.join(REPO, "build", "obj_debug" if os.environ.get("HSB200_DEBUG", "") == "1"
+                   else "obj")
+DEBUG = os.environ.get("HSB200_DEBUG", "") == "1"
+LIB_CUDA = os.path.join(HERE, "libhsb200_debug.so" if DEBUG else "libhsb200.so")
 LIB_HOST = os.path.join(HERE, "libhsbuild.so")
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -25,6 +27,8 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 # reference rounds (explicit fma() calls are still fused).
 NVFLAGS = ["-O3", "-lineinfo", "-std=c++17", "--fmad=false", "-Xcompiler", "-fPIC",
            "-Xcompiler", "-O3", "-I", os.path.join(REPO, "include")]
+if DEBUG:
+    NVFLAGS += ["-DHS_DEBUG"]
 
 
 def _sources(ext):

@@ -52,7 +52,7 @@ void free_device_arrays(DeviceIndex* ix) {
   cudaSetDevice(ix->device);
   void* ptrs[] = {ix->order,    ix->post_dims,  ix->post_ptr, ix->post,       ix->res_indptr,
                   ix->res_indices, ix->res_data, ix->subdims,  ix->dim_off,    ix->cen_off,
-                  ix->centers,  ix->packed,     ix->sq_lo,    ix->sq_step,    ix->sq_codes,
+                  ix->centers,  ix->vcodes,     ix->sq_lo,    ix->sq_step,    ix->sq_codes,
                   ix->wh_mean,  ix->wh_inv_t,   ix->ds_dense, ix->ds_indptr,  ix->ds_indices,
                   ix->ds_data,  ix->scratch};
   for (void* p : ptrs)
@@ -448,13 +448,16 @@ int hs_index_create(const hs_index_desc* ds, int device, hs_index_t* out) {
     HS_CHECK(dupload(*ix, &ix->dim_off, doff.data(), K));
     HS_CHECK(dupload(*ix, &ix->cen_off, coff.data(), K));
     HS_CHECK(dupload(*ix, &ix->centers, ds->centers, csum));
-    if (ds->n_centers == 16) {
-      ix->pstride = ((n + 15) / 16) * 16 + 16;
-      HS_CHECK(dalloc(*ix, &ix->packed, (size_t)ix->npairs * ix->pstride));
-      HS_CUDA(cudaMemset(ix->packed, 0, (size_t)ix->npairs * ix->pstride));
-      if (n)
-        HS_CUDA(cudaMemcpy2D(ix->packed, ix->pstride, ds->packed, n, n, ix->npairs,
-                             cudaMemcpyHostToDevice));
+    if (ds->n_centers == 16 && ds->packed) {
+      // upload the reference pair-major layout, re-tile into vertical planes
+      ix->vstride = vertical_stride(n);
+      HS_CHECK(dalloc(*ix, &ix->vcodes, (size_t)K * ix->vstride));
+      uint8_t* tmp = nullptr;
+      HS_CUDA(cudaMalloc(&tmp, std::max<size_t>((size_t)ix->npairs * n, 1)));
+      if (n) HS_CUDA(cudaMemcpy(tmp, ds->packed, (size_t)ix->npairs * n, cudaMemcpyHostToDevice));
+      launch_to_vertical(tmp, n, K, ix->vstride, ix->vcodes, 0);
+      HS_CUDA(cudaDeviceSynchronize());
+      cudaFree(tmp);
     }
     ix->has_sq = ds->has_sq;
     if (ds->has_sq) {
@@ -539,7 +542,7 @@ int hs_search_batch_dev(hs_index_t index, const hs_query_batch* queries,
   if (!index || !queries) HS_FAIL(HS_EINVAL, "null argument");
   std::lock_guard<std::mutex> lock(index->mu);
   HS_CUDA(cudaSetDevice(index->device));
-  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : index->stream;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);  // NULL = legacy default stream
   int64_t nnz = 0;
   int max_row = 0;
   HS_CHECK(derive_hints(*index, queries, &nnz, &max_row, st));

@@ -47,6 +47,22 @@ struct Status {
 
 constexpr int kNumSMs = 148;
 
+// Device bounds checks for the debug build (HSB200_DEBUG=1 => -DHS_DEBUG).
+#ifdef HS_DEBUG
+#define HS_DCHECK(cond, ...)                                                       \
+  do {                                                                             \
+    if (!(cond)) {                                                                 \
+      printf("HS_DCHECK %s:%d (%s) block(%d,%d) thread %d\n", __FILE__, __LINE__,   \
+             #cond, blockIdx.x, blockIdx.y, threadIdx.x);                          \
+      __trap();                                                                    \
+    }                                                                              \
+  } while (0)
+#else
+#define HS_DCHECK(cond, ...) \
+  do {                       \
+  } while (0)
+#endif
+
 // --------------------------------------------------------------------------
 // candidate entries and the reference ordering (pipeline.py:165-189):
 // better = higher score, ties to the smaller tie id (original id).

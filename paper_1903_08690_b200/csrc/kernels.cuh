@@ -36,8 +36,8 @@ struct DeviceIndex {
   int32_t* dim_off = nullptr;  // [K] first dense dim of subspace k
   int32_t* cen_off = nullptr;  // [K] offset of centers[k] in `centers`
   float* centers = nullptr;
-  uint8_t* packed = nullptr;  // [npairs][pstride]
-  int64_t pstride = 0;
+  uint32_t* vcodes = nullptr;  // [K][vstride] vertical nibble planes (stage1.cu)
+  int64_t vstride = 0;
   int has_sq = 0;
   float *sq_lo = nullptr, *sq_step = nullptr;
   uint8_t* sq_codes = nullptr;  // [n][d_dense]
@@ -102,6 +102,9 @@ struct Stage1Plan {
   bool sparse_only_acc = false;  // DUMP: raw accumulator (no weights, no dense)
 };
 int stage1_chunk_points();
+int64_t vertical_stride(int64_t n);
+void launch_to_vertical(const uint8_t* packed, int64_t n, int K, int64_t vstride, uint32_t* v,
+                        cudaStream_t st);
 Stage1Plan plan_stage1(const DeviceIndex& ix, int64_t nq, int64_t k, int max_qnnz, int mode);
 size_t stage1_smem_bytes(const DeviceIndex& ix, const Stage1Plan& p);
 void launch_map_dims(const DeviceIndex& ix, const QueryView& q, int64_t nnz, bool use_weight,

@@ -8,20 +8,26 @@
 //   dense score   dense.py:317, pipeline.py:213   (bias_total + scale*total) + offset
 //   stage-1 score pipeline.py:202   acc + dense
 //
-// Grid: (tiles, queries).  A CTA owns a contiguous tile of layout slots and
-// walks it in chunks of kChunk points.  Per chunk it
-//   1. zeroes an f64 accumulator for the chunk in shared memory,
-//   2. finds, for every query dim, the slice of its posting list inside the
-//      chunk (cursor + galloping search on the ascending ids) and adds the
-//      slices dim by dim (ascending dim order per point => bit-exact f64),
-//   3. scans the pair-major packed codes for the chunk (one 8-byte load per
-//      pair row per thread = 8 points), summing u8 LUT entries in integers,
-//   4. forms the f64 stage-1 score with the reference's rounding order, and
-//   5. offers each point to a shared-memory candidate buffer guarded by the
-//      running k-th best (score desc, original id asc); overflow triggers an
-//      in-place bitonic compaction to the best k.
-// At the end the tile's best k are written out, best first, padded with
-// worst entries so the merge can treat every tile slot uniformly.
+// Grid: (queries, tiles) — the query index varies fastest so the CTAs that
+// are resident together stream the same tile of codes and share it in L2.
+// A CTA walks its tile of layout slots in chunks of kChunk points:
+//   1. dense: codes are stored "vertically" (re-tiled at upload): one u32 per
+//      (subspace, 8 points), nibble j = code of point j.  A thread owns 16
+//      points; per subspace it loads one uint2 and looks the 16 codes up in
+//      the 16-byte u8 table held in 4 registers with PRMT (the GPU analogue
+//      of the paper's in-register PSHUFB LUT16): two PRMTs
+//      select among entries 0-7 / 8-15 and a third builds the byte mask from
+//      the nibbles' bit 3.  Sums accumulate as 2 x u16 lanes per register
+//      (K*255 < 2^16 for K <= 257; wider K is flushed every 256 subspaces).
+//   2. sparse: every query dim keeps a cursor into its ascending posting list
+//      and the id it points at (`dnext`) in shared memory, so a chunk only
+//      touches the dims whose next posting falls inside it.  The active dims
+//      are compacted in ascending order and their slices added dim by dim
+//      into an f64 accumulator in shared memory (ascending dim order per
+//      point, starting from +0.0 => bit-exact with the reference).
+//   3. score = acc + ((bias_total + scale*total) + offset), unfused f64.
+//   4. offer to a shared-memory candidate buffer guarded by the running k-th
+//      best (score desc, original id asc); overflow => bitonic compaction.
 #include "kernels.cuh"
 
 namespace hs {
@@ -29,8 +35,9 @@ namespace hs {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kPPT = 8;                       // points per thread per chunk
-constexpr int kChunk = kThreads * kPPT;       // 2048 points
+constexpr int kPPT = 16;                   // points per thread per chunk
+constexpr int kChunk = kThreads * kPPT;    // 4096 points
+constexpr int kOfferRound = kThreads * 4;  // worst-case offers per insertion round
 
 struct Stage1Args {
   int64_t n;
@@ -47,9 +54,9 @@ struct Stage1Args {
   const double* qv;
   // dense
   int has_dense;
-  int npairs, Kp;
-  const uint8_t* packed;
-  int64_t pstride;
+  int K, Kp;
+  const uint32_t* vcodes;  // [K][vstride] u32, nibble j = point 8*word + j
+  int64_t vstride;
   const uint8_t* luts;
   const double* bias_total;
   const double* scale;
@@ -63,22 +70,41 @@ struct Stage1Args {
   int max_qnnz;
 };
 
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t s) {
+  uint32_t r;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(s));
+  return r;
+}
+
+// Eight 16-entry lookups.  w: nibble j = code of point j.  T: the u8 table
+// (entries 0..15 in bytes of T.x..T.w).  r0 = bytes for points 0-3, r1 = 4-7.
+__device__ __forceinline__ void lut8(const uint4& T, uint32_t w, uint32_t& r0, uint32_t& r1) {
+  const uint32_t x = w ^ 0x88888888u;             // entries 8..15 become selectors 0..7
+  const uint32_t a0 = prmt(T.x, T.y, w), a1 = prmt(T.x, T.y, w >> 16);
+  const uint32_t b0 = prmt(T.z, T.w, x), b1 = prmt(T.z, T.w, x >> 16);
+  const uint32_t m = w & 0x88888888u;
+  const uint32_t s = m | (m >> 3);                // nibble 9 where code >= 8, else 0
+  const uint32_t k0 = prmt(0x00008000u, 0u, s);   // sign-replicated 0x80 -> 0xFF
+  const uint32_t k1 = prmt(0x00008000u, 0u, s >> 16);
+  r0 = (b0 & k0) | (a0 & ~k0);
+  r1 = (b1 & k1) | (a1 & ~k1);
+}
+
 __device__ __forceinline__ uint32_t lower_bound_ids(const uint2* __restrict__ post, uint32_t lo,
                                                     uint32_t hi, uint32_t key) {
   while (lo < hi) {
     const uint32_t mid = lo + ((hi - lo) >> 1);
-    if (post[mid].x < key) lo = mid + 1;
+    if (__ldg(&post[mid].x) < key) lo = mid + 1;
     else hi = mid;
   }
   return lo;
 }
 
-// number of ids < key starting at cur (ids ascending), galloping
-__device__ __forceinline__ uint32_t count_below(const uint2* __restrict__ post, uint32_t cur,
-                                                uint32_t end, uint32_t key) {
-  if (cur >= end || post[cur].x >= key) return 0;
+// number of ids < key starting at cur, given post[cur].x < key (galloping)
+__device__ __forceinline__ uint32_t count_below_known(const uint2* __restrict__ post, uint32_t cur,
+                                                      uint32_t end, uint32_t key) {
   uint32_t prev = cur, step = 1;
-  while (prev + step < end && post[prev + step].x < key) {
+  while (prev + step < end && __ldg(&post[prev + step].x) < key) {
     prev += step;
     step <<= 1;
   }
@@ -87,15 +113,18 @@ __device__ __forceinline__ uint32_t count_below(const uint2* __restrict__ post, 
 }
 
 struct Smem {
-  uint8_t* lut;
+  Cand* buf;
+  Cand* th;
   double* acc;
+  uint4* lut;
   double* dqv;
   uint32_t* dcur;
   uint32_t* dend;
-  uint32_t* dcnt;
-  Cand* buf;
-  int* ctl;  // [0]=cnt [1]=need [2]=have_th
-  Cand* th;  // threshold entry
+  uint32_t* dnext;
+  uint32_t* alist;  // active dims of the chunk (ascending)
+  uint32_t* abase;  // their slice start
+  uint32_t* acnt;   // their slice length
+  int* ctl;         // [0]=cnt [2]=have_th [4..12]=warp sums
 };
 
 __device__ void compact(Smem& s, int k) {
@@ -116,11 +145,37 @@ __device__ void compact(Smem& s, int k) {
   __syncthreads();
 }
 
+__device__ __forceinline__ int block_sum(int v, int* scratch) {
+  // scratch: >= kThreads/32 ints; returns the block total to every thread
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) scratch[w] = v;
+  __syncthreads();
+  int t = 0;
+#pragma unroll
+  for (int i = 0; i < kThreads / 32; ++i) t += scratch[i];
+  __syncthreads();
+  return t;
+}
+
+__device__ __forceinline__ void accum16(uint32_t* acc2, uint32_t r0, uint32_t r1, uint32_t r2,
+                                        uint32_t r3) {
+  acc2[0] += r0 & 0x00FF00FFu;
+  acc2[1] += prmt(r0, 0u, 0x4341u);  // bytes 1,3 -> u16 lanes
+  acc2[2] += r1 & 0x00FF00FFu;
+  acc2[3] += prmt(r1, 0u, 0x4341u);
+  acc2[4] += r2 & 0x00FF00FFu;
+  acc2[5] += prmt(r2, 0u, 0x4341u);
+  acc2[6] += r3 & 0x00FF00FFu;
+  acc2[7] += prmt(r3, 0u, 0x4341u);
+}
+
 __global__ void __launch_bounds__(kThreads) k_stage1(Stage1Args a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int tile = blockIdx.x;
-  const int64_t q = blockIdx.y;
+  const int64_t q = blockIdx.x;
+  const int tile = blockIdx.y;
   const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
 
   // ---- carve shared memory ----
   Smem s;
@@ -131,18 +186,23 @@ __global__ void __launch_bounds__(kThreads) k_stage1(Stage1Args a) {
   p += sizeof(Cand);
   s.acc = reinterpret_cast<double*>(p);
   p += sizeof(double) * kChunk;
+  s.lut = reinterpret_cast<uint4*>(p);
+  p += 16 * (size_t)a.Kp;
   s.dqv = reinterpret_cast<double*>(p);
   p += sizeof(double) * a.max_qnnz;
   s.dcur = reinterpret_cast<uint32_t*>(p);
   p += sizeof(uint32_t) * a.max_qnnz;
   s.dend = reinterpret_cast<uint32_t*>(p);
   p += sizeof(uint32_t) * a.max_qnnz;
-  s.dcnt = reinterpret_cast<uint32_t*>(p);
+  s.dnext = reinterpret_cast<uint32_t*>(p);
+  p += sizeof(uint32_t) * a.max_qnnz;
+  s.alist = reinterpret_cast<uint32_t*>(p);
+  p += sizeof(uint32_t) * a.max_qnnz;
+  s.abase = reinterpret_cast<uint32_t*>(p);
+  p += sizeof(uint32_t) * a.max_qnnz;
+  s.acnt = reinterpret_cast<uint32_t*>(p);
   p += sizeof(uint32_t) * a.max_qnnz;
   s.ctl = reinterpret_cast<int*>(p);
-  p += sizeof(int) * 4;
-  p = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(p) + 15) & ~uintptr_t(15));
-  s.lut = p;
 
   const int64_t tile_lo = (int64_t)tile * a.tile_pts;
   const int64_t tile_hi = min(a.n, tile_lo + a.tile_pts);
@@ -150,103 +210,155 @@ __global__ void __launch_bounds__(kThreads) k_stage1(Stage1Args a) {
   // ---- per-query setup ----
   const int64_t qb = a.qptr[q], qe = a.qptr[q + 1];
   const int nd = (int)(qe - qb);
+  HS_DCHECK(nd >= 0 && nd <= a.max_qnnz);
   for (int d = tid; d < nd; d += blockDim.x) {
     const uint32_t b = a.lbeg[qb + d], e = a.lend[qb + d];
+    HS_DCHECK(b <= e);
+    const uint32_t c = lower_bound_ids(a.post, b, e, (uint32_t)tile_lo);
     s.dqv[d] = a.qv[qb + d];
-    s.dcur[d] = lower_bound_ids(a.post, b, e, (uint32_t)tile_lo);
+    s.dcur[d] = c;
     s.dend[d] = e;
+    s.dnext[d] = c < e ? __ldg(&a.post[c].x) : 0xFFFFFFFFu;
   }
   if (a.has_dense) {
     const uint4* src = reinterpret_cast<const uint4*>(a.luts + q * (int64_t)a.Kp * 16);
-    uint4* dst = reinterpret_cast<uint4*>(s.lut);
-    for (int i = tid; i < a.Kp; i += blockDim.x) dst[i] = src[i];
+    for (int i = tid; i < a.Kp; i += blockDim.x) s.lut[i] = src[i];
   }
-  if (tid == 0) {
-    s.ctl[0] = 0;
-    s.ctl[1] = 0;
-    s.ctl[2] = 0;
-  }
+  if (tid < 16) s.ctl[tid] = 0;
   double btot = 0.0, scl = 0.0, off = 0.0;
   if (a.has_dense) {
     btot = a.bias_total[q];
     scl = a.scale[q];
     off = a.offset ? a.offset[q] : 0.0;
   }
+  const uint2* vc = reinterpret_cast<const uint2*>(a.vcodes);
+  const int64_t vrow = a.vstride >> 1;  // uint2 per subspace row
   __syncthreads();
 
   for (int64_t cb = tile_lo; cb < tile_hi; cb += kChunk) {
     const int64_t ce = min(tile_hi, cb + (int64_t)kChunk);
-    // ---- 1+2: sparse accumulation for this chunk ----
-    for (int i = tid; i < kChunk; i += blockDim.x) s.acc[i] = 0.0;
-    int any = 0;
-    for (int d = tid; d < nd; d += blockDim.x) {
-      const uint32_t c = count_below(a.post, s.dcur[d], s.dend[d], (uint32_t)ce);
-      s.dcnt[d] = c;
-      any |= (c != 0);
+    const int64_t p0 = cb + (int64_t)tid * kPPT;
+    HS_DCHECK(cb >= tile_lo && ce <= a.n);
+
+    // ---- dense: LUT16 scan of this thread's 16 points ----
+    uint32_t tot[kPPT];
+#pragma unroll
+    for (int j = 0; j < kPPT; ++j) tot[j] = 0;
+    if (a.has_dense && p0 < ce) {
+      const uint2* col = vc + (p0 >> 4);
+      uint32_t acc2[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc2[j] = 0;
+      int k = 0;
+      for (int kb = 0; kb < a.K; kb += 256) {
+        const int kend = min(a.K, kb + 256);
+        for (; k + 4 <= kend; k += 4) {
+          uint2 w[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) w[u] = __ldg(col + (int64_t)(k + u) * vrow);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const uint4 T = s.lut[k + u];
+            uint32_t r0, r1, r2, r3;
+            lut8(T, w[u].x, r0, r1);
+            lut8(T, w[u].y, r2, r3);
+            accum16(acc2, r0, r1, r2, r3);
+          }
+        }
+        for (; k < kend; ++k) {
+          const uint2 w = __ldg(col + (int64_t)k * vrow);
+          const uint4 T = s.lut[k];
+          uint32_t r0, r1, r2, r3;
+          lut8(T, w.x, r0, r1);
+          lut8(T, w.y, r2, r3);
+          accum16(acc2, r0, r1, r2, r3);
+        }
+        // widen: acc2[2g] holds points (4g, 4g+2), acc2[2g+1] holds (4g+1, 4g+3)
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          tot[4 * g + 0] += acc2[2 * g] & 0xFFFFu;
+          tot[4 * g + 2] += acc2[2 * g] >> 16;
+          tot[4 * g + 1] += acc2[2 * g + 1] & 0xFFFFu;
+          tot[4 * g + 3] += acc2[2 * g + 1] >> 16;
+          acc2[2 * g] = 0;
+          acc2[2 * g + 1] = 0;
+        }
+      }
     }
-    any = __syncthreads_or(any);
-    if (any) {
-      for (int d = 0; d < nd; ++d) {
-        const uint32_t c = s.dcnt[d];
-        if (c == 0) continue;  // uniform across the block
-        const uint32_t base = s.dcur[d];
-        const double qv = s.dqv[d];
-        for (uint32_t i = tid; i < c; i += blockDim.x) {
-          const uint2 pw = a.post[base + i];
+
+    // ---- sparse: active dims of this chunk, in ascending dim order ----
+    int nact = 0;
+    for (int base = 0; base < nd; base += blockDim.x) {
+      const int d = base + tid;
+      const bool f = d < nd && s.dnext[d] < (uint32_t)ce;
+      const unsigned bal = __ballot_sync(0xffffffffu, f);
+      if (lane == 0) s.ctl[4 + warp] = __popc(bal);
+      __syncthreads();
+      int before = 0, total = 0;
+#pragma unroll
+      for (int i = 0; i < kThreads / 32; ++i) {
+        const int c = s.ctl[4 + i];
+        before += (i < warp) ? c : 0;
+        total += c;
+      }
+      if (f) {
+        const int slot = nact + before + __popc(bal & ((1u << lane) - 1u));
+        HS_DCHECK(slot < a.max_qnnz);
+        const uint32_t cur = s.dcur[d], end = s.dend[d];
+        HS_DCHECK(cur < end);
+        HS_DCHECK(__ldg(&a.post[cur].x) == s.dnext[d]);
+        HS_DCHECK(s.dnext[d] >= (uint32_t)cb);
+        const uint32_t cnt = count_below_known(a.post, cur, end, (uint32_t)ce);
+        HS_DCHECK(cnt >= 1 && __ldg(&a.post[cur + cnt - 1].x) < (uint32_t)ce);
+        const uint32_t nc = cur + cnt;
+        s.alist[slot] = d;
+        s.abase[slot] = cur;
+        s.acnt[slot] = cnt;
+        s.dcur[d] = nc;
+        s.dnext[d] = nc < end ? __ldg(&a.post[nc].x) : 0xFFFFFFFFu;
+      }
+      nact += total;
+      __syncthreads();
+    }
+#ifdef HS_DEBUG
+    for (int i = tid; i < nact; i += blockDim.x) {
+      const uint32_t id0 = __ldg(&a.post[s.abase[i]].x);
+      if (!(id0 >= (uint32_t)cb && id0 < (uint32_t)ce))
+        printf("STALE q=%d i=%d nact=%d d=%u base=%u cnt=%u id0=%u cb=%lld ctlw=%d,%d,%d,%d,%d,%d,%d,%d\n",
+               (int)q, i, nact, s.alist[i], s.abase[i], s.acnt[i], id0, (long long)cb, s.ctl[4],
+               s.ctl[5], s.ctl[6], s.ctl[7], s.ctl[8], s.ctl[9], s.ctl[10], s.ctl[11]);
+    }
+    __syncthreads();
+#endif
+    if (nact > 0) {
+      for (int i = tid; i < kChunk; i += blockDim.x) s.acc[i] = 0.0;
+      __syncthreads();
+      for (int i = 0; i < nact; ++i) {
+        const uint32_t b = s.abase[i], c = s.acnt[i];
+        const double qv = s.dqv[s.alist[i]];
+        for (uint32_t j = tid; j < c; j += blockDim.x) {
+          const uint2 pw = __ldg(&a.post[b + j]);
+#ifdef HS_DEBUG
+          if (!(pw.x >= cb && pw.x < ce)) {
+            if (j == tid && tid < 2)
+              printf("BADSLICE q=%d tile=%d i=%d nact=%d d=%u b=%u c=%u j=%u id=%u cb=%lld ce=%lld nd=%d\n",
+                     (int)q, tile, i, nact, s.alist[i], b, c, j, pw.x, (long long)cb,
+                     (long long)ce, nd);
+            __trap();
+          }
+#endif
           // f64(q) * f64(w) is exact, so contraction cannot change the sum
           s.acc[pw.x - cb] += qv * (double)__uint_as_float(pw.y);
         }
         __syncthreads();
       }
-      for (int d = tid; d < nd; d += blockDim.x) s.dcur[d] += s.dcnt[d];
     }
 
-    // ---- 3: LUT16 scan, 8 points per thread ----
-    const int64_t p0 = cb + (int64_t)tid * kPPT;
-    uint32_t tot[kPPT];
-#pragma unroll
-    for (int j = 0; j < kPPT; ++j) tot[j] = 0;
-    if (a.has_dense && p0 < ce) {
-      const uint8_t* col = a.packed + p0;
-      int r = 0;
-      for (; r + 4 <= a.npairs; r += 4) {
-        uint2 w[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-          w[u] = __ldg(reinterpret_cast<const uint2*>(col + (int64_t)(r + u) * a.pstride));
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const uint8_t* t0 = s.lut + (r + u) * 32;
-          const uint8_t* t1 = t0 + 16;
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const uint32_t b0 = (w[u].x >> (8 * j)) & 0xFF;
-            const uint32_t b1 = (w[u].y >> (8 * j)) & 0xFF;
-            tot[j] += t0[b0 & 15] + t1[b0 >> 4];
-            tot[4 + j] += t0[b1 & 15] + t1[b1 >> 4];
-          }
-        }
-      }
-      for (; r < a.npairs; ++r) {
-        const uint2 w = __ldg(reinterpret_cast<const uint2*>(col + (int64_t)r * a.pstride));
-        const uint8_t* t0 = s.lut + r * 32;
-        const uint8_t* t1 = t0 + 16;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const uint32_t b0 = (w.x >> (8 * j)) & 0xFF;
-          const uint32_t b1 = (w.y >> (8 * j)) & 0xFF;
-          tot[j] += t0[b0 & 15] + t1[b0 >> 4];
-          tot[4 + j] += t0[b1 & 15] + t1[b1 >> 4];
-        }
-      }
-    }
-    __syncthreads();  // acc complete before reading it below
-
-    // ---- 4: stage-1 scores ----
+    // ---- scores ----
     double sc[kPPT];
 #pragma unroll
     for (int j = 0; j < kPPT; ++j) {
-      const double acc = s.acc[tid * kPPT + j];
+      const double acc = nact > 0 ? s.acc[tid * kPPT + j] : 0.0;
       if (a.raw_dense) {
         sc[j] = __dadd_rn(btot, __dmul_rn(scl, (double)tot[j]));
       } else if (a.has_dense) {
@@ -284,7 +396,7 @@ __global__ void __launch_bounds__(kThreads) k_stage1(Stage1Args a) {
       continue;
     }
 
-    // ---- 5: offer to the candidate buffer ----
+    // ---- offer to the candidate buffer ----
     unsigned mask = 0;
     {
       const int have = s.ctl[2];
@@ -298,37 +410,65 @@ __global__ void __launch_bounds__(kThreads) k_stage1(Stage1Args a) {
         if (pass) mask |= 1u << j;
       }
     }
-    atomicAdd(&s.ctl[1], __popc(mask));
-    __syncthreads();
-    if (s.ctl[0] + s.ctl[1] > a.cap) {  // uniform
-      compact(s, a.k);
-      // re-filter against the tightened threshold
-      const Cand th = *s.th;
-      unsigned m2 = 0;
+    // snapshot the count before block_sum's barriers: threads that pass the
+    // room check start appending (atomicAdd on ctl[0]) right after it
+    const int cnt0 = s.ctl[0];
+    const int need = block_sum(__popc(mask), s.ctl + 4);
+    if (cnt0 + need <= a.cap) {
+      // common case: room for every offer
+      if (mask) {
+        int pos = atomicAdd(&s.ctl[0], __popc(mask));
+        HS_DCHECK(pos + __popc(mask) <= a.cap);
 #pragma unroll
-      for (int j = 0; j < kPPT; ++j) {
-        if (!(mask >> j & 1)) continue;
-        bool pass = sc[j] > th.s;
-        if (!pass && sc[j] == th.s) pass = a.order[p0 + j] < th.tie;
-        if (pass) m2 |= 1u << j;
+        for (int j = 0; j < kPPT; ++j) {
+          if (!(mask >> j & 1)) continue;
+          Cand c;
+          c.s = sc[j];
+          c.slot = (uint32_t)(p0 + j);
+          c.tie = a.order[p0 + j];
+          s.buf[pos++] = c;
+        }
       }
-      mask = m2;
-    }
-    if (mask) {
-      int pos = atomicAdd(&s.ctl[0], __popc(mask));
+      __syncthreads();
+    } else {
+      // rounds of <= 4 offers per thread, compacting whenever room runs out
 #pragma unroll
-      for (int j = 0; j < kPPT; ++j) {
-        if (!(mask >> j & 1)) continue;
-        Cand c;
-        c.s = sc[j];
-        c.slot = (uint32_t)(p0 + j);
-        c.tie = a.order[p0 + j];
-        s.buf[pos++] = c;
+      for (int r = 0; r < kPPT / 4; ++r) {
+        unsigned m = (mask >> (4 * r)) & 0xFu;
+        const int cnt_r = s.ctl[0];  // read before the barriers, see above
+        const int nr = block_sum(__popc(m), s.ctl + 4);
+        if (nr == 0) continue;
+        if (cnt_r + nr > a.cap) {
+          compact(s, a.k);
+          const Cand th = *s.th;
+          unsigned m2 = 0;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            if (!(m >> j & 1)) continue;
+            const int jj = 4 * r + j;
+            bool pass = sc[jj] > th.s;
+            if (!pass && sc[jj] == th.s) pass = a.order[p0 + jj] < th.tie;
+            if (pass) m2 |= 1u << j;
+          }
+          m = m2;
+        }
+        if (m) {
+          int pos = atomicAdd(&s.ctl[0], __popc(m));
+          HS_DCHECK(pos + __popc(m) <= a.cap);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            if (!(m >> j & 1)) continue;
+            const int jj = 4 * r + j;
+            Cand c;
+            c.s = sc[jj];
+            c.slot = (uint32_t)(p0 + jj);
+            c.tie = a.order[p0 + jj];
+            s.buf[pos++] = c;
+          }
+        }
+        __syncthreads();
       }
     }
-    __syncthreads();
-    if (tid == 0) s.ctl[1] = 0;
-    __syncthreads();
   }
 
   if (a.mode == S1_EMIT_ALL) {
@@ -371,21 +511,52 @@ __global__ void k_map_dims(const uint32_t* __restrict__ dims_q, const float* __r
   qv[i] = (double)v;
 }
 
+// pair-major packed codes (dense.py:156-170) -> vertical nibble planes
+__global__ void k_to_vertical(const uint8_t* __restrict__ packed, int64_t n, int K,
+                              int64_t vstride, uint32_t* __restrict__ v) {
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // word (8 points)
+  const int k = blockIdx.y;
+  if (g >= vstride) return;
+  const uint8_t* row = packed + (int64_t)(k >> 1) * n;
+  const int sh = (k & 1) ? 4 : 0;
+  uint32_t w = 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const int64_t pt = g * 8 + j;
+    const uint32_t c = pt < n ? ((row[pt] >> sh) & 0xFu) : 0u;
+    w |= c << (4 * j);
+  }
+  v[(int64_t)k * vstride + g] = w;
+}
+
 }  // namespace
 
 int stage1_chunk_points() { return kChunk; }
+
+int64_t vertical_stride(int64_t n) {
+  // u32 words per subspace row: 2 words per 16 points, padded to 64 B
+  const int64_t words = ((n + 15) / 16) * 2;
+  return ((words + 15) / 16) * 16;
+}
+
+void launch_to_vertical(const uint8_t* packed, int64_t n, int K, int64_t vstride, uint32_t* v,
+                        cudaStream_t st) {
+  if (K <= 0) return;
+  dim3 grid((unsigned)ceil_div(vstride, 256), (unsigned)K);
+  k_to_vertical<<<grid, 256, 0, st>>>(packed, n, K, vstride, v);
+}
 
 Stage1Plan plan_stage1(const DeviceIndex& ix, int64_t nq, int64_t k, int max_qnnz, int mode) {
   Stage1Plan p;
   p.mode = mode;
   p.max_qnnz = max_qnnz < 1 ? 1 : max_qnnz;
   const int64_t nchunks = ceil_div(ix.n, kChunk);
+  const int64_t target_ctas = 3LL * kNumSMs;
   if (mode == S1_SELECT) {
-    // enough tiles to fill the GPU, but tiles much larger than k so the
-    // per-tile keep actually filters; the merge sorts ntiles*k entries.
-    const int64_t target_ctas = 4LL * kNumSMs;
+    // enough tiles to fill the GPU, tiles much larger than k so the per-tile
+    // keep filters; the merge then sorts ntiles*k entries per query
     int64_t ntiles = ceil_div(target_ctas, nq > 0 ? nq : 1);
-    const int64_t min_tile_chunks = ceil_div(8 * k, kChunk);  // tile >= ~8k points
+    const int64_t min_tile_chunks = ceil_div(8 * k, kChunk);
     const int64_t max_tiles_by_k = nchunks / (min_tile_chunks > 0 ? min_tile_chunks : 1);
     if (ntiles > max_tiles_by_k) ntiles = max_tiles_by_k;
     if (ntiles * k > 65536) ntiles = 65536 / (k > 0 ? k : 1);
@@ -399,11 +570,10 @@ Stage1Plan plan_stage1(const DeviceIndex& ix, int64_t nq, int64_t k, int max_qnn
       p.out_per_tile = p.tile_pts;
     } else {
       p.k = (int)k;
-      p.cap = next_pow2(k + kChunk);
+      p.cap = next_pow2(k + kOfferRound);
       p.out_per_tile = k;
     }
   } else {
-    const int64_t target_ctas = 4LL * kNumSMs;
     int64_t ntiles = ceil_div(target_ctas, nq > 0 ? nq : 1);
     if (ntiles > nchunks) ntiles = nchunks;
     if (ntiles < 1) ntiles = 1;
@@ -411,20 +581,21 @@ Stage1Plan plan_stage1(const DeviceIndex& ix, int64_t nq, int64_t k, int max_qnn
     p.ntiles = (int)ceil_div(ix.n, p.tile_pts);
     p.out_per_tile = (mode == S1_EMIT_ALL) ? p.tile_pts : 0;
   }
+  if (p.ntiles < 1) p.ntiles = 1;
   return p;
 }
 
 size_t stage1_smem_bytes(const DeviceIndex& ix, const Stage1Plan& p) {
   size_t b = sizeof(Cand) * (size_t)(p.mode == S1_SELECT ? p.cap : 0) + sizeof(Cand);
   b += sizeof(double) * kChunk;
-  b += (sizeof(double) + 3 * sizeof(uint32_t)) * (size_t)p.max_qnnz;
-  b += sizeof(int) * 4 + 16;
-  b += (size_t)ix.Kp * 16;
+  b += 16 * (size_t)ix.Kp;
+  b += (sizeof(double) + 6 * sizeof(uint32_t)) * (size_t)p.max_qnnz;
+  b += sizeof(int) * 16;
   return b;
 }
 
 void launch_map_dims(const DeviceIndex& ix, const QueryView& q, int64_t nnz, bool use_weight,
-                       uint32_t* lbeg, uint32_t* lend, double* qv, cudaStream_t st) {
+                     uint32_t* lbeg, uint32_t* lend, double* qv, cudaStream_t st) {
   if (nnz <= 0) return;
   const int T = 256;
   k_map_dims<<<(unsigned)ceil_div(nnz, T), T, 0, st>>>(
@@ -437,7 +608,7 @@ int launch_stage1(const DeviceIndex& ix, const QueryView& q, const Stage1Plan& p
                   const uint8_t* luts, const double* bias_total, const double* scale,
                   const double* offset, Cand* out, double* dump, cudaStream_t st,
                   uint32_t* dump_tot, bool raw_dense) {
-  if (q.nq <= 0) return HS_OK;
+  if (q.nq <= 0 || ix.n <= 0) return HS_OK;
   Stage1Args a;
   a.n = ix.n;
   a.tile_pts = p.tile_pts;
@@ -451,11 +622,11 @@ int launch_stage1(const DeviceIndex& ix, const QueryView& q, const Stage1Plan& p
   a.lbeg = lbeg;
   a.lend = lend;
   a.qv = qv;
-  a.has_dense = (ix.d_dense > 0 && p.use_dense && !p.sparse_only_acc) ? 1 : 0;
-  a.npairs = ix.npairs;
+  a.has_dense = (ix.d_dense > 0 && ix.K > 0 && p.use_dense && !p.sparse_only_acc) ? 1 : 0;
+  a.K = ix.K;
   a.Kp = ix.Kp;
-  a.packed = ix.packed;
-  a.pstride = ix.pstride;
+  a.vcodes = ix.vcodes;
+  a.vstride = ix.vstride;
   a.luts = luts;
   a.bias_total = bias_total;
   a.scale = scale;
@@ -470,7 +641,7 @@ int launch_stage1(const DeviceIndex& ix, const QueryView& q, const Stage1Plan& p
   if (smem > 227 * 1024) HS_FAIL(HS_EUNSUPPORTED, "stage-1 shared memory exceeds 227 KB "
                                                   "(too many query nonzeros or candidates)");
   HS_CUDA(cudaFuncSetAttribute(k_stage1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  dim3 grid((unsigned)p.ntiles, (unsigned)q.nq);
+  dim3 grid((unsigned)q.nq, (unsigned)p.ntiles);
   k_stage1<<<grid, kThreads, smem, st>>>(a);
   HS_CUDA(cudaGetLastError());
   return HS_OK;

@@ -1,0 +1,108 @@
+"""GPU parity on the BASELINE data laws (seeded generator), scaled down so the
+CPU oracle finishes in seconds: cfg1/cfg2-shaped hybrid data with K=64/128,
+dense-only (cfg3-shaped) and sparse-only unpruned (cfg4-shaped)."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import paper_1903_08690_b200 as hs
+from paper_1903_08690_b200 import synth
+from oracle import hybrid_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _scaled(name, n, nq, **over):
+    ds, qs, cfg = synth.make_config(name, n=n, n_queries=nq)
+    kw = dict(cfg.index)
+    kw.update(over)
+    kw.setdefault("kmeans_iters", 4)
+    kw["train_sample"] = min(n, 20_000)
+    idx = hs.build_index(ds, hs.HybridIndexConfig(**kw))
+    return ds, qs, cfg, idx
+
+
+def _check_search(idx, qs, h, a, b, exact, n_oracle=None):
+    res = hs.search_batch(idx, qs, h, overfetch=a, retain=b, exact_final_rerank=exact)
+    n_oracle = qs.n if n_oracle is None else n_oracle
+    for i in range(n_oracle):
+        ids, sc, _ = O.search_topk(idx, *O.query_parts(qs, i), h, overfetch=a, retain=b,
+                                   exact_final_rerank=exact)
+        assert res[i].ids.tolist() == ids.tolist(), i
+        np.testing.assert_allclose(res[i].scores, sc, rtol=1e-9)
+    return res
+
+
+@pytest.mark.parametrize("name,n,top_t", [("cfg2", 30_000, 128), ("cfg1", 40_000, 128),
+                                          ("cfg1", 20_000, None)])
+def test_hybrid_law_search_matches_oracle(name, n, top_t):
+    ds, qs, cfg, idx = _scaled(name, n, 12, top_t=top_t)
+    s = cfg.search
+    _check_search(idx, qs, s["h"], s["overfetch"], s["retain"], s["exact_final_rerank"])
+    _check_search(idx, qs, 10, 5.0, 2.0, False)
+
+
+def test_stage1_scores_and_totals_k128():
+    ds, qs, cfg, idx = _scaled("cfg2", 20_000, 6)
+    s1 = hs.stage1_scores(idx, qs)
+    for i in range(qs.n):
+        ref = O.stage1_scores(idx, *O.query_parts(qs, i))
+        # whitening offset is a BLAS ddot the GPU does not reproduce bit-for-bit
+        np.testing.assert_allclose(s1[i], ref, rtol=1e-12, atol=1e-15)
+
+
+def test_dense_only_law_top100():
+    ds, qs, cfg, idx = _scaled("cfg3", 60_000, 8)
+    res = _check_search(idx, qs, 100, 1.0, 1.0, False)
+    assert all(len(r.ids) == 100 for r in res)
+
+
+def test_sparse_only_unpruned_law_top10():
+    law = synth.CONFIGS["cfg4"]
+    ds = synth.generate(law.data, 0, n=50_000)
+    qs = synth.generate(law.data, 1, n=10, mean_nnz=law.query_mean_nnz)
+    idx = hs.build_index(ds, hs.HybridIndexConfig(top_t=None))
+    _check_search(idx, qs, 10, 1.0, 1.0, False)
+    acc_gpu = hs.stage1_scores(idx, qs)
+    for i in range(qs.n):
+        assert np.array_equal(acc_gpu[i], O.stage1_scores(idx, *O.query_parts(qs, i)))
+
+
+def test_device_entry_point_matches_host_entry_point():
+    import torch
+
+    ds, qs, cfg, idx = _scaled("cfg2", 30_000, 16)
+    s = cfg.search
+    host = hs.search_batch(idx, qs, s["h"], overfetch=s["overfetch"], retain=s["retain"],
+                           exact_final_rerank=True)
+    dev = hs.device_index(idx)
+    p = hs.search.resolve_params(idx, s["h"], s["overfetch"], s["retain"], True)
+    from paper_1903_08690_b200 import _native as nat
+
+    sp_ = qs.sparse
+    t = [torch.as_tensor(np.asarray(sp_.indptr, np.int64)).cuda(),
+         torch.as_tensor(np.asarray(sp_.indices, np.int32)).cuda(),
+         torch.as_tensor(np.asarray(sp_.data, np.float32)).cuda(),
+         torch.as_tensor(np.ascontiguousarray(qs.dense, np.float32)).cuda()]
+    b = nat.QueryBatch()
+    b.nq, b.sp_indptr, b.sp_dims, b.sp_vals, b.dense = qs.n, *[x.data_ptr() for x in t]
+    b.nnz, b.max_row_nnz = int(sp_.nnz), int(np.diff(sp_.indptr).max())
+    kh = s["h"]
+    ids = torch.empty((qs.n, kh), dtype=torch.int64, device="cuda")
+    sc = torch.empty((qs.n, kh), dtype=torch.float64, device="cuda")
+    torch.cuda.synchronize()
+    dev.search_dev(b, p, ids.data_ptr(), sc.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    for i in range(qs.n):
+        assert ids[i].tolist() == host[i].ids.tolist()
+        assert sc[i].tolist() == host[i].scores.tolist()
+
+
+def test_multi_chunk_tiles_many_queries():
+    """Tiles spanning many 4096-point chunks (the bench regime): 300 queries over
+    100K points => 2 tiles x 13 chunks per CTA."""
+    ds, qs, cfg, idx = _scaled("cfg2", 100_000, 300)
+    s = cfg.search
+    _check_search(idx, qs, s["h"], s["overfetch"], s["retain"], True, n_oracle=6)
