@@ -28,6 +28,8 @@
 //   3. score = acc + ((bias_total + scale*total) + offset), unfused f64.
 //   4. offer to a shared-memory candidate buffer guarded by the running k-th
 //      best (score desc, original id asc); overflow => bitonic compaction.
+#include <cstdlib>
+
 #include "kernels.cuh"
 
 namespace hs {
@@ -38,6 +40,7 @@ constexpr int kThreads = 256;
 constexpr int kPPT = 16;                   // points per thread per chunk
 constexpr int kChunk = kThreads * kPPT;    // 4096 points
 constexpr int kOfferRound = kThreads * 4;  // worst-case offers per insertion round
+constexpr int kSmallPostings = 512;        // below this a chunk's postings skip the barriers
 
 struct Stage1Args {
   int64_t n;
@@ -68,6 +71,7 @@ struct Stage1Args {
   uint32_t* dump_tot;  // DUMP: integer totals (optional)
   int raw_dense;       // DUMP: bias_total + scale*total only (lut16_scan semantics)
   int max_qnnz;
+  int exp_flags;       // dev experiments (HSB200_EXP): 1 no dense, 2 no sparse, 4 no offers
 };
 
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t s) {
@@ -82,10 +86,12 @@ __device__ __forceinline__ void lut8(const uint4& T, uint32_t w, uint32_t& r0, u
   const uint32_t x = w ^ 0x88888888u;             // entries 8..15 become selectors 0..7
   const uint32_t a0 = prmt(T.x, T.y, w), a1 = prmt(T.x, T.y, w >> 16);
   const uint32_t b0 = prmt(T.z, T.w, x), b1 = prmt(T.z, T.w, x >> 16);
-  const uint32_t m = w & 0x88888888u;
-  const uint32_t s = m | (m >> 3);                // nibble 9 where code >= 8, else 0
-  const uint32_t k0 = prmt(0x00008000u, 0u, s);   // sign-replicated 0x80 -> 0xFF
-  const uint32_t k1 = prmt(0x00008000u, 0u, s >> 16);
+  // mask selector: nibble bit 3 = code bit 3, bit 0 = code bit 3 too (bits 1-2
+  // carry junk from the next code).  Bytes of 0x80008000: even 0x00, odd 0x80,
+  // so a clear bit 3 selects 0x00 and a set one sign-replicates 0x80 -> 0xFF.
+  const uint32_t s = (w & 0x88888888u) | ((w >> 3) & 0x77777777u);
+  const uint32_t k0 = prmt(0x80008000u, 0x80008000u, s);
+  const uint32_t k1 = prmt(0x80008000u, 0x80008000u, s >> 16);
   r0 = (b0 & k0) | (a0 & ~k0);
   r1 = (b1 & k1) | (a1 & ~k1);
 }
@@ -158,16 +164,14 @@ __device__ __forceinline__ int block_sum(int v, int* scratch) {
   return t;
 }
 
-__device__ __forceinline__ void accum16(uint32_t* acc2, uint32_t r0, uint32_t r1, uint32_t r2,
-                                        uint32_t r3) {
-  acc2[0] += r0 & 0x00FF00FFu;
-  acc2[1] += prmt(r0, 0u, 0x4341u);  // bytes 1,3 -> u16 lanes
-  acc2[2] += r1 & 0x00FF00FFu;
-  acc2[3] += prmt(r1, 0u, 0x4341u);
-  acc2[4] += r2 & 0x00FF00FFu;
-  acc2[5] += prmt(r2, 0u, 0x4341u);
-  acc2[6] += r3 & 0x00FF00FFu;
-  acc2[7] += prmt(r3, 0u, 0x4341u);
+// two subspaces' lookups for the same 16 points, widened to u16 lanes and
+// added with one IADD3 per lane pair (byte sums of two entries fit in 16 bits)
+__device__ __forceinline__ void accum32(uint32_t* acc2, const uint32_t* r, const uint32_t* t) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    acc2[2 * i] += (r[i] & 0x00FF00FFu) + (t[i] & 0x00FF00FFu);
+    acc2[2 * i + 1] += prmt(r[i], 0u, 0x4341u) + prmt(t[i], 0u, 0x4341u);  // bytes 1,3
+  }
 }
 
 __global__ void __launch_bounds__(kThreads) k_stage1(Stage1Args a) {
@@ -244,7 +248,7 @@ __global__ void __launch_bounds__(kThreads) k_stage1(Stage1Args a) {
     uint32_t tot[kPPT];
 #pragma unroll
     for (int j = 0; j < kPPT; ++j) tot[j] = 0;
-    if (a.has_dense && p0 < ce) {
+    if (a.has_dense && p0 < ce && !(a.exp_flags & 1)) {
       const uint2* col = vc + (p0 >> 4);
       uint32_t acc2[8];
 #pragma unroll
@@ -252,26 +256,28 @@ __global__ void __launch_bounds__(kThreads) k_stage1(Stage1Args a) {
       int k = 0;
       for (int kb = 0; kb < a.K; kb += 256) {
         const int kend = min(a.K, kb + 256);
-        for (; k + 4 <= kend; k += 4) {
-          uint2 w[4];
+        for (; k + 8 <= kend; k += 8) {
+          uint2 w[8];
 #pragma unroll
-          for (int u = 0; u < 4; ++u) w[u] = __ldg(col + (int64_t)(k + u) * vrow);
+          for (int u = 0; u < 8; ++u) w[u] = __ldg(col + (int64_t)(k + u) * vrow);
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const uint4 T = s.lut[k + u];
-            uint32_t r0, r1, r2, r3;
-            lut8(T, w[u].x, r0, r1);
-            lut8(T, w[u].y, r2, r3);
-            accum16(acc2, r0, r1, r2, r3);
+          for (int u = 0; u < 8; u += 2) {
+            const uint4 T0 = s.lut[k + u], T1 = s.lut[k + u + 1];
+            uint32_t r[4], t[4];
+            lut8(T0, w[u].x, r[0], r[1]);
+            lut8(T0, w[u].y, r[2], r[3]);
+            lut8(T1, w[u + 1].x, t[0], t[1]);
+            lut8(T1, w[u + 1].y, t[2], t[3]);
+            accum32(acc2, r, t);
           }
         }
         for (; k < kend; ++k) {
           const uint2 w = __ldg(col + (int64_t)k * vrow);
           const uint4 T = s.lut[k];
-          uint32_t r0, r1, r2, r3;
-          lut8(T, w.x, r0, r1);
-          lut8(T, w.y, r2, r3);
-          accum16(acc2, r0, r1, r2, r3);
+          uint32_t r[4], t[4] = {0u, 0u, 0u, 0u};
+          lut8(T, w.x, r[0], r[1]);
+          lut8(T, w.y, r[2], r[3]);
+          accum32(acc2, r, t);
         }
         // widen: acc2[2g] holds points (4g, 4g+2), acc2[2g+1] holds (4g+1, 4g+3)
 #pragma unroll
@@ -287,10 +293,10 @@ __global__ void __launch_bounds__(kThreads) k_stage1(Stage1Args a) {
     }
 
     // ---- sparse: active dims of this chunk, in ascending dim order ----
-    int nact = 0;
+    int nact = 0, npost = 0;
     for (int base = 0; base < nd; base += blockDim.x) {
       const int d = base + tid;
-      const bool f = d < nd && s.dnext[d] < (uint32_t)ce;
+      const bool f = d < nd && s.dnext[d] < (uint32_t)ce && !(a.exp_flags & 2);
       const unsigned bal = __ballot_sync(0xffffffffu, f);
       if (lane == 0) s.ctl[4 + warp] = __popc(bal);
       __syncthreads();
@@ -320,6 +326,11 @@ __global__ void __launch_bounds__(kThreads) k_stage1(Stage1Args a) {
       nact += total;
       __syncthreads();
     }
+    if (nact > 0) {
+      int mine = 0;
+      for (int i = tid; i < nact; i += blockDim.x) mine += (int)s.acnt[i];
+      npost = block_sum(mine, s.ctl + 4);
+    }
 #ifdef HS_DEBUG
     for (int i = tid; i < nact; i += blockDim.x) {
       const uint32_t id0 = __ldg(&a.post[s.abase[i]].x);
@@ -330,7 +341,24 @@ __global__ void __launch_bounds__(kThreads) k_stage1(Stage1Args a) {
     }
     __syncthreads();
 #endif
-    if (nact > 0) {
+    if (nact > 0 && npost <= kSmallPostings) {
+      // few postings: every thread walks them all in dim order (broadcast
+      // loads) and adds only those landing on its own 16 points — per-point
+      // order stays ascending in dim with no block barriers
+      double* mine = s.acc + tid * kPPT;
+#pragma unroll
+      for (int j = 0; j < kPPT; ++j) mine[j] = 0.0;
+      for (int i = 0; i < nact; ++i) {
+        const uint32_t b = s.abase[i], c = s.acnt[i];
+        const double qv = s.dqv[s.alist[i]];
+        for (uint32_t j = 0; j < c; ++j) {
+          const uint2 pw = __ldg(&a.post[b + j]);
+          const uint32_t local = pw.x - (uint32_t)cb;
+          HS_DCHECK(local < (uint32_t)kChunk);
+          if ((local >> 4) == (uint32_t)tid) mine[local & 15] += qv * (double)__uint_as_float(pw.y);
+        }
+      }
+    } else if (nact > 0) {
       for (int i = tid; i < kChunk; i += blockDim.x) s.acc[i] = 0.0;
       __syncthreads();
       for (int i = 0; i < nact; ++i) {
@@ -397,6 +425,14 @@ __global__ void __launch_bounds__(kThreads) k_stage1(Stage1Args a) {
     }
 
     // ---- offer to the candidate buffer ----
+    if (a.exp_flags & 4) {
+      double t = 0;
+#pragma unroll
+      for (int j = 0; j < kPPT; ++j) t += sc[j];
+      if (t == 12345.678) s.ctl[15] = 1;  // keep the scores live
+      __syncthreads();
+      continue;
+    }
     unsigned mask = 0;
     {
       const int have = s.ctl[2];
@@ -551,6 +587,8 @@ Stage1Plan plan_stage1(const DeviceIndex& ix, int64_t nq, int64_t k, int max_qnn
   p.mode = mode;
   p.max_qnnz = max_qnnz < 1 ? 1 : max_qnnz;
   const int64_t nchunks = ceil_div(ix.n, kChunk);
+  // one wave of resident CTAs (3 per SM): more tiles per query cost more in
+  // per-tile selection than they save in wave quantisation (measured)
   const int64_t target_ctas = 3LL * kNumSMs;
   if (mode == S1_SELECT) {
     // enough tiles to fill the GPU, tiles much larger than k so the per-tile
@@ -637,6 +675,13 @@ int launch_stage1(const DeviceIndex& ix, const QueryView& q, const Stage1Plan& p
   a.dump_tot = dump_tot;
   a.raw_dense = raw_dense ? 1 : 0;
   a.max_qnnz = p.max_qnnz;
+  {
+    static const int exp_flags = [] {
+      const char* e = getenv("HSB200_EXP");
+      return e ? atoi(e) : 0;
+    }();
+    a.exp_flags = exp_flags;
+  }
   const size_t smem = stage1_smem_bytes(ix, p);
   if (smem > 227 * 1024) HS_FAIL(HS_EUNSUPPORTED, "stage-1 shared memory exceeds 227 KB "
                                                   "(too many query nonzeros or candidates)");
