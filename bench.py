@@ -110,20 +110,14 @@ class ClockSampler:
 
 def build_workload(args, rank, world):
     """Seeded cfg data (this rank's id-range shard) + queries + index."""
-    from paper_1903_08690_b200 import build_index, synth
+    from paper_1903_08690_b200 import build_index, sharded, synth
 
     cfg = synth.CONFIGS[args.workload]
     n_total = args.n or cfg.data.n
     t0 = time.time()
     ds_full = synth.generate(cfg.data, seed=0, n=n_total)
-    lo = n_total * rank // world
-    hi = n_total * (rank + 1) // world
-    if world > 1:
-        from paper_1903_08690_b200 import HybridDataset
-
-        ds = HybridDataset(ds_full.sparse[lo:hi], ds_full.dense[lo:hi])
-    else:
-        ds = ds_full
+    lo, _ = sharded.shard_bounds(n_total, rank, world)
+    ds = sharded.shard_dataset(ds_full, rank, world) if world > 1 else ds_full
     qs = synth.generate(cfg.data, seed=1, n=args.queries, mean_nnz=cfg.query_mean_nnz)
     t_gen = time.time() - t0
     kw = {}
@@ -131,7 +125,11 @@ def build_workload(args, rank, world):
         kw["top_t"] = None if args.top_t == "none" else int(args.top_t)
     icfg = cfg.index_config(**kw)
     t0 = time.time()
-    idx = build_index(ds, icfg)
+    exact = cfg.search["exact_final_rerank"]
+    idx = build_index(ds, icfg, keep_dataset=exact)
+    if cfg.search["overfetch"] == 1.0 and idx.dense_index is not None:
+        # "no rerank" configs: the stage-1 composition (cfg 3)
+        idx.dense_index.residual = None
     t_build = time.time() - t0
     return cfg, ds_full, ds, qs, idx, icfg, lo, t_gen, t_build
 
@@ -222,7 +220,10 @@ def main():
     ap.add_argument("--queries", type=int, default=None)
     ap.add_argument("--n", type=int, default=None)
     ap.add_argument("--top-t", default=None)
-    ap.add_argument("--cpu-sample", type=int, default=24)
+    ap.add_argument("--cpu-sample", type=int, default=None)
+    ap.add_argument("--truth-queries", type=int, default=None)
+    ap.add_argument("--qb1", type=int, default=16,
+                    help="single-query launches timed for the Qb=1 scan roofline")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -234,6 +235,11 @@ def main():
 
     if args.queries is None:
         args.queries = synth.CONFIGS[args.workload].n_queries
+    big = args.workload in ("cfg3", "cfg4")
+    if args.cpu_sample is None:
+        args.cpu_sample = 8 if big else 24
+    if args.truth_queries is None:
+        args.truth_queries = 200 if big else args.queries
     if args.impl == "reference":
         run_reference_arm(args, rank, world)
         return
@@ -328,6 +334,25 @@ def main():
         torch.cuda.synchronize()
         for k, v in dev_index.kernel_times().items():
             ktimes[k] = ktimes.get(k, 0.0) + v / 2
+    qb1 = None
+    if world == 1 and args.qb1 > 0:
+        # Qb=1: one query per launch, stage-1 kernel time per pass over the codes
+        from paper_1903_08690_b200 import HybridDataset
+
+        t1 = []
+        for i in range(min(args.qb1, nq)):
+            one = HybridDataset(qs.sparse[i:i + 1], qs.dense[i:i + 1])
+            b1, hold1, _ = query_device_buffers(one, idx.d_dense, torch, dev)
+            o_i = torch.empty((1, kh), dtype=torch.int64, device=dev)
+            o_s = torch.empty((1, kh), dtype=torch.float64, device=dev)
+            flush.zero_()
+            torch.cuda.synchronize()
+            dev_index.search_dev(b1, params, o_i.data_ptr(), o_s.data_ptr(), stream.cuda_stream)
+            torch.cuda.synchronize()
+            kt = dev_index.kernel_times()
+            if i > 0:  # first launch warms the per-launch path
+                t1.append(kt.get("stage1", 0.0))
+        qb1 = float(np.mean(t1)) if t1 else None
     dev_index.set_timing(False)
 
     # ---- results (rank-local then merged) and recall@10 vs exact brute force ----
@@ -338,7 +363,7 @@ def main():
         res_ids = out_ids.cpu().numpy()
     recall = None
     if rank == 0:
-        truth_q = nq
+        truth_q = min(nq, args.truth_queries)
         from paper_1903_08690_b200 import HybridDataset
 
         qsub = HybridDataset(qs.sparse[:truth_q], qs.dense[:truth_q])
@@ -381,6 +406,7 @@ def main():
     postings = int(lens[pos][hit].sum()) if len(sidx.dims) else 0
     alg_bytes = nq * (idx.n * npairs + K * 16) + 8 * postings
     s1_ms = ktimes.get("stage1")
+    per_query_bytes = (idx.n * npairs + K * 16) + 8 * postings / max(nq, 1)
     roof = None
     if s1_ms:
         achieved = alg_bytes / (s1_ms / 1e3) / 1e9
@@ -390,6 +416,11 @@ def main():
                 "alg_bytes_per_launch": alg_bytes,
                 "note": "alg bytes = Q*(N*ceil(K/2) codes + K*16 LUT) + 8 B/posting; Qb=1 "
                         "(each query streams the codes; repeats hit L2)"}
+        if qb1:
+            a1 = per_query_bytes / (qb1 / 1e3) / 1e9
+            roof["qb1"] = {"stage1_ms": qb1, "alg_bytes": per_query_bytes, "achieved": a1,
+                           "frac": a1 / peak,
+                           "note": "one query per launch, L2 flushed before each launch"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
