@@ -133,20 +133,156 @@ struct Smem {
   int* ctl;         // [0]=cnt [2]=have_th [4..12]=warp sums
 };
 
+// Order-preserving 64-bit key of an f64 score (-0.0 folded into +0.0: the
+// reference compares them equal and breaks the tie by id).
+__device__ __forceinline__ unsigned long long score_key(double x) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(x + 0.0);
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+
+// Warp 0 helper: among 256 bins, walking bins in the given direction (desc =
+// from 255 down), find the bin where the running count reaches `need`.
+// Writes bin, the count still needed inside it, and the bin's size to ctl[12..14].
+__device__ __forceinline__ void find_bin(const unsigned* hist, int need, bool desc, int* out) {
+  const int lane = threadIdx.x & 31;
+  unsigned c[8];
+  unsigned tot = 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const int bin = desc ? 255 - (lane * 8 + j) : lane * 8 + j;
+    c[j] = hist[bin];
+    tot += c[j];
+  }
+  unsigned incl = tot;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  const unsigned excl = incl - tot;
+  const bool here = excl < (unsigned)need && incl >= (unsigned)need;
+  if (here) {
+    unsigned run = excl;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      if (run + c[j] >= (unsigned)need) {
+        out[0] = desc ? 255 - (lane * 8 + j) : lane * 8 + j;
+        out[1] = need - (int)run;
+        out[2] = (int)c[j];
+        break;
+      }
+      run += c[j];
+    }
+  }
+}
+
+// Keep the best k of buf[0..cnt) by (score desc, original id asc) and set the
+// running threshold to the k-th best.  Radix select over the score key (8-bit
+// digits, early exit when a whole bin is taken) then, for exact score ties at
+// the boundary, over the id; in-place order-preserving compaction.  O(cnt)
+// per digit — replaces a bitonic sort of the whole buffer.  The shared-memory
+// chunk accumulator is free at this point and holds the 256-bin histogram.
 __device__ void compact(Smem& s, int k) {
   const int cnt = s.ctl[0];
-  int P = 1;
-  while (P < cnt) P <<= 1;
-  for (int i = cnt + threadIdx.x; i < P; i += blockDim.x) s.buf[i] = worst_cand();
-  __syncthreads();
-  bitonic_sort_block(s.buf, P);
-  if (threadIdx.x == 0) {
-    const int keep = cnt < k ? cnt : k;
-    s.ctl[0] = keep;
-    if (keep == k && k > 0) {
-      *s.th = s.buf[k - 1];
-      s.ctl[2] = 1;
+  __syncthreads();  // every thread has read ctl[0]
+  if (cnt <= k) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  unsigned* hist = reinterpret_cast<unsigned*>(s.acc);
+  unsigned long long prefix = 0, pmask = 0;
+  int need = k;
+  bool whole_bin = false;
+  for (int shift = 56; shift >= 0; shift -= 8) {
+    for (int i = tid; i < 256; i += blockDim.x) hist[i] = 0;
+    __syncthreads();
+    for (int i = tid; i < cnt; i += blockDim.x) {
+      const unsigned long long key = score_key(s.buf[i].s);
+      if ((key & pmask) == prefix) atomicAdd(&hist[(key >> shift) & 255], 1u);
     }
+    __syncthreads();
+    if (warp == 0) find_bin(hist, need, true, s.ctl + 12);
+    __syncthreads();
+    const int b = s.ctl[12];
+    need = s.ctl[13];
+    prefix |= (unsigned long long)b << shift;
+    pmask |= 0xFFull << shift;
+    whole_bin = s.ctl[14] == need;
+    __syncthreads();
+    if (whole_bin) break;
+  }
+  // boundary ties in score: the `need` smallest ids among key == prefix
+  uint32_t tie_lim = 0xFFFFFFFFu;
+  if (!whole_bin) {
+    uint32_t tpre = 0, tmask = 0;
+    int tneed = need;
+    for (int shift = 24; shift >= 0; shift -= 8) {
+      for (int i = tid; i < 256; i += blockDim.x) hist[i] = 0;
+      __syncthreads();
+      for (int i = tid; i < cnt; i += blockDim.x) {
+        const Cand e = s.buf[i];
+        if (score_key(e.s) == prefix && (e.tie & tmask) == tpre)
+          atomicAdd(&hist[(e.tie >> shift) & 255], 1u);
+      }
+      __syncthreads();
+      if (warp == 0) find_bin(hist, tneed, false, s.ctl + 12);
+      __syncthreads();
+      tpre |= (uint32_t)s.ctl[12] << shift;
+      tmask |= 0xFFu << shift;
+      tneed = s.ctl[13];
+      __syncthreads();
+    }
+    tie_lim = tpre;
+  }
+  // in-place compaction (ranks never exceed indices) + worst kept entry
+  Cand worst;
+  worst.s = INFINITY;
+  worst.tie = 0;
+  worst.slot = 0;
+  int kept = 0;
+  for (int base = 0; base < cnt; base += blockDim.x) {
+    const int i = base + tid;
+    Cand e;
+    bool keep = false;
+    if (i < cnt) {
+      e = s.buf[i];
+      const unsigned long long key = score_key(e.s) & pmask;
+      keep = key > prefix || (key == prefix && (whole_bin || e.tie <= tie_lim));
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, keep);
+    if (lane == 0) s.ctl[4 + warp] = __popc(bal);
+    __syncthreads();
+    int before = 0, total = 0;
+#pragma unroll
+    for (int w = 0; w < kThreads / 32; ++w) {
+      const int c = s.ctl[4 + w];
+      before += (w < warp) ? c : 0;
+      total += c;
+    }
+    if (keep) {
+      s.buf[kept + before + __popc(bal & ((1u << lane) - 1u))] = e;
+      if (better(worst, e)) worst = e;
+    }
+    kept += total;
+    __syncthreads();
+  }
+  // block min of the kept entries -> threshold
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    Cand o_;
+    o_.s = __shfl_xor_sync(0xffffffffu, worst.s, o);
+    o_.tie = __shfl_xor_sync(0xffffffffu, worst.tie, o);
+    o_.slot = 0;
+    if (better(worst, o_)) worst = o_;
+  }
+  Cand* wbuf = reinterpret_cast<Cand*>(s.acc);  // histogram no longer needed
+  if (lane == 0) wbuf[warp] = worst;
+  __syncthreads();
+  if (tid == 0) {
+    Cand w = wbuf[0];
+    for (int i = 1; i < kThreads / 32; ++i)
+      if (better(w, wbuf[i])) w = wbuf[i];
+    *s.th = w;
+    s.ctl[0] = kept;
+    s.ctl[2] = 1;
   }
   __syncthreads();
 }
@@ -174,7 +310,7 @@ __device__ __forceinline__ void accum32(uint32_t* acc2, const uint32_t* r, const
   }
 }
 
-__global__ void __launch_bounds__(kThreads) k_stage1(Stage1Args a) {
+__global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int64_t q = blockIdx.x;
   const int tile = blockIdx.y;
@@ -256,10 +392,19 @@ __global__ void __launch_bounds__(kThreads) k_stage1(Stage1Args a) {
       int k = 0;
       for (int kb = 0; kb < a.K; kb += 256) {
         const int kend = min(a.K, kb + 256);
+        uint2 wn[8];
+        if (k + 8 <= kend) {
+#pragma unroll
+          for (int u = 0; u < 8; ++u) wn[u] = __ldg(col + (int64_t)(k + u) * vrow);
+        }
         for (; k + 8 <= kend; k += 8) {
           uint2 w[8];
 #pragma unroll
-          for (int u = 0; u < 8; ++u) w[u] = __ldg(col + (int64_t)(k + u) * vrow);
+          for (int u = 0; u < 8; ++u) w[u] = wn[u];
+          if (k + 16 <= kend) {  // prefetch the next group while this one computes
+#pragma unroll
+            for (int u = 0; u < 8; ++u) wn[u] = __ldg(col + (int64_t)(k + 8 + u) * vrow);
+          }
 #pragma unroll
           for (int u = 0; u < 8; u += 2) {
             const uint4 T0 = s.lut[k + u], T1 = s.lut[k + u + 1];
@@ -514,7 +659,7 @@ __global__ void __launch_bounds__(kThreads) k_stage1(Stage1Args a) {
     return;
   }
   if (a.mode != S1_SELECT) return;
-  compact(s, a.k);
+  compact(s, a.k);  // best k of the tile, unordered (the merge sorts)
   Cand* o = a.out + (q * a.ntiles + tile) * a.out_per_tile;
   const int keep = s.ctl[0];
   for (int i = tid; i < a.out_per_tile; i += blockDim.x) o[i] = i < keep ? s.buf[i] : worst_cand();
