@@ -7,6 +7,7 @@
 //   select (merge tiles to the top k1) -> stage2 -> stage3 -> outputs,
 // all enqueued on the index's stream with no host round trip between stages.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <vector>
@@ -20,6 +21,11 @@ void set_error(const std::string& msg) { g_err = msg; }
 const char* last_error() { return g_err.c_str(); }
 
 namespace {
+
+bool getenv_flag(const char* name) {
+  const char* e = getenv(name);
+  return e && e[0] && e[0] != '0';
+}
 
 template <typename T>
 int dalloc(DeviceIndex& ix, T** p, size_t count) {
@@ -54,7 +60,7 @@ void free_device_arrays(DeviceIndex* ix) {
                   ix->res_indices, ix->res_data, ix->subdims,  ix->dim_off,    ix->cen_off,
                   ix->centers,  ix->vcodes,     ix->sq_lo,    ix->sq_step,    ix->sq_codes,
                   ix->wh_mean,  ix->wh_inv_t,   ix->ds_dense, ix->ds_indptr,  ix->ds_indices,
-                  ix->ds_data,  ix->scratch};
+                  ix->ds_data,  ix->scratch,    ix->skip_row, ix->skip};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (ix->stream) cudaStreamDestroy(ix->stream);
@@ -140,7 +146,9 @@ struct Timer {
       } else {
         ix->tms[it - ix->tnames.begin()] += ms;
       }
-      if (nm == "map_dims" || nm == "lut_build" || nm == "stage1" || nm == "merge") st3[0] += ms;
+      if (nm == "map_dims" || nm == "lut_build" || nm == "sparse_bucket" || nm == "stage1" ||
+          nm == "merge")
+        st3[0] += ms;
       else if (nm == "stage2") st3[1] += ms;
       else if (nm == "stage3") st3[2] += ms;
     }
@@ -183,12 +191,16 @@ int run_search(DeviceIndex& ix, const hs_query_batch& qb, int64_t nnz, int max_q
   }
   const int64_t d = ix.d_dense;
   const int Kp16 = ix.Kp * 16;
+  const int64_t nchunks = ceil_div(ix.n, stage1_chunk_points());
+  const int64_t capq = bucket_capacity(ix);
+  const bool use_buckets = nnz > 0 && ix.nnz_post > 0 && !getenv_flag("HSB200_NO_BUCKETS");
   size_t need = 0;
   {
     Arena a{nullptr};
     a.take<uint32_t>(nnz + 1);
     a.take<uint32_t>(nnz + 1);
     a.take<double>(nnz + 1);
+    a.take<int32_t>(nnz + 1);
     a.take<double>(QB * d + 1);
     a.take<double>(QB * d + 1);
     a.take<uint8_t>(QB * Kp16 + 16);
@@ -199,6 +211,12 @@ int run_search(DeviceIndex& ix, const hs_query_batch& qb, int64_t nnz, int max_q
     a.take<Cand>((size_t)s1_entries + 1);
     a.take<Cand>(QB * sz.k1 + 1);
     a.take<Cand>(QB * sz.k2 + 1);
+    if (use_buckets) {
+      a.take<int>(QB);
+      a.take<uint32_t>(QB * (nchunks + 1));
+      a.take<uint32_t>(QB * capq);
+      a.take<double>(QB * capq);
+    }
     need = a.off + 1024;
   }
   HS_CHECK(ensure_scratch(ix, need));
@@ -206,6 +224,7 @@ int run_search(DeviceIndex& ix, const hs_query_batch& qb, int64_t nnz, int max_q
   uint32_t* lbeg = a.take<uint32_t>(nnz + 1);
   uint32_t* lend = a.take<uint32_t>(nnz + 1);
   double* qv = a.take<double>(nnz + 1);
+  int32_t* lidx = a.take<int32_t>(nnz + 1);
   double* qd = a.take<double>(QB * d + 1);
   double* qw = a.take<double>(QB * d + 1);
   uint8_t* luts = a.take<uint8_t>(QB * Kp16 + 16);
@@ -216,6 +235,15 @@ int run_search(DeviceIndex& ix, const hs_query_batch& qb, int64_t nnz, int max_q
   Cand* s1out = a.take<Cand>((size_t)s1_entries + 1);
   Cand* cand1 = a.take<Cand>(QB * sz.k1 + 1);
   Cand* cand2 = a.take<Cand>(QB * sz.k2 + 1);
+  SparseBuckets sb;
+  if (use_buckets) {
+    sb.mode = a.take<int>(QB);
+    sb.boff = a.take<uint32_t>(QB * (nchunks + 1));
+    sb.slots = a.take<uint32_t>(QB * capq);
+    sb.vals = a.take<double>(QB * capq);
+    sb.capq = capq;
+    sb.nchunks = (int)nchunks;
+  }
 
   if (tm) tm->mark("begin");
   QueryView all;
@@ -224,7 +252,7 @@ int run_search(DeviceIndex& ix, const hs_query_batch& qb, int64_t nnz, int max_q
   all.sp_dims = qb.sp_dims;
   all.sp_vals = qb.sp_vals;
   all.dense = qb.dense;
-  launch_map_dims(ix, all, nnz, true, lbeg, lend, qv, st);
+  launch_map_dims(ix, all, nnz, true, lbeg, lend, qv, lidx, st);
   ix.launches += nnz > 0 ? 1 : 0;
   if (tm) tm->mark("map_dims");
   if (d > 0) HS_CUDA(cudaMemsetAsync(bad, 0, sizeof(int) * QB, st));
@@ -245,8 +273,15 @@ int run_search(DeviceIndex& ix, const hs_query_batch& qb, int64_t nnz, int max_q
     } else if (params->exact_final_rerank) {
       // no dense part: qd unused
     }
+    if (use_buckets) {
+      launch_sparse_bucket(ix, qc, lbeg, lend, qv, sb, st);
+      HS_CUDA(cudaGetLastError());
+      ix.launches += 1;
+      if (tm) tm->mark("sparse_bucket");
+    }
     ix.launches += (d > 0 ? 1 : 0) + 4;  // lut_build, stage1, merge, stage2, stage3
-    HS_CHECK(launch_stage1(ix, qc, pc, lbeg, lend, qv, luts, btot, scl, off, s1out, nullptr, st));
+    HS_CHECK(launch_stage1(ix, qc, pc, lbeg, lend, qv, lidx, luts, btot, scl, off, s1out, nullptr, st,
+                           nullptr, false, use_buckets ? &sb : nullptr));
     if (tm) tm->mark("stage1");
     HS_CHECK(launch_select_topk(s1out, nqc, (int64_t)pc.ntiles * pc.out_per_tile, sz.k1, cand1, st));
     if (tm) tm->mark("merge");
@@ -420,6 +455,7 @@ int hs_index_create(const hs_index_desc* ds, int device, hs_index_t* out) {
       HS_CHECK(dalloc(*ix, &ix->post, 1));
     }
   }
+  if (nnz_post) HS_CHECK(build_skip_tables(*ix, ds->post_ptr));
   // sparse residual
   if (ds->res_indptr && n) {
     ix->res_nnz = ds->res_indptr[n] - ds->res_indptr[0];
@@ -678,7 +714,7 @@ int hs_lut16_scan(const uint8_t* packed, int64_t n, int32_t K, const uint8_t* qt
   qv.nq = nq;
   qv.sp_indptr = dptr;
   Stage1Plan p = plan_stage1(*ix, nq, 1, 1, S1_DUMP);
-  HS_CHECK(launch_stage1(*ix, qv, p, nullptr, nullptr, nullptr, dl, dbt, dsc2, nullptr, nullptr,
+  HS_CHECK(launch_stage1(*ix, qv, p, nullptr, nullptr, nullptr, nullptr, dl, dbt, dsc2, nullptr, nullptr,
                          dout, ix->stream, dtot, true));
   HS_CUDA(cudaStreamSynchronize(ix->stream));
   HS_CUDA(cudaMemcpy(scores, dout, sizeof(double) * nq * n, cudaMemcpyDeviceToHost));
@@ -703,9 +739,11 @@ static int stage1_dump(hs_index_t index, const hs_query_batch* queries, double* 
   double *qv, *qd, *qw, *bt, *sc, *of, *dump;
   uint8_t* luts;
   int* bad;
+  int32_t* lidx;
   HS_CHECK(dalloc(tmp, &lb, dq.nnz + 1));
   HS_CHECK(dalloc(tmp, &le, dq.nnz + 1));
   HS_CHECK(dalloc(tmp, &qv, dq.nnz + 1));
+  HS_CHECK(dalloc(tmp, &lidx, dq.nnz + 1));
   HS_CHECK(dalloc(tmp, &qd, nq * d + 1));
   HS_CHECK(dalloc(tmp, &qw, nq * d + 1));
   HS_CHECK(dalloc(tmp, &luts, nq * index->Kp * 16 + 16));
@@ -721,19 +759,33 @@ static int stage1_dump(hs_index_t index, const hs_query_batch* queries, double* 
   qvw.sp_dims = dq.b.sp_dims;
   qvw.sp_vals = dq.b.sp_vals;
   qvw.dense = dq.b.dense;
-  launch_map_dims(*index, qvw, dq.nnz, !raw_acc, lb, le, qv, index->stream);
+  launch_map_dims(*index, qvw, dq.nnz, !raw_acc, lb, le, qv, lidx, index->stream);
   if (!raw_acc && d > 0)
     launch_lut_build(*index, qvw.dense, nq, qd, qw, luts, bt, sc, of, bad, index->stream);
   Stage1Plan p = plan_stage1(*index, nq, 1, dq.max_row, S1_DUMP);
   p.sparse_only_acc = raw_acc;
-  HS_CHECK(launch_stage1(*index, qvw, p, lb, le, qv, luts, bt, sc, of, nullptr, dump,
-                         index->stream));
+  SparseBuckets sb;
+  const bool use_buckets = dq.nnz > 0 && index->nnz_post > 0 && !getenv_flag("HSB200_NO_BUCKETS");
+  if (use_buckets) {
+    sb.nchunks = (int)ceil_div(n, stage1_chunk_points());
+    sb.capq = bucket_capacity(*index);
+    HS_CHECK(dalloc(tmp, &sb.mode, nq));
+    HS_CHECK(dalloc(tmp, &sb.boff, nq * (sb.nchunks + 1)));
+    HS_CHECK(dalloc(tmp, &sb.slots, nq * sb.capq));
+    HS_CHECK(dalloc(tmp, &sb.vals, nq * sb.capq));
+    launch_sparse_bucket(*index, qvw, lb, le, qv, sb, index->stream);
+  }
+  HS_CHECK(launch_stage1(*index, qvw, p, lb, le, qv, lidx, luts, bt, sc, of, nullptr, dump,
+                         index->stream, nullptr, false, use_buckets ? &sb : nullptr));
   HS_CUDA(cudaStreamSynchronize(index->stream));
   std::vector<int> hbad(nq);
   HS_CUDA(cudaMemcpy(hbad.data(), bad, sizeof(int) * nq, cudaMemcpyDeviceToHost));
   HS_CUDA(cudaMemcpy(out, dump, sizeof(double) * nq * n, cudaMemcpyDeviceToHost));
-  cudaFree(lb); cudaFree(le); cudaFree(qv); cudaFree(qd); cudaFree(qw); cudaFree(luts);
+  cudaFree(lb); cudaFree(le); cudaFree(qv); cudaFree(lidx); cudaFree(qd); cudaFree(qw); cudaFree(luts);
   cudaFree(bt); cudaFree(sc); cudaFree(of); cudaFree(bad); cudaFree(dump);
+  if (use_buckets) {
+    cudaFree(sb.mode); cudaFree(sb.boff); cudaFree(sb.slots); cudaFree(sb.vals);
+  }
   for (int64_t i = 0; i < nq; ++i)
     if (hbad[i]) HS_FAIL(HS_EINVAL, "lookup table contains non-finite values");
   return HS_OK;

@@ -23,6 +23,12 @@ struct DeviceIndex {
   uint32_t* post_dims = nullptr;  // [n_active]
   uint32_t* post_ptr = nullptr;   // [n_active+1] (nnz_post < 2^32)
   uint2* post = nullptr;          // [nnz_post] {id, __float_as_uint(w)}
+  // chunk skip tables of long lists: skip_row[list] = row index or -1;
+  // row r holds, for every 4096-slot chunk c, the list-relative position of
+  // the first posting with id >= 4096*c (nchunks+1 entries)
+  int32_t* skip_row = nullptr;    // [n_active]
+  uint32_t* skip = nullptr;       // [n_long][nchunks+1]
+  int64_t n_long = 0;
 
   // forward sparse residual (layout order)
   int64_t res_nnz = 0;
@@ -101,6 +107,22 @@ struct Stage1Plan {
   bool use_dense = true;  // DUMP: include the dense part
   bool sparse_only_acc = false;  // DUMP: raw accumulator (no weights, no dense)
 };
+// per-query postings bucketed by 4096-slot chunk (stable: ascending dim then
+// slot inside a bucket) with exact f64 products; mode[q] = 1 when query q
+// uses the buckets, 0 when it streams its lists in stage 1
+struct SparseBuckets {
+  int* mode = nullptr;       // [nq]
+  uint32_t* boff = nullptr;  // [nq][nchunks+1]
+  uint32_t* slots = nullptr; // [nq][capq]
+  double* vals = nullptr;    // [nq][capq]
+  int64_t capq = 0;
+  int nchunks = 0;
+};
+int64_t bucket_capacity(const DeviceIndex& ix);
+int build_skip_tables(DeviceIndex& ix, const int64_t* host_ptr);
+void launch_sparse_bucket(const DeviceIndex& ix, const QueryView& q, const uint32_t* lbeg,
+                          const uint32_t* lend, const double* qv, const SparseBuckets& sb,
+                          cudaStream_t st);
 int stage1_chunk_points();
 int64_t vertical_stride(int64_t n);
 void launch_to_vertical(const uint8_t* packed, int64_t n, int K, int64_t vstride, uint32_t* v,
@@ -108,12 +130,14 @@ void launch_to_vertical(const uint8_t* packed, int64_t n, int K, int64_t vstride
 Stage1Plan plan_stage1(const DeviceIndex& ix, int64_t nq, int64_t k, int max_qnnz, int mode);
 size_t stage1_smem_bytes(const DeviceIndex& ix, const Stage1Plan& p);
 void launch_map_dims(const DeviceIndex& ix, const QueryView& q, int64_t nnz, bool use_weight,
-                     uint32_t* lbeg, uint32_t* lend, double* qv, cudaStream_t st);
+                     uint32_t* lbeg, uint32_t* lend, double* qv, int32_t* lidx,
+                     cudaStream_t st);
 int launch_stage1(const DeviceIndex& ix, const QueryView& q, const Stage1Plan& p,
                   const uint32_t* lbeg, const uint32_t* lend, const double* qv,
-                  const uint8_t* luts, const double* bias_total, const double* scale,
+                  const int32_t* lidx, const uint8_t* luts, const double* bias_total, const double* scale,
                   const double* offset, Cand* out, double* dump, cudaStream_t st,
-                  uint32_t* dump_tot = nullptr, bool raw_dense = false);
+                  uint32_t* dump_tot = nullptr, bool raw_dense = false,
+                  const SparseBuckets* sb = nullptr);
 
 // select.cu
 int launch_select_topk(const Cand* in, int64_t nq, int64_t m, int64_t k, Cand* out,

@@ -28,7 +28,9 @@
 //   3. score = acc + ((bias_total + scale*total) + offset), unfused f64.
 //   4. offer to a shared-memory candidate buffer guarded by the running k-th
 //      best (score desc, original id asc); overflow => bitonic compaction.
+#include <algorithm>
 #include <cstdlib>
+#include <vector>
 
 #include "kernels.cuh"
 
@@ -55,6 +57,7 @@ struct Stage1Args {
   const uint32_t* lbeg;
   const uint32_t* lend;
   const double* qv;
+  const int32_t* lidx;
   // dense
   int has_dense;
   int K, Kp;
@@ -71,6 +74,17 @@ struct Stage1Args {
   uint32_t* dump_tot;  // DUMP: integer totals (optional)
   int raw_dense;       // DUMP: bias_total + scale*total only (lut16_scan semantics)
   int max_qnnz;
+  // bucketed postings (SparseBuckets); bmode == nullptr => stream every query
+  const int* bmode;
+  const uint32_t* boff;
+  const uint32_t* bslots;
+  const double* bvals;
+  int64_t capq;
+  int nchunks_g;
+  // skip tables (long lists)
+  const int32_t* skip_row;
+  const uint32_t* skip;
+  int nchunks_all;
   int exp_flags;       // dev experiments (HSB200_EXP): 1 no dense, 2 no sparse, 4 no offers
 };
 
@@ -130,6 +144,8 @@ struct Smem {
   uint32_t* alist;  // active dims of the chunk (ascending)
   uint32_t* abase;  // their slice start
   uint32_t* acnt;   // their slice length
+  int32_t* dskip;   // skip-table row of the dim's list, -1 if short
+  uint32_t* dbeg;   // list begin (absolute posting index)
   int* ctl;         // [0]=cnt [2]=have_th [4..12]=warp sums
 };
 
@@ -342,6 +358,10 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
   p += sizeof(uint32_t) * a.max_qnnz;
   s.acnt = reinterpret_cast<uint32_t*>(p);
   p += sizeof(uint32_t) * a.max_qnnz;
+  s.dskip = reinterpret_cast<int32_t*>(p);
+  p += sizeof(int32_t) * a.max_qnnz;
+  s.dbeg = reinterpret_cast<uint32_t*>(p);
+  p += sizeof(uint32_t) * a.max_qnnz;
   s.ctl = reinterpret_cast<int*>(p);
 
   const int64_t tile_lo = (int64_t)tile * a.tile_pts;
@@ -349,16 +369,29 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
 
   // ---- per-query setup ----
   const int64_t qb = a.qptr[q], qe = a.qptr[q + 1];
-  const int nd = (int)(qe - qb);
+  const bool bucketed = a.bmode != nullptr && a.bmode[q] == 1;
+  const int nd = bucketed ? 0 : (int)(qe - qb);  // bucketed queries skip the cursors
   HS_DCHECK(nd >= 0 && nd <= a.max_qnnz);
+  const uint32_t* qboff = bucketed ? a.boff + q * (int64_t)(a.nchunks_g + 1) : nullptr;
+  const uint32_t* qslots = bucketed ? a.bslots + q * a.capq : nullptr;
+  const double* qvals = bucketed ? a.bvals + q * a.capq : nullptr;
   for (int d = tid; d < nd; d += blockDim.x) {
     const uint32_t b = a.lbeg[qb + d], e = a.lend[qb + d];
     HS_DCHECK(b <= e);
-    const uint32_t c = lower_bound_ids(a.post, b, e, (uint32_t)tile_lo);
+    const int32_t li = a.lidx ? a.lidx[qb + d] : -1;
+    const int32_t row = (li >= 0 && a.skip_row) ? a.skip_row[li] : -1;
     s.dqv[d] = a.qv[qb + d];
-    s.dcur[d] = c;
+    s.dskip[d] = row;
+    s.dbeg[d] = b;
     s.dend[d] = e;
-    s.dnext[d] = c < e ? __ldg(&a.post[c].x) : 0xFFFFFFFFu;
+    if (row < 0) {  // short list: cursor + next id
+      const uint32_t c = lower_bound_ids(a.post, b, e, (uint32_t)tile_lo);
+      s.dcur[d] = c;
+      s.dnext[d] = c < e ? __ldg(&a.post[c].x) : 0xFFFFFFFFu;
+    } else {
+      s.dcur[d] = b;
+      s.dnext[d] = 0xFFFFFFFFu;
+    }
   }
   if (a.has_dense) {
     const uint4* src = reinterpret_cast<const uint4*>(a.luts + q * (int64_t)a.Kp * 16);
@@ -437,93 +470,162 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
       }
     }
 
-    // ---- sparse: active dims of this chunk, in ascending dim order ----
+    // ---- sparse: bucketed postings of this chunk (pre-pass) ----
     int nact = 0, npost = 0;
-    for (int base = 0; base < nd; base += blockDim.x) {
-      const int d = base + tid;
-      const bool f = d < nd && s.dnext[d] < (uint32_t)ce && !(a.exp_flags & 2);
-      const unsigned bal = __ballot_sync(0xffffffffu, f);
-      if (lane == 0) s.ctl[4 + warp] = __popc(bal);
-      __syncthreads();
-      int before = 0, total = 0;
+    if (bucketed) {
+      const int64_t cg = cb / kChunk;
+      const uint32_t e0 = __ldg(qboff + cg), e1 = __ldg(qboff + cg + 1);
+      if (e1 > e0) {
+        // each thread walks the (short) bucket and adds to its own 16 points;
+        // bucket order is ascending dim per point => reference summation order
+        double* mine = s.acc + tid * kPPT;
 #pragma unroll
-      for (int i = 0; i < kThreads / 32; ++i) {
-        const int c = s.ctl[4 + i];
-        before += (i < warp) ? c : 0;
-        total += c;
-      }
-      if (f) {
-        const int slot = nact + before + __popc(bal & ((1u << lane) - 1u));
-        HS_DCHECK(slot < a.max_qnnz);
-        const uint32_t cur = s.dcur[d], end = s.dend[d];
-        HS_DCHECK(cur < end);
-        HS_DCHECK(__ldg(&a.post[cur].x) == s.dnext[d]);
-        HS_DCHECK(s.dnext[d] >= (uint32_t)cb);
-        const uint32_t cnt = count_below_known(a.post, cur, end, (uint32_t)ce);
-        HS_DCHECK(cnt >= 1 && __ldg(&a.post[cur + cnt - 1].x) < (uint32_t)ce);
-        const uint32_t nc = cur + cnt;
-        s.alist[slot] = d;
-        s.abase[slot] = cur;
-        s.acnt[slot] = cnt;
-        s.dcur[d] = nc;
-        s.dnext[d] = nc < end ? __ldg(&a.post[nc].x) : 0xFFFFFFFFu;
-      }
-      nact += total;
-      __syncthreads();
-    }
-    if (nact > 0) {
-      int mine = 0;
-      for (int i = tid; i < nact; i += blockDim.x) mine += (int)s.acnt[i];
-      npost = block_sum(mine, s.ctl + 4);
-    }
-#ifdef HS_DEBUG
-    for (int i = tid; i < nact; i += blockDim.x) {
-      const uint32_t id0 = __ldg(&a.post[s.abase[i]].x);
-      if (!(id0 >= (uint32_t)cb && id0 < (uint32_t)ce))
-        printf("STALE q=%d i=%d nact=%d d=%u base=%u cnt=%u id0=%u cb=%lld ctlw=%d,%d,%d,%d,%d,%d,%d,%d\n",
-               (int)q, i, nact, s.alist[i], s.abase[i], s.acnt[i], id0, (long long)cb, s.ctl[4],
-               s.ctl[5], s.ctl[6], s.ctl[7], s.ctl[8], s.ctl[9], s.ctl[10], s.ctl[11]);
-    }
-    __syncthreads();
-#endif
-    if (nact > 0 && npost <= kSmallPostings) {
-      // few postings: every thread walks them all in dim order (broadcast
-      // loads) and adds only those landing on its own 16 points — per-point
-      // order stays ascending in dim with no block barriers
-      double* mine = s.acc + tid * kPPT;
-#pragma unroll
-      for (int j = 0; j < kPPT; ++j) mine[j] = 0.0;
-      for (int i = 0; i < nact; ++i) {
-        const uint32_t b = s.abase[i], c = s.acnt[i];
-        const double qv = s.dqv[s.alist[i]];
-        for (uint32_t j = 0; j < c; ++j) {
-          const uint2 pw = __ldg(&a.post[b + j]);
-          const uint32_t local = pw.x - (uint32_t)cb;
+        for (int j = 0; j < kPPT; ++j) mine[j] = 0.0;
+        for (uint32_t e = e0; e < e1; ++e) {
+          const uint32_t local = __ldg(qslots + e) - (uint32_t)cb;
           HS_DCHECK(local < (uint32_t)kChunk);
-          if ((local >> 4) == (uint32_t)tid) mine[local & 15] += qv * (double)__uint_as_float(pw.y);
+          if ((local >> 4) == (uint32_t)tid) mine[local & 15] += __ldg(qvals + e);
         }
+        nact = 1;
+        npost = 0;
       }
-    } else if (nact > 0) {
-      for (int i = tid; i < kChunk; i += blockDim.x) s.acc[i] = 0.0;
-      __syncthreads();
-      for (int i = 0; i < nact; ++i) {
-        const uint32_t b = s.abase[i], c = s.acnt[i];
-        const double qv = s.dqv[s.alist[i]];
-        for (uint32_t j = tid; j < c; j += blockDim.x) {
-          const uint2 pw = __ldg(&a.post[b + j]);
-#ifdef HS_DEBUG
-          if (!(pw.x >= cb && pw.x < ce)) {
-            if (j == tid && tid < 2)
-              printf("BADSLICE q=%d tile=%d i=%d nact=%d d=%u b=%u c=%u j=%u id=%u cb=%lld ce=%lld nd=%d\n",
-                     (int)q, tile, i, nact, s.alist[i], b, c, j, pw.x, (long long)cb,
-                     (long long)ce, nd);
-            __trap();
+    }
+    if (!bucketed) {
+      // ---- sparse: active dims of this chunk, in ascending dim order ----
+      for (int base = 0; base < nd; base += blockDim.x) {
+        const int d = base + tid;
+        int32_t row = -1;
+        uint32_t sk0 = 0, sk1 = 0;
+        if (d < nd) {
+          row = s.dskip[d];
+          if (row >= 0) {
+            const uint32_t* r = a.skip + (int64_t)row * (a.nchunks_all + 1) + cb / kChunk;
+            sk0 = __ldg(r);
+            sk1 = __ldg(r + 1);
           }
-#endif
-          // f64(q) * f64(w) is exact, so contraction cannot change the sum
-          s.acc[pw.x - cb] += qv * (double)__uint_as_float(pw.y);
+        }
+        const bool f = d < nd && (row >= 0 ? sk1 > sk0 : s.dnext[d] < (uint32_t)ce) &&
+                       !(a.exp_flags & 2);
+        const unsigned bal = __ballot_sync(0xffffffffu, f);
+        if (lane == 0) s.ctl[4 + warp] = __popc(bal);
+        __syncthreads();
+        int before = 0, total = 0;
+  #pragma unroll
+        for (int i = 0; i < kThreads / 32; ++i) {
+          const int c = s.ctl[4 + i];
+          before += (i < warp) ? c : 0;
+          total += c;
+        }
+        if (f) {
+          const int slot = nact + before + __popc(bal & ((1u << lane) - 1u));
+          HS_DCHECK(slot < a.max_qnnz);
+          s.alist[slot] = d;
+          if (row >= 0) {
+            s.abase[slot] = s.dbeg[d] + sk0;
+            s.acnt[slot] = sk1 - sk0;
+          } else {
+            const uint32_t cur = s.dcur[d], end = s.dend[d];
+            HS_DCHECK(cur < end);
+            HS_DCHECK(__ldg(&a.post[cur].x) == s.dnext[d]);
+            HS_DCHECK(s.dnext[d] >= (uint32_t)cb);
+            const uint32_t cnt = count_below_known(a.post, cur, end, (uint32_t)ce);
+            HS_DCHECK(cnt >= 1 && __ldg(&a.post[cur + cnt - 1].x) < (uint32_t)ce);
+            const uint32_t nc = cur + cnt;
+            s.abase[slot] = cur;
+            s.acnt[slot] = cnt;
+            s.dcur[d] = nc;
+            s.dnext[d] = nc < end ? __ldg(&a.post[nc].x) : 0xFFFFFFFFu;
+          }
+        }
+        nact += total;
+        __syncthreads();
+      }
+      if (nact > 0) {
+        int mine = 0;
+        for (int i = tid; i < nact; i += blockDim.x) mine += (int)s.acnt[i];
+        npost = block_sum(mine, s.ctl + 4);
+      }
+  #ifdef HS_DEBUG
+      for (int i = tid; i < nact; i += blockDim.x) {
+        const uint32_t id0 = __ldg(&a.post[s.abase[i]].x);
+        if (!(id0 >= (uint32_t)cb && id0 < (uint32_t)ce))
+          printf("STALE q=%d i=%d nact=%d d=%u base=%u cnt=%u id0=%u cb=%lld ctlw=%d,%d,%d,%d,%d,%d,%d,%d\n",
+                 (int)q, i, nact, s.alist[i], s.abase[i], s.acnt[i], id0, (long long)cb, s.ctl[4],
+                 s.ctl[5], s.ctl[6], s.ctl[7], s.ctl[8], s.ctl[9], s.ctl[10], s.ctl[11]);
+      }
+      __syncthreads();
+  #endif
+      if (nact > 0 && npost <= kSmallPostings) {
+        // few postings: every thread walks them all in dim order (broadcast
+        // loads) and adds only those landing on its own 16 points — per-point
+        // order stays ascending in dim with no block barriers
+        double* mine = s.acc + tid * kPPT;
+  #pragma unroll
+        for (int j = 0; j < kPPT; ++j) mine[j] = 0.0;
+        for (int i = 0; i < nact; ++i) {
+          const uint32_t b = s.abase[i], c = s.acnt[i];
+          const double qv = s.dqv[s.alist[i]];
+          for (uint32_t j = 0; j < c; ++j) {
+            const uint2 pw = __ldg(&a.post[b + j]);
+            const uint32_t local = pw.x - (uint32_t)cb;
+            HS_DCHECK(local < (uint32_t)kChunk);
+            if ((local >> 4) == (uint32_t)tid) mine[local & 15] += qv * (double)__uint_as_float(pw.y);
+          }
+        }
+      } else if (nact > 0) {
+        // many postings: block-wide per dim, one barrier between dims; the
+        // next dim's first kPre*256 postings are loaded while this dim adds
+        constexpr int kPre = 4;
+        for (int i = tid; i < kChunk; i += blockDim.x) s.acc[i] = 0.0;
+        uint2 nxt[kPre];
+        {
+          const uint32_t b = s.abase[0], c = s.acnt[0];
+#pragma unroll
+          for (int r = 0; r < kPre; ++r) {
+            const uint32_t j = tid + r * blockDim.x;
+            nxt[r] = j < c ? __ldg(&a.post[b + j]) : make_uint2(0xFFFFFFFFu, 0u);
+          }
         }
         __syncthreads();
+        for (int i = 0; i < nact; ++i) {
+          const uint32_t b = s.abase[i], c = s.acnt[i];
+          const double qv = s.dqv[s.alist[i]];
+          uint2 cur[kPre];
+#pragma unroll
+          for (int r = 0; r < kPre; ++r) cur[r] = nxt[r];
+          if (i + 1 < nact) {
+            const uint32_t b2 = s.abase[i + 1], c2 = s.acnt[i + 1];
+#pragma unroll
+            for (int r = 0; r < kPre; ++r) {
+              const uint32_t j = tid + r * blockDim.x;
+              nxt[r] = j < c2 ? __ldg(&a.post[b2 + j]) : make_uint2(0xFFFFFFFFu, 0u);
+            }
+          }
+#pragma unroll
+          for (int r = 0; r < kPre; ++r) {
+            if (cur[r].x == 0xFFFFFFFFu) continue;
+            HS_DCHECK(cur[r].x >= cb && cur[r].x < ce);
+            // f64(q) * f64(w) is exact, so contraction cannot change the sum
+            s.acc[cur[r].x - cb] += qv * (double)__uint_as_float(cur[r].y);
+          }
+          // long slices: the rest in batches of 8 loads in flight per thread
+          constexpr int kB = 8;
+          for (uint32_t j0 = kPre * blockDim.x; j0 < c; j0 += kB * blockDim.x) {
+            uint2 v[kB];
+#pragma unroll
+            for (int r = 0; r < kB; ++r) {
+              const uint32_t j = j0 + tid + r * blockDim.x;
+              v[r] = j < c ? __ldg(&a.post[b + j]) : make_uint2(0xFFFFFFFFu, 0u);
+            }
+#pragma unroll
+            for (int r = 0; r < kB; ++r) {
+              if (v[r].x == 0xFFFFFFFFu) continue;
+              HS_DCHECK(v[r].x >= cb && v[r].x < ce);
+              s.acc[v[r].x - cb] += qv * (double)__uint_as_float(v[r].y);
+            }
+          }
+          __syncthreads();
+        }
       }
     }
 
@@ -671,7 +773,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
 __global__ void k_map_dims(const uint32_t* __restrict__ dims_q, const float* __restrict__ vals,
                            int64_t nnz, const uint32_t* __restrict__ post_dims, int64_t n_active,
                            const uint32_t* __restrict__ post_ptr, float weight, int use_weight,
-                           uint32_t* lbeg, uint32_t* lend, double* qv) {
+                           uint32_t* lbeg, uint32_t* lend, double* qv, int32_t* lidx) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nnz) return;
   const uint32_t dim = dims_q[i];
@@ -684,12 +786,147 @@ __global__ void k_map_dims(const uint32_t* __restrict__ dims_q, const float* __r
   if (lo < n_active && post_dims[lo] == dim) {
     lbeg[i] = post_ptr[lo];
     lend[i] = post_ptr[lo + 1];
+    lidx[i] = (int32_t)lo;
   } else {
     lbeg[i] = 0;
     lend[i] = 0;
+    lidx[i] = -1;
   }
   const float v = use_weight ? __fmul_rn(vals[i], weight) : vals[i];
   qv[i] = (double)v;
+}
+
+// ---------------------------------------------------------------------------
+// Sparse pre-pass: bucket one query's postings by 4096-slot chunk.
+// Counting sort on the chunk id; dims are scattered one after another (in the
+// query's ascending dim order) and, within a dim, runs of equal chunk keep
+// their ascending slots, so every bucket lists each point's postings in
+// ascending dim order — the reference's summation order (sparse.py:277-282).
+// ---------------------------------------------------------------------------
+constexpr int kBucketThreads = 256;
+
+__device__ __forceinline__ int block_max_scan(int v, int* scratch) {
+  // inclusive max-scan over the block in thread order
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int u = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v = max(v, u);
+  }
+  if (lane == 31) scratch[warp] = v;
+  __syncthreads();
+  int pre = -1;
+  for (int w = 0; w < warp; ++w) pre = max(pre, scratch[w]);
+  __syncthreads();
+  return max(v, pre);
+}
+
+__global__ void __launch_bounds__(kBucketThreads) k_sparse_bucket(
+    const int64_t* __restrict__ qptr, const uint32_t* __restrict__ lbeg,
+    const uint32_t* __restrict__ lend, const double* __restrict__ qv,
+    const uint2* __restrict__ post, int nchunks, int64_t capq, int* __restrict__ mode,
+    uint32_t* __restrict__ boff, uint32_t* __restrict__ slots, double* __restrict__ vals) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(smem_raw);  // [nchunks] hist -> cursor
+  int* scr = reinterpret_cast<int*>(cnt + nchunks + 1);     // [32]
+  const int64_t q = blockIdx.x;
+  const int tid = threadIdx.x;
+  const int64_t qb = qptr[q];
+  const int nd = (int)(qptr[q + 1] - qb);
+  int mine = 0;
+  for (int d = tid; d < nd; d += blockDim.x) mine += (int)(lend[qb + d] - lbeg[qb + d]);
+  // block sum
+  for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
+  if ((tid & 31) == 0) scr[tid >> 5] = mine;
+  __syncthreads();
+  int64_t E = 0;
+  for (int w = 0; w < kBucketThreads / 32; ++w) E += scr[w];
+  __syncthreads();
+  if (E == 0 || E > capq || E > 96LL * nchunks) {
+    if (tid == 0) mode[q] = 0;  // stream this query's lists in stage 1
+    return;
+  }
+  for (int c = tid; c < nchunks; c += blockDim.x) cnt[c] = 0;
+  __syncthreads();
+  for (int d = 0; d < nd; ++d) {
+    const uint32_t b = lbeg[qb + d], L = lend[qb + d] - b;
+    for (uint32_t j = tid; j < L; j += blockDim.x) atomicAdd(&cnt[__ldg(&post[b + j].x) >> 12], 1u);
+  }
+  __syncthreads();
+  // exclusive scan of the histogram (segment per thread, then across threads)
+  const int per = (nchunks + kBucketThreads - 1) / kBucketThreads;
+  const int c0 = min(nchunks, tid * per), c1 = min(nchunks, c0 + per);
+  uint32_t run = 0;
+  for (int c = c0; c < c1; ++c) run += cnt[c];
+  uint32_t incl = run;
+  const int lane = tid & 31, warp = tid >> 5;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t u = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += u;
+  }
+  if (lane == 31) scr[warp] = (int)incl;
+  __syncthreads();
+  uint32_t base = incl - run;
+  for (int w = 0; w < warp; ++w) base += (uint32_t)scr[w];
+  __syncthreads();
+  uint32_t* qb_off = boff + q * (int64_t)(nchunks + 1);
+  for (int c = c0; c < c1; ++c) {
+    const uint32_t v = cnt[c];
+    cnt[c] = base;
+    qb_off[c] = base;
+    base += v;
+  }
+  if (tid == 0) {
+    qb_off[nchunks] = (uint32_t)E;
+    mode[q] = 1;
+  }
+  __syncthreads();
+  uint32_t* qs = slots + q * capq;
+  double* qvv = vals + q * capq;
+  for (int d = 0; d < nd; ++d) {
+    const uint32_t b = lbeg[qb + d], L = lend[qb + d] - b;
+    const double qvd = qv[qb + d];
+    for (uint32_t jb = 0; jb < L; jb += blockDim.x) {
+      const uint32_t j = jb + tid;
+      const bool valid = j < L;
+      uint2 pw = make_uint2(0u, 0u);
+      uint32_t c = 0xFFFFFFFFu;
+      bool start = false, end = false;
+      if (valid) {
+        pw = __ldg(&post[b + j]);
+        c = pw.x >> 12;
+        start = (j == jb) || ((__ldg(&post[b + j - 1].x) >> 12) != c);
+        end = (j + 1 == L) || (tid == kBucketThreads - 1) || ((__ldg(&post[b + j + 1].x) >> 12) != c);
+      }
+      const int rs = block_max_scan(start ? tid : -1, scr);
+      uint32_t pos = 0;
+      if (valid) {
+        pos = cnt[c] + (uint32_t)(tid - rs);
+        qs[pos] = pw.x;
+        qvv[pos] = qvd * (double)__uint_as_float(pw.y);  // exact product of two f32
+      }
+      __syncthreads();  // every thread has used the old cursor
+      if (valid && end) cnt[c] += (uint32_t)(tid - rs + 1);
+      __syncthreads();
+    }
+  }
+}
+
+// skip table of one long list: row[c] = #postings with id < 4096*c
+__global__ void k_skip_rows(const uint2* __restrict__ post, const uint32_t* __restrict__ ptr,
+                            const int32_t* __restrict__ long_lists, int nchunks,
+                            uint32_t* __restrict__ skip) {
+  const int r = blockIdx.x;
+  const int li = long_lists[r];
+  const uint32_t b = ptr[li], L = ptr[li + 1] - b;
+  uint32_t* row = skip + (int64_t)r * (nchunks + 1);
+  for (uint32_t j = threadIdx.x; j <= L; j += blockDim.x) {
+    // chunks c in (chunk(j-1), chunk(j)] start at j
+    const int64_t cprev = j == 0 ? -1 : (int64_t)(__ldg(&post[b + j - 1].x) >> 12);
+    const int64_t ccur = j == L ? (int64_t)nchunks : (int64_t)(__ldg(&post[b + j].x) >> 12);
+    for (int64_t c = cprev + 1; c <= ccur; ++c) row[c] = j;
+  }
 }
 
 // pair-major packed codes (dense.py:156-170) -> vertical nibble planes
@@ -713,6 +950,52 @@ __global__ void k_to_vertical(const uint8_t* __restrict__ packed, int64_t n, int
 }  // namespace
 
 int stage1_chunk_points() { return kChunk; }
+
+int build_skip_tables(DeviceIndex& ix, const int64_t* host_ptr) {
+  const int64_t nchunks = ceil_div(ix.n, kChunk);
+  std::vector<int32_t> row(ix.n_active, -1);
+  std::vector<int32_t> longs;
+  for (int64_t i = 0; i < ix.n_active; ++i)
+    if (host_ptr[i + 1] - host_ptr[i] >= 2 * nchunks && nchunks > 1) {
+      row[i] = (int32_t)longs.size();
+      longs.push_back((int32_t)i);
+    }
+  ix.n_long = (int64_t)longs.size();
+  HS_CUDA(cudaMalloc(&ix.skip_row, sizeof(int32_t) * std::max<int64_t>(ix.n_active, 1)));
+  if (ix.n_active)
+    HS_CUDA(cudaMemcpy(ix.skip_row, row.data(), sizeof(int32_t) * ix.n_active,
+                       cudaMemcpyHostToDevice));
+  ix.bytes += sizeof(int32_t) * ix.n_active;
+  if (ix.n_long == 0) return HS_OK;
+  const size_t bytes = sizeof(uint32_t) * ix.n_long * (nchunks + 1);
+  HS_CUDA(cudaMalloc(&ix.skip, bytes));
+  ix.bytes += (int64_t)bytes;
+  int32_t* d_long = nullptr;
+  HS_CUDA(cudaMalloc(&d_long, sizeof(int32_t) * ix.n_long));
+  HS_CUDA(cudaMemcpy(d_long, longs.data(), sizeof(int32_t) * ix.n_long, cudaMemcpyHostToDevice));
+  k_skip_rows<<<(unsigned)ix.n_long, 256>>>(ix.post, ix.post_ptr, d_long, (int)nchunks, ix.skip);
+  HS_CUDA(cudaGetLastError());
+  HS_CUDA(cudaDeviceSynchronize());
+  cudaFree(d_long);
+  return HS_OK;
+}
+
+int64_t bucket_capacity(const DeviceIndex& ix) {
+  const int64_t nchunks = ceil_div(ix.n, kChunk);
+  return std::min<int64_t>(96 * nchunks, 32768);
+}
+
+void launch_sparse_bucket(const DeviceIndex& ix, const QueryView& q, const uint32_t* lbeg,
+                          const uint32_t* lend, const double* qv, const SparseBuckets& sb,
+                          cudaStream_t st) {
+  if (q.nq <= 0) return;
+  const size_t smem = sizeof(uint32_t) * (sb.nchunks + 1) + sizeof(int) * 32;
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(k_sparse_bucket, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_sparse_bucket<<<(unsigned)q.nq, kBucketThreads, smem, st>>>(
+      q.sp_indptr, lbeg, lend, qv, ix.post, sb.nchunks, sb.capq, sb.mode, sb.boff, sb.slots,
+      sb.vals);
+}
 
 int64_t vertical_stride(int64_t n) {
   // u32 words per subspace row: 2 words per 16 points, padded to 64 B
@@ -772,25 +1055,27 @@ size_t stage1_smem_bytes(const DeviceIndex& ix, const Stage1Plan& p) {
   size_t b = sizeof(Cand) * (size_t)(p.mode == S1_SELECT ? p.cap : 0) + sizeof(Cand);
   b += sizeof(double) * kChunk;
   b += 16 * (size_t)ix.Kp;
-  b += (sizeof(double) + 6 * sizeof(uint32_t)) * (size_t)p.max_qnnz;
+  b += (sizeof(double) + 8 * sizeof(uint32_t)) * (size_t)p.max_qnnz;
   b += sizeof(int) * 16;
   return b;
 }
 
 void launch_map_dims(const DeviceIndex& ix, const QueryView& q, int64_t nnz, bool use_weight,
-                     uint32_t* lbeg, uint32_t* lend, double* qv, cudaStream_t st) {
+                     uint32_t* lbeg, uint32_t* lend, double* qv, int32_t* lidx,
+                     cudaStream_t st) {
   if (nnz <= 0) return;
   const int T = 256;
   k_map_dims<<<(unsigned)ceil_div(nnz, T), T, 0, st>>>(
       q.sp_dims, q.sp_vals, nnz, ix.post_dims, ix.n_active, ix.post_ptr,
-      (float)ix.sparse_weight, use_weight && ix.sparse_weight != 1.0 ? 1 : 0, lbeg, lend, qv);
+      (float)ix.sparse_weight, use_weight && ix.sparse_weight != 1.0 ? 1 : 0, lbeg, lend, qv,
+      lidx);
 }
 
 int launch_stage1(const DeviceIndex& ix, const QueryView& q, const Stage1Plan& p,
                   const uint32_t* lbeg, const uint32_t* lend, const double* qv,
-                  const uint8_t* luts, const double* bias_total, const double* scale,
+                  const int32_t* lidx, const uint8_t* luts, const double* bias_total, const double* scale,
                   const double* offset, Cand* out, double* dump, cudaStream_t st,
-                  uint32_t* dump_tot, bool raw_dense) {
+                  uint32_t* dump_tot, bool raw_dense, const SparseBuckets* sb) {
   if (q.nq <= 0 || ix.n <= 0) return HS_OK;
   Stage1Args a;
   a.n = ix.n;
@@ -805,6 +1090,7 @@ int launch_stage1(const DeviceIndex& ix, const QueryView& q, const Stage1Plan& p
   a.lbeg = lbeg;
   a.lend = lend;
   a.qv = qv;
+  a.lidx = lidx;
   a.has_dense = (ix.d_dense > 0 && ix.K > 0 && p.use_dense && !p.sparse_only_acc) ? 1 : 0;
   a.K = ix.K;
   a.Kp = ix.Kp;
@@ -820,6 +1106,15 @@ int launch_stage1(const DeviceIndex& ix, const QueryView& q, const Stage1Plan& p
   a.dump_tot = dump_tot;
   a.raw_dense = raw_dense ? 1 : 0;
   a.max_qnnz = p.max_qnnz;
+  a.bmode = sb ? sb->mode : nullptr;
+  a.boff = sb ? sb->boff : nullptr;
+  a.bslots = sb ? sb->slots : nullptr;
+  a.bvals = sb ? sb->vals : nullptr;
+  a.capq = sb ? sb->capq : 0;
+  a.nchunks_g = sb ? sb->nchunks : 0;
+  a.skip_row = ix.skip_row;
+  a.skip = ix.skip;
+  a.nchunks_all = (int)ceil_div(ix.n, kChunk);
   {
     static const int exp_flags = [] {
       const char* e = getenv("HSB200_EXP");

@@ -106,3 +106,21 @@ def test_multi_chunk_tiles_many_queries():
     ds, qs, cfg, idx = _scaled("cfg2", 100_000, 300)
     s = cfg.search
     _check_search(idx, qs, s["h"], s["overfetch"], s["retain"], True, n_oracle=6)
+
+
+def test_bucketed_and_streamed_sparse_paths_agree(monkeypatch):
+    """The sparse pre-pass (postings bucketed per chunk) and the in-kernel
+    cursor stream must give identical stage-1 scores and results."""
+    ds, qs, cfg, idx = _scaled("cfg2", 60_000, 40)
+    s = cfg.search
+    a = hs.search_batch(idx, qs, s["h"], overfetch=s["overfetch"], retain=s["retain"],
+                        exact_final_rerank=True)
+    s1a = hs.stage1_scores(idx, qs)
+    monkeypatch.setenv("HSB200_NO_BUCKETS", "1")
+    b = hs.search_batch(idx, qs, s["h"], overfetch=s["overfetch"], retain=s["retain"],
+                        exact_final_rerank=True)
+    s1b = hs.stage1_scores(idx, qs)
+    assert np.array_equal(s1a, s1b)
+    for x, y in zip(a, b):
+        assert x.ids.tolist() == y.ids.tolist()
+        assert x.scores.tolist() == y.scores.tolist()
