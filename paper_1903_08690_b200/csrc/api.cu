@@ -111,6 +111,7 @@ int resolve_sizes(const DeviceIndex& ix, const hs_search_params* p, Sizes* s) {
 }
 
 constexpr int64_t kMaxRerank = 8192;  // k1/k2 held in shared memory for stages 2-3
+constexpr int64_t kTcMinQueries = 64;  // batches at least this large use the tensor cores
 
 // time accumulation helpers
 struct Timer {
@@ -146,8 +147,8 @@ struct Timer {
       } else {
         ix->tms[it - ix->tnames.begin()] += ms;
       }
-      if (nm == "map_dims" || nm == "lut_build" || nm == "sparse_bucket" || nm == "stage1" ||
-          nm == "merge")
+      if (nm == "map_dims" || nm == "lut_build" || nm == "sparse_bucket" || nm == "lut16_tc" ||
+          nm == "stage1" || nm == "merge")
         st3[0] += ms;
       else if (nm == "stage2") st3[1] += ms;
       else if (nm == "stage3") st3[2] += ms;
@@ -175,8 +176,16 @@ int run_search(DeviceIndex& ix, const hs_query_batch& qb, int64_t nnz, int max_q
     HS_FAIL(HS_EUNSUPPORTED, "overfetch*h above 8192 candidates is not supported");
   if (max_qnnz > 8192) HS_FAIL(HS_EUNSUPPORTED, "queries with more than 8192 sparse nonzeros");
 
+  // tensor-core LUT16 totals for large batches (>= kTcMinQueries queries)
+  const int64_t tc_ld = lut16_tc_ld(ix.n);
+  const bool use_tc = ix.d_dense > 0 && ix.K <= 257 && ix.K > 0 && nq >= kTcMinQueries &&
+                      !getenv_flag("HSB200_NO_TC");
   // query-chunk size bounded by scratch for the stage-1 per-tile outputs
   int64_t QB = std::min<int64_t>(nq, 2048);
+  if (use_tc) {  // u16 totals [QB][tc_ld]: keep them under ~2 GB, in groups of 128
+    const int64_t cap = std::max<int64_t>(128, (int64_t)(2.0e9 / (2.0 * tc_ld)) / 128 * 128);
+    QB = std::min(QB, cap);
+  }
   int64_t s1_entries = 0;
   for (;;) {
     const Stage1Plan p0 = plan_stage1(ix, QB, sz.k1, max_qnnz, S1_SELECT);
@@ -217,6 +226,7 @@ int run_search(DeviceIndex& ix, const hs_query_batch& qb, int64_t nnz, int max_q
       a.take<uint32_t>(QB * capq);
       a.take<double>(QB * capq);
     }
+    if (use_tc) a.take<uint16_t>(QB * tc_ld);
     need = a.off + 1024;
   }
   HS_CHECK(ensure_scratch(ix, need));
@@ -244,6 +254,7 @@ int run_search(DeviceIndex& ix, const hs_query_batch& qb, int64_t nnz, int max_q
     sb.capq = capq;
     sb.nchunks = (int)nchunks;
   }
+  uint16_t* tot16 = use_tc ? a.take<uint16_t>(QB * tc_ld) : nullptr;
 
   if (tm) tm->mark("begin");
   QueryView all;
@@ -266,6 +277,7 @@ int run_search(DeviceIndex& ix, const hs_query_batch& qb, int64_t nnz, int max_q
     qc.sp_vals = qb.sp_vals;
     qc.dense = qb.dense ? qb.dense + q0 * d : nullptr;
     Stage1Plan pc = plan_stage1(ix, nqc, sz.k1, max_qnnz, S1_SELECT);
+    pc.sparse = nnz > 0;
     if (d > 0) {
       launch_lut_build(ix, qc.dense, nqc, qd, qw, luts, btot, scl, off, bad, st);
       HS_CUDA(cudaGetLastError());
@@ -279,9 +291,16 @@ int run_search(DeviceIndex& ix, const hs_query_batch& qb, int64_t nnz, int max_q
       ix.launches += 1;
       if (tm) tm->mark("sparse_bucket");
     }
+    const bool tc_chunk = use_tc && nqc >= kTcMinQueries;
+    if (tc_chunk) {
+      HS_CHECK(launch_lut16_tc(ix, luts, nqc, tot16, tc_ld, st));
+      ix.launches += 1;
+      if (tm) tm->mark("lut16_tc");
+    }
     ix.launches += (d > 0 ? 1 : 0) + 4;  // lut_build, stage1, merge, stage2, stage3
     HS_CHECK(launch_stage1(ix, qc, pc, lbeg, lend, qv, lidx, luts, btot, scl, off, s1out, nullptr, st,
-                           nullptr, false, use_buckets ? &sb : nullptr));
+                           nullptr, false, use_buckets ? &sb : nullptr,
+                           tc_chunk ? tot16 : nullptr, tc_ld));
     if (tm) tm->mark("stage1");
     HS_CHECK(launch_select_topk(s1out, nqc, (int64_t)pc.ntiles * pc.out_per_tile, sz.k1, cand1, st));
     if (tm) tm->mark("merge");
@@ -764,6 +783,7 @@ static int stage1_dump(hs_index_t index, const hs_query_batch* queries, double* 
     launch_lut_build(*index, qvw.dense, nq, qd, qw, luts, bt, sc, of, bad, index->stream);
   Stage1Plan p = plan_stage1(*index, nq, 1, dq.max_row, S1_DUMP);
   p.sparse_only_acc = raw_acc;
+  p.sparse = dq.nnz > 0;
   SparseBuckets sb;
   const bool use_buckets = dq.nnz > 0 && index->nnz_post > 0 && !getenv_flag("HSB200_NO_BUCKETS");
   if (use_buckets) {

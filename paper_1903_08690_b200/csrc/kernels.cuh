@@ -106,6 +106,7 @@ struct Stage1Plan {
   int max_qnnz = 0;
   bool use_dense = true;  // DUMP: include the dense part
   bool sparse_only_acc = false;  // DUMP: raw accumulator (no weights, no dense)
+  bool sparse = true;     // the batch has sparse nonzeros to stream
 };
 // per-query postings bucketed by 4096-slot chunk (stable: ascending dim then
 // slot inside a bucket) with exact f64 products; mode[q] = 1 when query q
@@ -137,7 +138,14 @@ int launch_stage1(const DeviceIndex& ix, const QueryView& q, const Stage1Plan& p
                   const int32_t* lidx, const uint8_t* luts, const double* bias_total, const double* scale,
                   const double* offset, Cand* out, double* dump, cudaStream_t st,
                   uint32_t* dump_tot = nullptr, bool raw_dense = false,
-                  const SparseBuckets* sb = nullptr);
+                  const SparseBuckets* sb = nullptr, const uint16_t* tot16 = nullptr,
+                  int64_t tot_ld = 0);
+
+// lut16_tc.cu (tensor-core batched LUT16 totals)
+size_t lut16_tc_smem();
+int64_t lut16_tc_ld(int64_t n);
+int launch_lut16_tc(const DeviceIndex& ix, const uint8_t* luts, int64_t nq, uint16_t* tot,
+                    int64_t ld, cudaStream_t st);
 
 // select.cu
 int launch_select_topk(const Cand* in, int64_t nq, int64_t m, int64_t k, Cand* out,

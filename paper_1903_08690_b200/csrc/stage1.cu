@@ -85,6 +85,9 @@ struct Stage1Args {
   const int32_t* skip_row;
   const uint32_t* skip;
   int nchunks_all;
+  // precomputed LUT16 totals (tensor-core pass), [q][tot_ld] u16; null => PRMT scan
+  const uint16_t* tot16;
+  int64_t tot_ld;
   int exp_flags;       // dev experiments (HSB200_EXP): 1 no dense, 2 no sparse, 4 no offers
 };
 
@@ -146,6 +149,8 @@ struct Smem {
   uint32_t* acnt;   // their slice length
   int32_t* dskip;   // skip-table row of the dim's list, -1 if short
   uint32_t* dbeg;   // list begin (absolute posting index)
+  uint32_t* bslot;  // staged bucket entries (chunk-local slot)
+  double* bval;     // staged bucket entries (product)
   int* ctl;         // [0]=cnt [2]=have_th [4..12]=warp sums
 };
 
@@ -196,14 +201,17 @@ __device__ __forceinline__ void find_bin(const unsigned* hist, int need, bool de
 // running threshold to the k-th best.  Radix select over the score key (8-bit
 // digits, early exit when a whole bin is taken) then, for exact score ties at
 // the boundary, over the id; in-place order-preserving compaction.  O(cnt)
-// per digit — replaces a bitonic sort of the whole buffer.  The shared-memory
-// chunk accumulator is free at this point and holds the 256-bin histogram.
+// per digit — replaces a bitonic sort of the whole buffer.  The 256-bin
+// histogram lives in the bucket staging area (idle during the offer phase); the
+// chunk accumulator must survive, the offer loop re-reads it for scores.
+static_assert(sizeof(double) * kThreads >= 256 * sizeof(unsigned), "histogram fits the staging area");
+
 __device__ void compact(Smem& s, int k) {
   const int cnt = s.ctl[0];
   __syncthreads();  // every thread has read ctl[0]
   if (cnt <= k) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  unsigned* hist = reinterpret_cast<unsigned*>(s.acc);
+  unsigned* hist = reinterpret_cast<unsigned*>(s.bval);
   unsigned long long prefix = 0, pmask = 0;
   int need = k;
   bool whole_bin = false;
@@ -289,7 +297,7 @@ __device__ void compact(Smem& s, int k) {
     o_.slot = 0;
     if (better(worst, o_)) worst = o_;
   }
-  Cand* wbuf = reinterpret_cast<Cand*>(s.acc);  // histogram no longer needed
+  Cand* wbuf = reinterpret_cast<Cand*>(s.bval);  // histogram no longer needed
   if (lane == 0) wbuf[warp] = worst;
   __syncthreads();
   if (tid == 0) {
@@ -326,6 +334,9 @@ __device__ __forceinline__ void accum32(uint32_t* acc2, const uint32_t* r, const
   }
 }
 
+// DM: dense mode (0 none, 1 PRMT LUT16 scan, 2 precomputed u16 totals);
+// SP: the query batch has postings to stream (else the sparse phase is elided).
+template <int DM, bool SP>
 __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int64_t q = blockIdx.x;
@@ -362,6 +373,11 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
   p += sizeof(int32_t) * a.max_qnnz;
   s.dbeg = reinterpret_cast<uint32_t*>(p);
   p += sizeof(uint32_t) * a.max_qnnz;
+  p = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(p) + 7) & ~uintptr_t(7));
+  s.bval = reinterpret_cast<double*>(p);
+  p += sizeof(double) * kThreads;
+  s.bslot = reinterpret_cast<uint32_t*>(p);
+  p += sizeof(uint32_t) * kThreads;
   s.ctl = reinterpret_cast<int*>(p);
 
   const int64_t tile_lo = (int64_t)tile * a.tile_pts;
@@ -369,8 +385,8 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
 
   // ---- per-query setup ----
   const int64_t qb = a.qptr[q], qe = a.qptr[q + 1];
-  const bool bucketed = a.bmode != nullptr && a.bmode[q] == 1;
-  const int nd = bucketed ? 0 : (int)(qe - qb);  // bucketed queries skip the cursors
+  const bool bucketed = SP && a.bmode != nullptr && a.bmode[q] == 1;
+  const int nd = (SP && !bucketed) ? (int)(qe - qb) : 0;  // bucketed queries skip the cursors
   HS_DCHECK(nd >= 0 && nd <= a.max_qnnz);
   const uint32_t* qboff = bucketed ? a.boff + q * (int64_t)(a.nchunks_g + 1) : nullptr;
   const uint32_t* qslots = bucketed ? a.bslots + q * a.capq : nullptr;
@@ -393,19 +409,25 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
       s.dnext[d] = 0xFFFFFFFFu;
     }
   }
-  if (a.has_dense) {
+  if (DM == 1) {
     const uint4* src = reinterpret_cast<const uint4*>(a.luts + q * (int64_t)a.Kp * 16);
     for (int i = tid; i < a.Kp; i += blockDim.x) s.lut[i] = src[i];
   }
   if (tid < 16) s.ctl[tid] = 0;
   double btot = 0.0, scl = 0.0, off = 0.0;
-  if (a.has_dense) {
+  if (DM != 0) {
     btot = a.bias_total[q];
     scl = a.scale[q];
     off = a.offset ? a.offset[q] : 0.0;
   }
   const uint2* vc = reinterpret_cast<const uint2*>(a.vcodes);
   const int64_t vrow = a.vstride >> 1;  // uint2 per subspace row
+  uint4 tnext0 = make_uint4(0u, 0u, 0u, 0u), tnext1 = tnext0;
+  if (DM == 2 && tile_lo + (int64_t)tid * kPPT < tile_hi) {
+    const uint4* src = reinterpret_cast<const uint4*>(a.tot16 + q * a.tot_ld + tile_lo + tid * kPPT);
+    tnext0 = __ldg(src);
+    tnext1 = __ldg(src + 1);
+  }
   __syncthreads();
 
   for (int64_t cb = tile_lo; cb < tile_hi; cb += kChunk) {
@@ -417,7 +439,21 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
     uint32_t tot[kPPT];
 #pragma unroll
     for (int j = 0; j < kPPT; ++j) tot[j] = 0;
-    if (a.has_dense && p0 < ce && !(a.exp_flags & 1)) {
+    if (DM == 2 && p0 < ce) {
+      // totals of this chunk were prefetched during the previous chunk
+      const uint4 t0 = tnext0, t1 = tnext1;
+      if (p0 + kChunk < tile_hi) {
+        const uint4* nsrc = reinterpret_cast<const uint4*>(a.tot16 + q * a.tot_ld + p0 + kChunk);
+        tnext0 = __ldg(nsrc);
+        tnext1 = __ldg(nsrc + 1);
+      }
+      const uint32_t w8[8] = {t0.x, t0.y, t0.z, t0.w, t1.x, t1.y, t1.z, t1.w};
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        tot[2 * j] = w8[j] & 0xFFFFu;
+        tot[2 * j + 1] = w8[j] >> 16;
+      }
+    } else if (DM == 1 && p0 < ce && !(a.exp_flags & 1)) {
       const uint2* col = vc + (p0 >> 4);
       uint32_t acc2[8];
 #pragma unroll
@@ -472,25 +508,37 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
 
     // ---- sparse: bucketed postings of this chunk (pre-pass) ----
     int nact = 0, npost = 0;
-    if (bucketed) {
+    if (SP && bucketed) {
       const int64_t cg = cb / kChunk;
       const uint32_t e0 = __ldg(qboff + cg), e1 = __ldg(qboff + cg + 1);
       if (e1 > e0) {
-        // each thread walks the (short) bucket and adds to its own 16 points;
-        // bucket order is ascending dim per point => reference summation order
+        // The bucket is staged through shared memory in tiles of 256 entries
+        // (one coalesced load per thread); every thread then walks the tile
+        // and adds the entries that land on its own 16 points.  Bucket order
+        // is ascending dim per point => the reference summation order.
         double* mine = s.acc + tid * kPPT;
 #pragma unroll
         for (int j = 0; j < kPPT; ++j) mine[j] = 0.0;
-        for (uint32_t e = e0; e < e1; ++e) {
-          const uint32_t local = __ldg(qslots + e) - (uint32_t)cb;
-          HS_DCHECK(local < (uint32_t)kChunk);
-          if ((local >> 4) == (uint32_t)tid) mine[local & 15] += __ldg(qvals + e);
+        for (uint32_t base = e0; base < e1; base += kThreads) {
+          const uint32_t e = base + tid;
+          if (e < e1) {
+            s.bslot[tid] = __ldg(qslots + e) - (uint32_t)cb;
+            s.bval[tid] = __ldg(qvals + e);
+          }
+          __syncthreads();
+          const int cnt = (int)min((uint32_t)kThreads, e1 - base);
+          for (int j = 0; j < cnt; ++j) {
+            const uint32_t local = s.bslot[j];
+            HS_DCHECK(local < (uint32_t)kChunk);
+            if ((local >> 4) == (uint32_t)tid) mine[local & 15] += s.bval[j];
+          }
+          __syncthreads();
         }
         nact = 1;
         npost = 0;
       }
     }
-    if (!bucketed) {
+    if (SP && !bucketed) {
       // ---- sparse: active dims of this chunk, in ascending dim order ----
       for (int base = 0; base < nd; base += blockDim.x) {
         const int d = base + tid;
@@ -565,11 +613,17 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
         for (int i = 0; i < nact; ++i) {
           const uint32_t b = s.abase[i], c = s.acnt[i];
           const double qv = s.dqv[s.alist[i]];
-          for (uint32_t j = 0; j < c; ++j) {
-            const uint2 pw = __ldg(&a.post[b + j]);
-            const uint32_t local = pw.x - (uint32_t)cb;
-            HS_DCHECK(local < (uint32_t)kChunk);
-            if ((local >> 4) == (uint32_t)tid) mine[local & 15] += qv * (double)__uint_as_float(pw.y);
+          for (uint32_t j0 = 0; j0 < c; j0 += 8) {
+            uint2 pw[8];
+#pragma unroll
+            for (int r = 0; r < 8; ++r)  // independent loads in flight
+              pw[r] = j0 + r < c ? __ldg(&a.post[b + j0 + r]) : make_uint2(0xFFFFFFFFu, 0u);
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+              const uint32_t local = pw[r].x - (uint32_t)cb;
+              if (pw[r].x != 0xFFFFFFFFu && (local >> 4) == (uint32_t)tid)
+                mine[local & 15] += qv * (double)__uint_as_float(pw[r].y);
+            }
           }
         }
       } else if (nact > 0) {
@@ -629,26 +683,22 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
       }
     }
 
-    // ---- scores ----
-    double sc[kPPT];
-#pragma unroll
-    for (int j = 0; j < kPPT; ++j) {
-      const double acc = nact > 0 ? s.acc[tid * kPPT + j] : 0.0;
-      if (a.raw_dense) {
-        sc[j] = __dadd_rn(btot, __dmul_rn(scl, (double)tot[j]));
-      } else if (a.has_dense) {
+    // ---- scores (recomputed where needed instead of held in 16 f64 registers) ----
+    auto score = [&](int j) -> double {
+      const double acc = (SP && nact > 0) ? s.acc[tid * kPPT + j] : 0.0;
+      if (a.raw_dense) return __dadd_rn(btot, __dmul_rn(scl, (double)tot[j]));
+      if (DM != 0) {
         const double dn = __dadd_rn(__dadd_rn(btot, __dmul_rn(scl, (double)tot[j])), off);
-        sc[j] = __dadd_rn(acc, dn);
-      } else {
-        sc[j] = acc;
+        return __dadd_rn(acc, dn);
       }
-    }
+      return acc;
+    };
 
     if (a.mode == S1_DUMP) {
 #pragma unroll
       for (int j = 0; j < kPPT; ++j) {
         if (p0 + j >= ce) continue;
-        a.dump[q * a.n + p0 + j] = sc[j];
+        a.dump[q * a.n + p0 + j] = score(j);
         if (a.dump_tot) a.dump_tot[q * a.n + p0 + j] = tot[j];
       }
       __syncthreads();
@@ -661,7 +711,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
         const int64_t pt = p0 + j;
         if (pt < ce) {
           Cand c;
-          c.s = sc[j];
+          c.s = score(j);
           c.slot = (uint32_t)pt;
           c.tie = a.order[pt];
           o[pt - tile_lo] = c;
@@ -675,7 +725,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
     if (a.exp_flags & 4) {
       double t = 0;
 #pragma unroll
-      for (int j = 0; j < kPPT; ++j) t += sc[j];
+      for (int j = 0; j < kPPT; ++j) t += score(j);
       if (t == 12345.678) s.ctl[15] = 1;  // keep the scores live
       __syncthreads();
       continue;
@@ -688,8 +738,9 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
       for (int j = 0; j < kPPT; ++j) {
         const int64_t pt = p0 + j;
         if (pt >= ce) continue;
-        bool pass = !have || sc[j] > th.s;
-        if (!pass && sc[j] == th.s) pass = a.order[pt] < th.tie;
+        const double sj = score(j);
+        bool pass = !have || sj > th.s;
+        if (!pass && sj == th.s) pass = a.order[pt] < th.tie;
         if (pass) mask |= 1u << j;
       }
     }
@@ -706,7 +757,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
         for (int j = 0; j < kPPT; ++j) {
           if (!(mask >> j & 1)) continue;
           Cand c;
-          c.s = sc[j];
+          c.s = score(j);
           c.slot = (uint32_t)(p0 + j);
           c.tie = a.order[p0 + j];
           s.buf[pos++] = c;
@@ -729,8 +780,9 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
           for (int j = 0; j < 4; ++j) {
             if (!(m >> j & 1)) continue;
             const int jj = 4 * r + j;
-            bool pass = sc[jj] > th.s;
-            if (!pass && sc[jj] == th.s) pass = a.order[p0 + jj] < th.tie;
+            const double sj = score(jj);
+            bool pass = sj > th.s;
+            if (!pass && sj == th.s) pass = a.order[p0 + jj] < th.tie;
             if (pass) m2 |= 1u << j;
           }
           m = m2;
@@ -743,7 +795,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
             if (!(m >> j & 1)) continue;
             const int jj = 4 * r + j;
             Cand c;
-            c.s = sc[jj];
+            c.s = score(jj);
             c.slot = (uint32_t)(p0 + jj);
             c.tie = a.order[p0 + jj];
             s.buf[pos++] = c;
@@ -1056,6 +1108,7 @@ size_t stage1_smem_bytes(const DeviceIndex& ix, const Stage1Plan& p) {
   b += sizeof(double) * kChunk;
   b += 16 * (size_t)ix.Kp;
   b += (sizeof(double) + 8 * sizeof(uint32_t)) * (size_t)p.max_qnnz;
+  b += 8 + (sizeof(double) + sizeof(uint32_t)) * kThreads;  // bucket staging
   b += sizeof(int) * 16;
   return b;
 }
@@ -1075,7 +1128,8 @@ int launch_stage1(const DeviceIndex& ix, const QueryView& q, const Stage1Plan& p
                   const uint32_t* lbeg, const uint32_t* lend, const double* qv,
                   const int32_t* lidx, const uint8_t* luts, const double* bias_total, const double* scale,
                   const double* offset, Cand* out, double* dump, cudaStream_t st,
-                  uint32_t* dump_tot, bool raw_dense, const SparseBuckets* sb) {
+                  uint32_t* dump_tot, bool raw_dense, const SparseBuckets* sb,
+                  const uint16_t* tot16, int64_t tot_ld) {
   if (q.nq <= 0 || ix.n <= 0) return HS_OK;
   Stage1Args a;
   a.n = ix.n;
@@ -1115,6 +1169,8 @@ int launch_stage1(const DeviceIndex& ix, const QueryView& q, const Stage1Plan& p
   a.skip_row = ix.skip_row;
   a.skip = ix.skip;
   a.nchunks_all = (int)ceil_div(ix.n, kChunk);
+  a.tot16 = tot16;
+  a.tot_ld = tot_ld;
   {
     static const int exp_flags = [] {
       const char* e = getenv("HSB200_EXP");
@@ -1125,9 +1181,20 @@ int launch_stage1(const DeviceIndex& ix, const QueryView& q, const Stage1Plan& p
   const size_t smem = stage1_smem_bytes(ix, p);
   if (smem > 227 * 1024) HS_FAIL(HS_EUNSUPPORTED, "stage-1 shared memory exceeds 227 KB "
                                                   "(too many query nonzeros or candidates)");
-  HS_CUDA(cudaFuncSetAttribute(k_stage1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int dm = !a.has_dense ? 0 : (tot16 != nullptr ? 2 : 1);
+  const bool sp = p.sparse && ix.nnz_post > 0 && lbeg != nullptr;
+  void (*kern)(Stage1Args) = nullptr;
+  switch (dm * 2 + (sp ? 1 : 0)) {
+    case 0: kern = k_stage1<0, false>; break;
+    case 1: kern = k_stage1<0, true>; break;
+    case 2: kern = k_stage1<1, false>; break;
+    case 3: kern = k_stage1<1, true>; break;
+    case 4: kern = k_stage1<2, false>; break;
+    default: kern = k_stage1<2, true>; break;
+  }
+  HS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   dim3 grid((unsigned)q.nq, (unsigned)p.ntiles);
-  k_stage1<<<grid, kThreads, smem, st>>>(a);
+  kern<<<grid, kThreads, smem, st>>>(a);
   HS_CUDA(cudaGetLastError());
   return HS_OK;
 }

@@ -124,3 +124,24 @@ def test_bucketed_and_streamed_sparse_paths_agree(monkeypatch):
     for x, y in zip(a, b):
         assert x.ids.tolist() == y.ids.tolist()
         assert x.scores.tolist() == y.scores.tolist()
+
+
+@pytest.mark.parametrize("name,n,nq", [("cfg2", 40_000, 200), ("cfg3", 70_000, 150),
+                                       ("cfg1", 30_000, 130)])
+def test_tensor_core_lut16_path_matches_oracle_and_prmt(name, n, nq, monkeypatch):
+    """Batches >= 64 queries take the tcgen05 kind::i8 LUT16 pass; results must be
+    identical to the PRMT CUDA-core path and to the oracle."""
+    ds, qs, cfg, idx = _scaled(name, n, nq)
+    s = cfg.search
+    kw = dict(overfetch=s["overfetch"], retain=s["retain"],
+              exact_final_rerank=s["exact_final_rerank"])
+    tc = hs.search_batch(idx, qs, s["h"], **kw)
+    monkeypatch.setenv("HSB200_NO_TC", "1")
+    ref = hs.search_batch(idx, qs, s["h"], **kw)
+    for a, b in zip(tc, ref):
+        assert a.ids.tolist() == b.ids.tolist()
+        assert a.scores.tolist() == b.scores.tolist()
+    for i in range(0, qs.n, max(1, qs.n // 6)):
+        ids, sc, _ = O.search_topk(idx, *O.query_parts(qs, i), s["h"], **kw)
+        assert tc[i].ids.tolist() == ids.tolist()
+        np.testing.assert_allclose(tc[i].scores, sc, rtol=1e-9)
