@@ -324,6 +324,25 @@ def main():
         t_total = float(tt.item())
     value = nq * args.steps / (t_total / 1e3)
 
+    # ---- e2e through the public API with host buffers (N=1) ----
+    e2e = None
+    if world == 1:
+        for _ in range(2):
+            hs.search_batch(idx, qs, h, overfetch=s["overfetch"], retain=s["retain"],
+                            exact_final_rerank=s["exact_final_rerank"])
+        et = []
+        for _ in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            hs.search_batch(idx, qs, h, overfetch=s["overfetch"], retain=s["retain"],
+                            exact_final_rerank=s["exact_final_rerank"])
+            et.append(time.perf_counter() - t0)
+        d2h = nq * kh * (8 + 8)
+        e2e = {"value": nq * len(et) / sum(et), "unit": "queries/s",
+               "h2d_bytes_per_step": int(h2d_bytes), "d2h_bytes_per_step": int(d2h),
+               "ms_per_step": 1e3 * sum(et) / len(et)}
+
     # ---- per-kernel breakdown (separate profiled steps; timing adds syncs) ----
     dev_index.set_timing(True)
     ktimes = {}
@@ -371,25 +390,6 @@ def main():
                                         device=local)
         rec = [len(np.intersect1d(res_ids[i, :10], t_ids[i])) / 10 for i in range(truth_q)]
         recall = float(np.mean(rec))
-
-    # ---- e2e through the public API with host buffers (N=1) ----
-    e2e = None
-    if world == 1:
-        for _ in range(2):
-            hs.search_batch(idx, qs, h, overfetch=s["overfetch"], retain=s["retain"],
-                            exact_final_rerank=s["exact_final_rerank"])
-        et = []
-        for _ in range(args.steps):
-            flush.zero_()
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            hs.search_batch(idx, qs, h, overfetch=s["overfetch"], retain=s["retain"],
-                            exact_final_rerank=s["exact_final_rerank"])
-            et.append(time.perf_counter() - t0)
-        d2h = nq * kh * (8 + 8)
-        e2e = {"value": nq * len(et) / sum(et), "unit": "queries/s",
-               "h2d_bytes_per_step": int(h2d_bytes), "d2h_bytes_per_step": int(d2h),
-               "ms_per_step": 1e3 * sum(et) / len(et)}
 
     # ---- roofline of the dominant kernel (fused stage 1) ----
     peak, peak_kind = _peaks()

@@ -60,9 +60,11 @@ void free_device_arrays(DeviceIndex* ix) {
                   ix->res_indices, ix->res_data, ix->subdims,  ix->dim_off,    ix->cen_off,
                   ix->centers,  ix->vcodes,     ix->sq_lo,    ix->sq_step,    ix->sq_codes,
                   ix->wh_mean,  ix->wh_inv_t,   ix->ds_dense, ix->ds_indptr,  ix->ds_indices,
-                  ix->ds_data,  ix->scratch,    ix->skip_row, ix->skip};
+                  ix->ds_data,  ix->scratch,    ix->skip_row, ix->skip,     ix->io_dev,
+                  ix->hcodes};
   for (void* p : ptrs)
     if (p) cudaFree(p);
+  if (ix->io_host) cudaFreeHost(ix->io_host);
   if (ix->stream) cudaStreamDestroy(ix->stream);
 }
 
@@ -178,13 +180,14 @@ int run_search(DeviceIndex& ix, const hs_query_batch& qb, int64_t nnz, int max_q
 
   // tensor-core LUT16 totals for large batches (>= kTcMinQueries queries)
   const int64_t tc_ld = lut16_tc_ld(ix.n);
-  const bool use_tc = ix.d_dense > 0 && ix.K <= 257 && ix.K > 0 && nq >= kTcMinQueries &&
+  const bool use_tc = ix.d_dense > 0 && lut16_tc_supported(ix) && nq >= kTcMinQueries &&
                       !getenv_flag("HSB200_NO_TC");
   // query-chunk size bounded by scratch for the stage-1 per-tile outputs
   int64_t QB = std::min<int64_t>(nq, 2048);
-  if (use_tc) {  // u16 totals [QB][tc_ld]: keep them under ~2 GB, in groups of 128
-    const int64_t cap = std::max<int64_t>(128, (int64_t)(2.0e9 / (2.0 * tc_ld)) / 128 * 128);
-    QB = std::min(QB, cap);
+  if (use_tc) {  // u16 totals [QB][tc_ld]: under ~8 GB, whole tensor-core groups
+    const int64_t grp = lut16_tc_group(ix);
+    const int64_t cap = std::max<int64_t>(grp, (int64_t)(8.0e9 / (2.0 * tc_ld)) / grp * grp);
+    if (QB > cap) QB = cap;
   }
   int64_t s1_entries = 0;
   for (;;) {
@@ -322,27 +325,39 @@ int run_search(DeviceIndex& ix, const hs_query_batch& qb, int64_t nnz, int max_q
   return HS_OK;
 }
 
-// host query batch -> device copies (owned by the returned holder)
+// host query batch -> device copies through the handle's pinned staging
+// buffer; `result_bytes` more device bytes are reserved after the queries for
+// the caller's outputs (DevQueries::out)
 struct DevQueries {
   hs_query_batch b{};
-  std::vector<void*> bufs;
   int64_t nnz = 0;
   int max_row = 0;
-  ~DevQueries() {
-    for (void* p : bufs) cudaFree(p);
-  }
+  char* out = nullptr;       // device result area
+  char* out_host = nullptr;  // pinned host mirror of it
 };
 
-int upload_queries(const DeviceIndex& ix, const hs_query_batch* q, DevQueries* out, bool check) {
+int grow(void** p, size_t* have, size_t want, bool host, cudaStream_t st) {
+  if (want <= *have) return HS_OK;
+  HS_CUDA(cudaStreamSynchronize(st));
+  if (*p) host ? cudaFreeHost(*p) : cudaFree(*p);
+  *p = nullptr;
+  *have = 0;
+  const size_t bytes = want + want / 4 + 4096;
+  if (host) HS_CUDA(cudaMallocHost(p, bytes));
+  else HS_CUDA(cudaMalloc(p, bytes));
+  *have = bytes;
+  return HS_OK;
+}
+
+int upload_queries(DeviceIndex& ix, const hs_query_batch* q, DevQueries* out, bool check,
+                   size_t result_bytes = 0) {
   if (!q || q->nq < 0) HS_FAIL(HS_EINVAL, "bad query batch");
   const int64_t nq = q->nq;
   const int64_t base = nq ? q->sp_indptr[0] : 0;
   const int64_t nnz = nq ? q->sp_indptr[nq] - base : 0;
   int max_row = 0;
-  std::vector<int64_t> ptr(nq + 1);
-  for (int64_t i = 0; i <= nq; ++i) ptr[i] = q->sp_indptr[i] - base;
   for (int64_t i = 0; i < nq; ++i) {
-    const int64_t len = ptr[i + 1] - ptr[i];
+    const int64_t len = q->sp_indptr[i + 1] - q->sp_indptr[i];
     if (len < 0) HS_FAIL(HS_EINVAL, "query indptr not monotone");
     max_row = std::max<int64_t>(max_row, len);
   }
@@ -350,31 +365,38 @@ int upload_queries(const DeviceIndex& ix, const hs_query_batch* q, DevQueries* o
     for (int64_t i = 0; i < nnz; ++i)
       if ((int64_t)q->sp_dims[base + i] >= ix.d_sparse)
         HS_FAIL(HS_EINVAL, "query sparse dimension out of range");
-  auto up = [&](const void* src, size_t bytes, void** dst) -> int {
-    *dst = nullptr;
-    HS_CUDA(cudaMalloc(dst, bytes ? bytes : 16));
-    out->bufs.push_back(*dst);
-    if (bytes) HS_CUDA(cudaMemcpyAsync(*dst, src, bytes, cudaMemcpyHostToDevice, ix.stream));
-    return HS_OK;
-  };
-  void *dptr, *ddims, *dvals, *ddense = nullptr;
-  HS_CHECK(up(ptr.data(), sizeof(int64_t) * (nq + 1), &dptr));
-  HS_CHECK(up(q->sp_dims + base, sizeof(uint32_t) * nnz, &ddims));
-  HS_CHECK(up(q->sp_vals + base, sizeof(float) * nnz, &dvals));
-  if (ix.d_dense > 0) {
-    if (!q->dense) HS_FAIL(HS_EINVAL, "query dense dimension mismatch");
-    HS_CHECK(up(q->dense, sizeof(float) * nq * ix.d_dense, &ddense));
+  if (ix.d_dense > 0 && nq > 0 && !q->dense) HS_FAIL(HS_EINVAL, "query dense dimension mismatch");
+  Arena lay{nullptr};
+  const size_t o_ptr = (size_t)lay.take<int64_t>(nq + 1);
+  const size_t o_dims = (size_t)lay.take<uint32_t>(nnz + 1);
+  const size_t o_vals = (size_t)lay.take<float>(nnz + 1);
+  const size_t o_dense = (size_t)lay.take<float>(nq * ix.d_dense + 1);
+  const size_t in_bytes = lay.off;
+  const size_t o_out = (size_t)lay.take<char>(result_bytes + 1);
+  HS_CHECK(grow(&ix.io_dev, &ix.io_dev_bytes, lay.off, false, ix.stream));
+  HS_CHECK(grow(&ix.io_host, &ix.io_host_bytes, lay.off, true, ix.stream));
+  char* hb = static_cast<char*>(ix.io_host);
+  char* db = static_cast<char*>(ix.io_dev);
+  int64_t* hp = reinterpret_cast<int64_t*>(hb + o_ptr);
+  for (int64_t i = 0; i <= nq; ++i) hp[i] = q->sp_indptr[i] - base;
+  if (nnz) {
+    std::memcpy(hb + o_dims, q->sp_dims + base, sizeof(uint32_t) * nnz);
+    std::memcpy(hb + o_vals, q->sp_vals + base, sizeof(float) * nnz);
   }
-  HS_CUDA(cudaStreamSynchronize(ix.stream));  // ptr vector goes out of scope
+  if (ix.d_dense > 0 && nq > 0)
+    std::memcpy(hb + o_dense, q->dense, sizeof(float) * nq * ix.d_dense);
+  HS_CUDA(cudaMemcpyAsync(db, hb, in_bytes, cudaMemcpyHostToDevice, ix.stream));
   out->b.nq = nq;
-  out->b.sp_indptr = static_cast<int64_t*>(dptr);
-  out->b.sp_dims = static_cast<uint32_t*>(ddims);
-  out->b.sp_vals = static_cast<float*>(dvals);
-  out->b.dense = static_cast<float*>(ddense);
+  out->b.sp_indptr = reinterpret_cast<int64_t*>(db + o_ptr);
+  out->b.sp_dims = reinterpret_cast<uint32_t*>(db + o_dims);
+  out->b.sp_vals = reinterpret_cast<float*>(db + o_vals);
+  out->b.dense = ix.d_dense > 0 ? reinterpret_cast<float*>(db + o_dense) : nullptr;
   out->b.nnz = nnz;
   out->b.max_row_nnz = max_row;
   out->nnz = nnz;
   out->max_row = max_row;
+  out->out = db + o_out;
+  out->out_host = hb + o_out;
   return HS_OK;
 }
 
@@ -511,6 +533,8 @@ int hs_index_create(const hs_index_desc* ds, int device, hs_index_t* out) {
       HS_CUDA(cudaMalloc(&tmp, std::max<size_t>((size_t)ix->npairs * n, 1)));
       if (n) HS_CUDA(cudaMemcpy(tmp, ds->packed, (size_t)ix->npairs * n, cudaMemcpyHostToDevice));
       launch_to_vertical(tmp, n, K, ix->vstride, ix->vcodes, 0);
+      HS_CHECK(dalloc(*ix, &ix->hcodes, (size_t)ceil_div(K, 8) * n));
+      launch_to_hcodes(tmp, n, K, ix->hcodes, 0);
       HS_CUDA(cudaDeviceSynchronize());
       cudaFree(tmp);
     }
@@ -566,28 +590,30 @@ int hs_search_batch(hs_index_t index, const hs_query_batch* queries,
   HS_CUDA(cudaSetDevice(index->device));
   Sizes sz;
   HS_CHECK(resolve_sizes(*index, params, &sz));
-  DevQueries dq;
-  HS_CHECK(upload_queries(*index, queries, &dq, true));
+  if (!queries) HS_FAIL(HS_EINVAL, "null query batch");
   const int64_t nq = queries->nq;
   const int64_t total = nq * sz.kh;
-  int64_t* d_ids = nullptr;
-  double* d_sc = nullptr;
-  HS_CUDA(cudaMalloc(&d_ids, sizeof(int64_t) * std::max<int64_t>(total, 1)));
-  HS_CUDA(cudaMalloc(&d_sc, sizeof(double) * std::max<int64_t>(total, 1)));
+  const size_t ids_bytes = ((sizeof(int64_t) * total + 255) & ~size_t(255));
+  DevQueries dq;
+  HS_CHECK(upload_queries(*index, queries, &dq, true, ids_bytes + sizeof(double) * total));
+  int64_t* d_ids = reinterpret_cast<int64_t*>(dq.out);
+  double* d_sc = reinterpret_cast<double*>(dq.out + ids_bytes);
   Timer tm(index, index->stream, index->timing);
   int rc = run_search(*index, dq.b, dq.nnz, dq.max_row, params, d_ids, d_sc, index->stream, &tm,
                       true);
-  if (rc == HS_OK && total) {
-    cudaMemcpyAsync(out_ids, d_ids, sizeof(int64_t) * total, cudaMemcpyDeviceToHost, index->stream);
-    cudaMemcpyAsync(out_scores, d_sc, sizeof(double) * total, cudaMemcpyDeviceToHost,
-                    index->stream);
-  }
-  cudaError_t e = cudaStreamSynchronize(index->stream);
+  cudaError_t e = cudaSuccess;
+  if (rc == HS_OK && total)
+    e = cudaMemcpyAsync(dq.out_host, dq.out, ids_bytes + sizeof(double) * total,
+                        cudaMemcpyDeviceToHost, index->stream);
+  const cudaError_t es = cudaStreamSynchronize(index->stream);
+  if (e == cudaSuccess) e = es;
   tm.finish(stage_seconds);
-  cudaFree(d_ids);
-  cudaFree(d_sc);
   if (rc != HS_OK) return rc;
   if (e != cudaSuccess) HS_FAIL(HS_ECUDA, std::string("CUDA error: ") + cudaGetErrorString(e));
+  if (total) {
+    std::memcpy(out_ids, dq.out_host, sizeof(int64_t) * total);
+    std::memcpy(out_scores, dq.out_host + ids_bytes, sizeof(double) * total);
+  }
   return HS_OK;
 }
 

@@ -43,6 +43,7 @@ struct DeviceIndex {
   int32_t* cen_off = nullptr;  // [K] offset of centers[k] in `centers`
   float* centers = nullptr;
   uint32_t* vcodes = nullptr;  // [K][vstride] vertical nibble planes (stage1.cu)
+  uint32_t* hcodes = nullptr;  // [ceil(K/8)][n] 8 codes per point word (lut16_tc.cu)
   int64_t vstride = 0;
   int has_sq = 0;
   float *sq_lo = nullptr, *sq_step = nullptr;
@@ -65,6 +66,12 @@ struct DeviceIndex {
   // scratch arena (grown on demand, owned by the handle)
   void* scratch = nullptr;
   size_t scratch_bytes = 0;
+  // host entry point I/O staging (grown on demand): device query/result
+  // buffers and a pinned host mirror, so a call does no cudaMalloc/cudaFree
+  void* io_dev = nullptr;
+  size_t io_dev_bytes = 0;
+  void* io_host = nullptr;
+  size_t io_host_bytes = 0;
 
   // per-kernel timing of the last batch (CUDA events; bench roofline)
   bool timing = true;      // host entry point
@@ -142,8 +149,10 @@ int launch_stage1(const DeviceIndex& ix, const QueryView& q, const Stage1Plan& p
                   int64_t tot_ld = 0);
 
 // lut16_tc.cu (tensor-core batched LUT16 totals)
-size_t lut16_tc_smem();
+bool lut16_tc_supported(const DeviceIndex& ix);
 int64_t lut16_tc_ld(int64_t n);
+int64_t lut16_tc_group(const DeviceIndex& ix);  // queries per tensor-core group
+void launch_to_hcodes(const uint8_t* packed, int64_t n, int K, uint32_t* h, cudaStream_t st);
 int launch_lut16_tc(const DeviceIndex& ix, const uint8_t* luts, int64_t nq, uint16_t* tot,
                     int64_t ld, cudaStream_t st);
 

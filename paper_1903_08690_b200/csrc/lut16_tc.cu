@@ -1,46 +1,59 @@
 // lut16_tc.cu — K2 on the 5th-generation tensor cores: batched LUT16 totals.
 //
-// For a group of 128 queries and a block of 256 points the LUT16 totals
+// For a block of 128 points and a group of NQ queries the LUT16 totals
 // (reference lut16_scan, dense.py:263-317: total = sum_k table[k][code_k])
 // are an integer matrix product
 //
-//     T[q][n] = sum_{k,c} LUT[q][k][c] * onehot(code_k(n) == c)
+//     T[n][q] = sum_{k,c} onehot(code_k(n) == c) * LUT[q][k][c]
 //
-// with A = the queries' u8 tables (128 x 16K, K-major: one 16-byte row per
-// (query, subspace) — exactly the LUT layout) and B = the one-hot expansion of
-// the points' 4-bit codes (256 x 16K, K-major: one 16-byte row per (point,
-// subspace) with a single 1).  tcgen05.mma kind::i8 (u8 x u8 -> s32) computes
-// it exactly in TMEM (K*255 < 2^31), so totals are bit-identical to the scalar
-// semantics; the epilogue narrows them to u16 (K <= 257 keeps them < 2^16)
-// for the fused stage-1 kernel, which adds the sparse part and selects.
+// issued as tcgen05.mma kind::i8 (u8 x u8 -> s32, exact: K*255 < 2^31) in the
+// "A in tensor memory" form:
+//   A (128 points x 16K, K-major) = the one-hot expansion of the points'
+//     4-bit codes, generated in registers and written straight into TMEM with
+//     tcgen05.st (no shared-memory round trip for the expanded operand);
+//   B (NQ queries x 16K, K-major) = the group's u8 tables, resident in shared
+//     memory while the CTA walks the group's point blocks (one 16-byte row per
+//     (query, subspace) — exactly the LUT layout), so the only shared-memory
+//     traffic in the steady state is the tensor core reading B;
+//   D (128 x NQ s32) in TMEM, double-buffered so the epilogue of block i
+//     overlaps the MMAs of block i+1.
+// Totals are bit-identical to the scalar semantics; the epilogue narrows them
+// to u16 (K <= 257 keeps them < 2^16) row-major [query][point] for the fused
+// stage-1 kernel, which adds the sparse part and selects.
 //
-// Shared-memory operand layout (SWIZZLE_NONE, K-major "interleave" canonical
-// layout): 16-byte column block b (= subspace) holds all MN rows
-// contiguously, 16 B per row, so 8-row core matrices are 128 B apart
-// (SBO = 128 B) and the two 16-byte K halves of one MMA are MN*16 B apart
-// (LBO).  One MMA consumes 32 B of K = 2 subspaces.
+// Warp roles (288 threads, one CTA per SM — it owns all 512 TMEM columns):
+//   warps 0-3  producers: thread = point lane; per K chunk of 8 subspaces one
+//              coalesced u32 load (8 codes), 32 one-hot words, one
+//              tcgen05.st.32x32b.x32 into an A ring slot, arrive `afull`;
+//   warps 4-7  epilogue: tcgen05.ld the finished accumulator, store u16,
+//              arrive `dempty`;
+//   warp 8     TMEM allocation; lane 0 issues the MMAs (<= 4 per chunk,
+//              K = 32 B = 2 subspaces each) and the tcgen05.commit arrivals.
 //
-// Pipeline per CTA (query group g, a range of point blocks): K is walked in
-// chunks of kKC subspaces through two shared-memory stages; all 256 threads
-// write a stage (LUT rows + one-hot rows), fence the async proxy, and thread 0
-// issues the chunk's MMAs and commits them to the stage's mbarrier, so the
-// next chunk is produced while the tensor core consumes this one.  After the
-// last chunk of a block the epilogue warps read the 128x256 s32 accumulator
-// (warp w reads TMEM lanes 32*(w%4).. of columns 128*(w/4)..) and store u16
-// totals row-major [query][point].
+// Shared-memory B layout (SWIZZLE_NONE, K-major canonical): 16-byte column
+// block k (= subspace) holds the NQ query rows contiguously, so 8-row core
+// matrices are 128 B apart (SBO) and the two subspaces of one MMA are NQ*16 B
+// apart (LBO).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <mutex>
+
 #include "kernels.cuh"
 
 namespace hs {
 
 namespace {
 
-constexpr int kTM = 128;      // queries per group (MMA M)
-constexpr int kTN = 256;      // points per block (MMA N)
-constexpr int kKC = 8;        // subspaces per K chunk (= 4 MMAs of K=32 B)
-constexpr int kTThreads = 256;
-constexpr int kStageA = kKC * kTM * 16;  // 16 KB
-constexpr int kStageB = kKC * kTN * 16;  // 32 KB
-constexpr int kStages = 2;
+constexpr int kPM = 128;       // points per block (MMA M, TMEM lanes)
+constexpr int kKC = 8;         // subspaces per K chunk (4 MMAs, 32 TMEM columns of A)
+constexpr int kProd = 128;     // producer threads (warps 0-3)
+constexpr int kThreadsTc = 288;
+constexpr int kTmemCols = 512;
+constexpr int kMaxNQ = 224;    // 2*NQ accumulator + >= 2 A slots of 32 columns <= 512
+constexpr size_t kStageBytes = 4 * 2 * 32 * 32 * 2;  // epilogue staging: 4 warps x 2 x 32x32 u16
+constexpr size_t kSmemBudget = 200 * 1024;          // resident B (the group's tables)
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -56,11 +69,11 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo_bytes,
   return d;
 }
 
-// kind::i8 instruction descriptor: u8 x u8 -> s32, K-major A and B, M=128, N=256
-__host__ __device__ constexpr uint32_t idesc_u8() {
-  return (2u << 4)               // c_format = S32
+// kind::i8 instruction descriptor: u8 x u8 -> s32, K-major A and B, M=128, N=n
+__device__ __forceinline__ uint32_t idesc_u8(int n) {
+  return (2u << 4)                 // c_format = S32
          | (0u << 7) | (0u << 10)  // a/b format = unsigned 8-bit
-         | ((uint32_t)(kTN >> 3) << 17) | ((uint32_t)(kTM >> 4) << 24);
+         | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(kPM >> 4) << 24);
 }
 
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
@@ -73,17 +86,34 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "WAIT_%=:\n\t"
       "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
       "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
-      "r"(parity));
+      "r"(parity)
+      : "memory");
 }
 
-__device__ __forceinline__ void mma_u8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void mma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc,
                                        uint32_t idesc, uint32_t accumulate) {
-  const uint32_t z = 0;
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, {%5, %6, %7, %8}, p;\n\t}" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(z), "r"(z), "r"(z), "r"(z));
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+// TMA tensor store of one 32x32 u16 tile (rows = queries, cols = points)
+__device__ __forceinline__ void tma_store_tile(const CUtensorMap* map, const void* ssrc, int x,
+                                               int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+          reinterpret_cast<uint64_t>(map)),
+      "r"(smem_u32(ssrc)), "r"(x), "r"(y)
+      : "memory");
 }
 
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
@@ -103,200 +133,325 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
         "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])             \
       : "r"(taddr))
 
+#define TMEM_ST32(taddr, r)                                                                        \
+  asm volatile(                                                                                    \
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"  \
+      "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr), \
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),      \
+      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]),            \
+      "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]),          \
+      "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]),          \
+      "r"(r[29]), "r"(r[30]), "r"(r[31])                                                           \
+      : "memory")
+
 struct TcArgs {
-  int64_t n;          // points
-  int64_t nq;         // queries in this batch
-  int K, Kp;          // subspaces (codes), padded LUT rows
-  const uint32_t* vcodes;
-  int64_t vstride;    // u32 words per subspace plane
-  const uint8_t* luts;  // [nq][Kp][16]
-  uint16_t* tot;      // [nq][ld] u16 totals
+  int64_t n;               // points
+  int64_t nq;              // queries in this batch
+  int K, Kp;               // subspaces (codes), LUT rows per query (even)
+  int nq_grp;              // NQ: queries per group (MMA N, multiple of 32)
+  int slots;               // A ring slots (32 TMEM columns each)
+  const uint32_t* hcodes;  // [ceil(K/8)][n]: nibble s = code of subspace 8c+s
+  const uint8_t* luts;     // [nq][Kp][16]
+  uint16_t* tot;           // [nq][ld] u16 totals
   int64_t ld;
-  int blocks_per_cta;
+  int64_t ngroups;
+  int64_t nblocks;         // point blocks of 128
+  int64_t items_per_cta;   // contiguous (group, block) items per CTA
 };
 
-__global__ void __launch_bounds__(kTThreads, 1) k_lut16_tc(TcArgs a) {
+// One-hot words of 8 subspaces: word 4s + i has byte (code & 3) = 1 when
+// (code >> 2) == i, for the code of subspace s (its 16-byte K row); subspaces
+// at or past `valid` are all zero.
+__device__ __forceinline__ void onehot8(uint32_t w, int valid, uint32_t* r) {
+#pragma unroll
+  for (int s = 0; s < kKC; ++s) {
+    const uint32_t code = (w >> (4 * s)) & 15u;
+    const uint32_t bit = s < valid ? 1u << (8 * (code & 3u)) : 0u;
+    const uint32_t c4 = code >> 2;
+    r[4 * s + 0] = c4 == 0 ? bit : 0u;
+    r[4 * s + 1] = c4 == 1 ? bit : 0u;
+    r[4 * s + 2] = c4 == 2 ? bit : 0u;
+    r[4 * s + 3] = c4 == 3 ? bit : 0u;
+  }
+}
+
+__global__ void __launch_bounds__(kThreadsTc, 1)
+    k_lut16_tc(TcArgs a, const __grid_constant__ CUtensorMap tmap) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  unsigned char* sA = smem_raw;                      // [stage][kKC][128][16]
-  unsigned char* sB = sA + kStages * kStageA;        // [stage][kKC][256][16]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + kStages * kStageB);  // [kStages]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + kStages);
+  const int NQ = a.nq_grp;
+  unsigned char* sB = smem_raw;  // [Kp][NQ][16]
+  uint16_t* sStage = reinterpret_cast<uint16_t*>(sB + (size_t)a.Kp * NQ * 16);  // epilogue staging
+  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(sStage) + kStageBytes);
+  uint64_t* afull = bars;              // [slots] producers -> MMA (count 128)
+  uint64_t* aempty = afull + a.slots;  // [slots] MMA commit -> producers
+  uint64_t* dfull = aempty + a.slots;  // [2]     MMA commit -> epilogue
+  uint64_t* dempty = dfull + 2;        // [2]     epilogue -> MMA (count 128)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dempty + 2);
 
-  const int tid = threadIdx.x, warp = tid >> 5;
-  const int64_t g = blockIdx.x;  // query group
-  const int64_t q0 = g * kTM;
-  const int64_t nblocks = (a.n + kTN - 1) / kTN;
-  const int64_t blk0 = (int64_t)blockIdx.y * a.blocks_per_cta;
-  const int64_t blk1 = min(nblocks, blk0 + a.blocks_per_cta);
-  const int nkc = (a.K + kKC - 1) / kKC;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t it0 = (int64_t)blockIdx.x * a.items_per_cta;
+  const int64_t it1 = min(a.ngroups * a.nblocks, it0 + a.items_per_cta);
+  if (it0 >= it1) return;
+  const int nkc = (a.Kp + kKC - 1) / kKC;
 
-  if (warp == 0) {
+  if (warp == 8) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(tmem_slot)),
-                 "r"(kTN));
+                 "r"(kTmemCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 0) {
-    for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
+    for (int s = 0; s < a.slots; ++s) {
+      mbar_init(&afull[s], kProd);
+      mbar_init(&aempty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&dfull[b], 1);
+      mbar_init(&dempty[b], kProd);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = *tmem_slot;
-  const uint32_t idesc = idesc_u8();
-  uint32_t phase[kStages] = {0u, 0u};
-  bool pending[kStages] = {false, false};  // a commit on this stage not yet waited for
+  const uint32_t tmem_a = tmem + 2u * (uint32_t)NQ;  // A ring after the two accumulators
 
-  // Producer registers: this thread's 4 LUT rows (A) and 8 code words (B) of
-  // the next K chunk are loaded one chunk ahead so global-load latency hides
-  // behind the current chunk's shared-memory writes and MMAs.
-  constexpr int kArows = kTM * kKC / kTThreads;  // 4
-  uint4 ra[kArows];
-  uint32_t rc[kKC];
-  auto load_chunk = [&](int64_t blk, int kc) {
-    const int s0 = kc * kKC;
-#pragma unroll
-    for (int r = 0; r < kArows; ++r) {
-      const int i = tid + r * kTThreads;
-      const int q = i & (kTM - 1), s = i >> 7;
-      ra[r] = (q0 + q < a.nq && s0 + s < a.Kp)
-                  ? __ldg(reinterpret_cast<const uint4*>(a.luts + ((q0 + q) * a.Kp + s0 + s) * 16))
-                  : make_uint4(0u, 0u, 0u, 0u);
-    }
-    const int64_t p = blk * kTN + tid;
-#pragma unroll
-    for (int s = 0; s < kKC; ++s)
-      rc[s] = (s0 + s < a.K && p < a.n) ? __ldg(a.vcodes + (int64_t)(s0 + s) * a.vstride + (p >> 3))
-                                        : 0u;
-  };
-  if (blk0 < blk1) load_chunk(blk0, 0);
-
-  for (int64_t blk = blk0; blk < blk1; ++blk) {
-    const int64_t p0 = blk * kTN;
-    for (int kc = 0; kc < nkc; ++kc) {
-      const int st = kc & 1;
-      // the MMAs that last read this stage must be done before overwriting it
-      if (pending[st]) {
-        mbar_wait(&bars[st], phase[st]);
-        phase[st] ^= 1u;
-        pending[st] = false;
-      }
-      unsigned char* A = sA + st * kStageA;
-      unsigned char* B = sB + st * kStageB;
-#pragma unroll
-      for (int r = 0; r < kArows; ++r) {
-        const int i = tid + r * kTThreads;
-        *reinterpret_cast<uint4*>(A + (i >> 7) * (kTM * 16) + (i & (kTM - 1)) * 16) = ra[r];
-      }
-      {
-        const int sh = 4 * (int)((p0 + tid) & 7);
-#pragma unroll
-        for (int s = 0; s < kKC; ++s) {
-          const uint32_t code = (rc[s] >> sh) & 15u;
-          const uint32_t bit = 1u << (8 * (code & 3u));
-          const uint32_t c4 = code >> 2;
-          uint4 v;
-          v.x = c4 == 0 ? bit : 0u;
-          v.y = c4 == 1 ? bit : 0u;
-          v.z = c4 == 2 ? bit : 0u;
-          v.w = c4 == 3 ? bit : 0u;
-          if (kc * kKC + s >= a.K) v = make_uint4(0u, 0u, 0u, 0u);
-          *reinterpret_cast<uint4*>(B + s * (kTN * 16) + tid * 16) = v;
-        }
-      }
-      // prefetch the next chunk (possibly of the next block) into registers
-      if (kc + 1 < nkc) load_chunk(blk, kc + 1);
-      else if (blk + 1 < blk1) load_chunk(blk + 1, 0);
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      __syncthreads();
-      if (tid == 0) {
-        asm volatile("tcgen05.fence::after_thread_sync;");
-        const uint32_t a_addr = smem_u32(A), b_addr = smem_u32(B);
-#pragma unroll
-        for (int m = 0; m < kKC / 2; ++m) {
-          const uint64_t ad = smem_desc(a_addr + m * 2 * (kTM * 16), kTM * 16, 128);
-          const uint64_t bd = smem_desc(b_addr + m * 2 * (kTN * 16), kTN * 16, 128);
-          mma_u8(tmem, ad, bd, idesc, (kc > 0 || m > 0) ? 1u : 0u);
-        }
-        mma_commit(&bars[st]);
-      }
-      pending[st] = true;
-    }
-    // wait for the block's last chunk (commit tracks all earlier MMAs too)
-#pragma unroll
-    for (int st = 0; st < kStages; ++st) {
-      if (pending[st]) {
-        mbar_wait(&bars[st], phase[st]);
-        phase[st] ^= 1u;
-        pending[st] = false;
-      }
-    }
-    asm volatile("tcgen05.fence::after_thread_sync;");
-    // epilogue: warp w reads lanes 32*(w%4).. (queries) and columns 128*(w/4)..
+  // Items are (group, block) pairs in group-major order; a CTA's contiguous
+  // range spans few groups.  Per group segment: load the group's tables into
+  // shared memory, then stream its blocks through the pipeline.  Pipeline
+  // counters run across segments so the barrier parities stay in step.
+  int64_t blk_it = 0;
+  int slot = 0;          // A ring position (producers and issuer walk it in step)
+  uint32_t round = 0;    // completed passes over the ring
+  int64_t ep_tile = 0;  // epilogue tiles issued by this thread (staging parity)
+  for (int64_t seg = it0; seg < it1;) {
+    const int64_t g = seg / a.nblocks;
+    const int64_t b0 = seg % a.nblocks;
+    const int64_t b1 = min(a.nblocks, b0 + (it1 - seg));
+    const int64_t q0 = g * NQ;
+    const int64_t nblk = b1 - b0;
+    // ---- B: the group's tables, [k][q][16].  Safe to overwrite: the
+    // previous segment's epilogue waited for its last dfull commit, which
+    // tracks every earlier MMA, before reaching this barrier.
+    __syncthreads();
     {
-      const int quad = warp & 3, half = warp >> 2;
-      const int64_t q = q0 + quad * 32 + (tid & 31);
-      uint16_t* row = a.tot + q * a.ld + p0 + half * 128;
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t r[32];
-        const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(half * 128 + c * 32);
-        TMEM_LD32(taddr, r);
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        if (q < a.nq) {
-          uint4 w[4];
-          uint32_t* wp = reinterpret_cast<uint32_t*>(w);
-#pragma unroll
-          for (int j = 0; j < 16; ++j) wp[j] = (r[2 * j] & 0xFFFFu) | (r[2 * j + 1] << 16);
-          uint4* dst = reinterpret_cast<uint4*>(row + c * 32);
-#pragma unroll
-          for (int j = 0; j < 4; ++j) dst[j] = w[j];
+      const int rows = a.Kp * NQ;
+      for (int i = tid; i < rows; i += blockDim.x) {
+        const int k = i / NQ, q = i - k * NQ;
+        uint4 v = make_uint4(0u, 0u, 0u, 0u);
+        if (q0 + q < a.nq)
+          v = __ldg(reinterpret_cast<const uint4*>(a.luts + ((q0 + q) * a.Kp + k) * 16));
+        *reinterpret_cast<uint4*>(sB + (size_t)i * 16) = v;
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    __syncthreads();
+
+    if (warp < 4) {
+      // ---- producers: one-hot A chunks into the TMEM ring ----
+      const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+      for (int64_t bi = 0; bi < nblk; ++bi) {
+        const int64_t p = (b0 + bi) * kPM + tid;
+        const bool live = p < a.n;
+        uint32_t wnext = live ? __ldg(a.hcodes + p) : 0u;
+        for (int c = 0; c < nkc; ++c) {
+          const uint32_t w = wnext;
+          if (c + 1 < nkc) wnext = live ? __ldg(a.hcodes + (int64_t)(c + 1) * a.n + p) : 0u;
+          uint32_t r[32];
+          onehot8(w, live ? min(kKC, a.K - c * kKC) : 0, r);
+          if (round > 0) {
+            mbar_wait(&aempty[slot], (round - 1) & 1u);
+            asm volatile("tcgen05.fence::after_thread_sync;");
+          }
+          TMEM_ST32(tmem_a + lane_base + (uint32_t)(slot * 32), r);
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+          asm volatile("tcgen05.fence::before_thread_sync;");
+          mbar_arrive(&afull[slot]);
+          if (++slot == a.slots) {
+            slot = 0;
+            ++round;
+          }
         }
       }
+    } else if (warp < 8) {
+      // ---- epilogue: accumulator -> u16 totals [query][point] ----
+      // Per 32x32 tile (32 points of this warp's lanes x 32 queries): the
+      // tile is transposed through shared memory (conflict-free u16 stores,
+      // one query row per 64 B) and one lane hands it to the TMA engine as a
+      // 2-D tensor store; two staging buffers per warp.
+      const int quad = warp & 3;
+      const uint32_t lane_base = (uint32_t)(quad * 32) << 16;
+      uint16_t* stg = sStage + quad * 2 * 1024;
+      for (int64_t bi = 0; bi < nblk; ++bi) {
+        const int64_t bt = blk_it + bi;
+        const int buf = (int)(bt & 1);
+        mbar_wait(&dfull[buf], (uint32_t)((bt >> 1) & 1));
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const int64_t pbase = (b0 + bi) * kPM + quad * 32;
+        for (int c = 0; c < NQ; c += 32) {
+          uint32_t r[32];
+          TMEM_LD32(tmem + lane_base + (uint32_t)(buf * NQ + c), r);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          if (c + 32 >= NQ) {  // accumulator fully read: release it to the MMA
+            asm volatile("tcgen05.fence::before_thread_sync;");
+            mbar_arrive(&dempty[buf]);
+          }
+          const int sb = (int)(ep_tile & 1);
+          if (ep_tile >= 2 && lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          __syncwarp();
+          uint16_t* t = stg + sb * 1024;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) t[j * 32 + lane] = (uint16_t)r[j];
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) {
+            if (q0 + c < a.nq) tma_store_tile(&tmap, t, (int)pbase, (int)(q0 + c));
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          }
+          ++ep_tile;
+        }
+      }
+    } else if (lane == 0) {
+      // ---- MMA issuer ----
+      const uint32_t idesc = idesc_u8(NQ);
+      const uint32_t b_addr = smem_u32(sB);
+      for (int64_t bi = 0; bi < nblk; ++bi) {
+        const int64_t bt = blk_it + bi;
+        const int buf = (int)(bt & 1);
+        if (bt >= 2) {
+          mbar_wait(&dempty[buf], (uint32_t)(((bt >> 1) - 1) & 1));
+          asm volatile("tcgen05.fence::after_thread_sync;");
+        }
+        const uint32_t d = tmem + (uint32_t)(buf * NQ);
+        for (int c = 0; c < nkc; ++c) {
+          mbar_wait(&afull[slot], round & 1u);
+          asm volatile("tcgen05.fence::after_thread_sync;");
+          const int kc = min(kKC, a.Kp - c * kKC);  // even
+          for (int m = 0; m < kc / 2; ++m) {
+            const int k0 = c * kKC + 2 * m;
+            const uint64_t bd =
+                smem_desc(b_addr + (uint32_t)(k0 * NQ * 16), (uint32_t)(NQ * 16), 128);
+            mma_ts(d, tmem_a + (uint32_t)(slot * 32 + m * 8), bd, idesc,
+                   (c > 0 || m > 0) ? 1u : 0u);
+          }
+          mma_commit(&aempty[slot]);
+          if (++slot == a.slots) {
+            slot = 0;
+            ++round;
+          }
+        }
+        mma_commit(&dfull[buf]);
+      }
     }
-    asm volatile("tcgen05.fence::before_thread_sync;");
-    __syncthreads();  // TMEM reads done before the next block's MMAs overwrite it
+    blk_it += nblk;
+    seg += nblk;
   }
+  if (warp >= 4 && warp < 8 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   __syncthreads();
-  if (warp == 0)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTN));
+  if (warp == 8) {
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(kTmemCols));
+  }
+}
+
+// pair-major packed codes (dense.py:156-170) -> [ceil(K/8)][n] u32, nibble s
+// of word (c, p) = code of subspace 8c+s of point p (zero past K)
+__global__ void k_to_hcodes(const uint8_t* __restrict__ packed, int64_t n, int npairs,
+                            uint32_t* __restrict__ h) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int c = blockIdx.y;
+  if (p >= n) return;
+  uint32_t w = 0;
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    const int pair = 4 * c + t;
+    if (pair < npairs) w |= (uint32_t)packed[(int64_t)pair * n + p] << (8 * t);
+  }
+  h[(int64_t)c * n + p] = w;
+}
+
+int pick_nq(int Kp, int64_t nq) {
+  const int64_t by_smem = (int64_t)(kSmemBudget - 1024) / ((int64_t)Kp * 16);
+  int64_t v = std::min<int64_t>(kMaxNQ, by_smem) / 32 * 32;
+  const int64_t need = ceil_div(nq, 32) * 32;  // small batches: no idle columns
+  if (need < v) v = need;
+  return (int)std::max<int64_t>(v, 0);
 }
 
 }  // namespace
 
-size_t lut16_tc_smem() {
-  return kStages * (kStageA + kStageB) + kStages * sizeof(uint64_t) + 16;
+bool lut16_tc_supported(const DeviceIndex& ix) {
+  return ix.hcodes != nullptr && ix.K > 0 && ix.K <= 257 && pick_nq(ix.Kp, 1LL << 40) >= 32;
 }
 
-int64_t lut16_tc_ld(int64_t n) { return ((n + kTN - 1) / kTN) * kTN; }
+int64_t lut16_tc_ld(int64_t n) { return ((n + kPM - 1) / kPM) * kPM; }
+
+int64_t lut16_tc_group(const DeviceIndex& ix) { return pick_nq(ix.Kp, 1LL << 40); }
+
+void launch_to_hcodes(const uint8_t* packed, int64_t n, int K, uint32_t* h, cudaStream_t st) {
+  if (n <= 0 || K <= 0) return;
+  const int nkc = (K + kKC - 1) / kKC;
+  dim3 grid((unsigned)ceil_div(n, 256), (unsigned)nkc);
+  k_to_hcodes<<<grid, 256, 0, st>>>(packed, n, (K + 1) / 2, h);
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
 
 int launch_lut16_tc(const DeviceIndex& ix, const uint8_t* luts, int64_t nq, uint16_t* tot,
                     int64_t ld, cudaStream_t st) {
   if (nq <= 0 || ix.n <= 0) return HS_OK;
-  if (ix.K > 257) HS_FAIL(HS_EUNSUPPORTED, "tensor-core LUT16 needs K <= 257");
+  if (!lut16_tc_supported(ix)) HS_FAIL(HS_EUNSUPPORTED, "tensor-core LUT16 unsupported for this index");
+  const int NQ = pick_nq(ix.Kp, nq);
   TcArgs a;
   a.n = ix.n;
   a.nq = nq;
   a.K = ix.K;
   a.Kp = ix.Kp;
-  a.vcodes = ix.vcodes;
-  a.vstride = ix.vstride;
+  a.nq_grp = NQ;
+  a.slots = std::min(8, (kTmemCols - 2 * NQ) / 32);
+  a.hcodes = ix.hcodes;
   a.luts = luts;
   a.tot = tot;
   a.ld = ld;
-  const int64_t groups = ceil_div(nq, kTM);
-  const int64_t nblocks = ceil_div(ix.n, kTN);
-  // ~2 CTAs per SM worth of work items over (groups x point ranges)
-  int64_t ranges = ceil_div(2LL * kNumSMs, groups);
-  if (ranges > nblocks) ranges = nblocks;
-  if (ranges < 1) ranges = 1;
-  a.blocks_per_cta = (int)ceil_div(nblocks, ranges);
-  ranges = ceil_div(nblocks, a.blocks_per_cta);
-  const size_t smem = lut16_tc_smem();
+  a.ngroups = ceil_div(nq, NQ);
+  a.nblocks = ceil_div(ix.n, kPM);
+  // one CTA per SM (it owns all of TMEM), equal contiguous shares of the
+  // (group, block) items
+  const int64_t items = a.ngroups * a.nblocks;
+  const int64_t ctas = std::min<int64_t>(kNumSMs, items);
+  a.items_per_cta = ceil_div(items, ctas);
+  const int64_t grid = ceil_div(items, a.items_per_cta);
+  if (ld % kPM != 0) HS_FAIL(HS_EINVAL, "tensor-core totals stride must be a multiple of 128");
+  const size_t smem =
+      (size_t)a.Kp * NQ * 16 + kStageBytes + (2 * a.slots + 4) * sizeof(uint64_t) + 16;
   HS_CUDA(cudaFuncSetAttribute(k_lut16_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  dim3 grid((unsigned)groups, (unsigned)ranges);
-  k_lut16_tc<<<grid, kTThreads, smem, st>>>(a);
+  // totals [nq][ld] u16 as a 2-D tensor; 32x32 boxes, no swizzle
+  CUtensorMap tmap;
+  auto enc = encode_fn();
+  if (!enc) HS_FAIL(HS_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  const cuuint64_t gdim[2] = {(cuuint64_t)ld, (cuuint64_t)nq};
+  const cuuint64_t gstride[1] = {(cuuint64_t)ld * sizeof(uint16_t)};
+  const cuuint32_t box[2] = {32, 32};
+  const cuuint32_t estride[2] = {1, 1};
+  if (enc(&tmap, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, tot, gdim, gstride, box, estride,
+          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+          CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    HS_FAIL(HS_ECUDA, "cuTensorMapEncodeTiled failed for the totals buffer");
+  k_lut16_tc<<<(unsigned)grid, kThreadsTc, smem, st>>>(a, tmap);
   HS_CUDA(cudaGetLastError());
   return HS_OK;
 }

@@ -135,6 +135,15 @@ __device__ __forceinline__ uint32_t count_below_known(const uint2* __restrict__ 
   return lower_bound_ids(post, prev + 1, right, key) - cur;
 }
 
+// Chunk accumulator layout: point 16*t + j of the chunk lives at
+// j*256 + (t ^ j).  The owner threads' reads (fixed j, consecutive t) and the
+// posting stream's writes (consecutive points) both spread over all banks.
+static_assert(kChunk == kThreads * kPPT, "chunk = threads x points per thread");
+__device__ __forceinline__ int acc_ix(uint32_t local) {
+  const uint32_t j = local & (kPPT - 1), t = local / kPPT;
+  return (int)(j * kThreads + (t ^ j));
+}
+
 struct Smem {
   Cand* buf;
   Cand* th;
@@ -206,7 +215,21 @@ __device__ __forceinline__ void find_bin(const unsigned* hist, int need, bool de
 // chunk accumulator must survive, the offer loop re-reads it for scores.
 static_assert(sizeof(double) * kThreads >= 256 * sizeof(unsigned), "histogram fits the staging area");
 
-__device__ void compact(Smem& s, int k) {
+// Smallest u16 LUT total whose dense-only score (bias_total + scale*t) + offset
+// reaches the threshold score (65536: none).  The f64 ops are monotone in t
+// (scale >= 0), so a point with no sparse part and total < tlim cannot pass.
+__device__ int dense_tlim(double ths, double btot, double scl, double off) {
+  int lo = 0, hi = 65536;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    const double v = __dadd_rn(__dadd_rn(btot, __dmul_rn(scl, (double)mid)), off);
+    if (v >= ths) hi = mid;
+    else lo = mid + 1;
+  }
+  return lo;
+}
+
+__device__ void compact(Smem& s, int k, bool dense, double btot, double scl, double off) {
   const int cnt = s.ctl[0];
   __syncthreads();  // every thread has read ctl[0]
   if (cnt <= k) return;
@@ -307,6 +330,7 @@ __device__ void compact(Smem& s, int k) {
     *s.th = w;
     s.ctl[0] = kept;
     s.ctl[2] = 1;
+    s.ctl[3] = dense ? dense_tlim(w.s, btot, scl, off) : 0;
   }
   __syncthreads();
 }
@@ -512,28 +536,33 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
       const int64_t cg = cb / kChunk;
       const uint32_t e0 = __ldg(qboff + cg), e1 = __ldg(qboff + cg + 1);
       if (e1 > e0) {
-        // The bucket is staged through shared memory in tiles of 256 entries
-        // (one coalesced load per thread); every thread then walks the tile
-        // and adds the entries that land on its own 16 points.  Bucket order
-        // is ascending dim per point => the reference summation order.
-        double* mine = s.acc + tid * kPPT;
-#pragma unroll
-        for (int j = 0; j < kPPT; ++j) mine[j] = 0.0;
-        for (uint32_t base = e0; base < e1; base += kThreads) {
-          const uint32_t e = base + tid;
-          if (e < e1) {
-            s.bslot[tid] = __ldg(qslots + e) - (uint32_t)cb;
-            s.bval[tid] = __ldg(qvals + e);
-          }
-          __syncthreads();
-          const int cnt = (int)min((uint32_t)kThreads, e1 - base);
-          for (int j = 0; j < cnt; ++j) {
-            const uint32_t local = s.bslot[j];
-            HS_DCHECK(local < (uint32_t)kChunk);
-            if ((local >> 4) == (uint32_t)tid) mine[local & 15] += s.bval[j];
-          }
-          __syncthreads();
+        // Entries are in ascending dim order within the chunk.  The first
+        // entry of each point sums all of that point's entries in that order
+        // (the reference's per-point summation order) and stores the total;
+        // every other point of the chunk keeps the zero.
+        const uint32_t L = e1 - e0;
+        for (int i = tid; i < kChunk; i += kThreads) s.acc[i] = 0.0;
+        const bool staged = L <= (uint32_t)kThreads;
+        if (staged && tid < (int)L) {
+          s.bslot[tid] = __ldg(qslots + e0 + tid);
+          s.bval[tid] = __ldg(qvals + e0 + tid);
         }
+        __syncthreads();
+        for (uint32_t i = tid; i < L; i += kThreads) {
+          const uint32_t sl = staged ? s.bslot[i] : __ldg(qslots + e0 + i);
+          bool first = true;
+          for (uint32_t j = 0; j < i && first; ++j)
+            first = (staged ? s.bslot[j] : __ldg(qslots + e0 + j)) != sl;
+          if (!first) continue;
+          double sum = 0.0;
+          sum += staged ? s.bval[i] : __ldg(qvals + e0 + i);
+          for (uint32_t j = i + 1; j < L; ++j)
+            if ((staged ? s.bslot[j] : __ldg(qslots + e0 + j)) == sl)
+              sum += staged ? s.bval[j] : __ldg(qvals + e0 + j);
+          HS_DCHECK(sl - (uint32_t)cb < (uint32_t)kChunk);
+          s.acc[acc_ix(sl - (uint32_t)cb)] = sum;
+        }
+        __syncthreads();
         nact = 1;
         npost = 0;
       }
@@ -607,9 +636,8 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
         // few postings: every thread walks them all in dim order (broadcast
         // loads) and adds only those landing on its own 16 points — per-point
         // order stays ascending in dim with no block barriers
-        double* mine = s.acc + tid * kPPT;
   #pragma unroll
-        for (int j = 0; j < kPPT; ++j) mine[j] = 0.0;
+        for (int j = 0; j < kPPT; ++j) s.acc[acc_ix(tid * kPPT + j)] = 0.0;
         for (int i = 0; i < nact; ++i) {
           const uint32_t b = s.abase[i], c = s.acnt[i];
           const double qv = s.dqv[s.alist[i]];
@@ -622,7 +650,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
             for (int r = 0; r < 8; ++r) {
               const uint32_t local = pw[r].x - (uint32_t)cb;
               if (pw[r].x != 0xFFFFFFFFu && (local >> 4) == (uint32_t)tid)
-                mine[local & 15] += qv * (double)__uint_as_float(pw[r].y);
+                s.acc[acc_ix(local)] += qv * (double)__uint_as_float(pw[r].y);
             }
           }
         }
@@ -660,7 +688,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
             if (cur[r].x == 0xFFFFFFFFu) continue;
             HS_DCHECK(cur[r].x >= cb && cur[r].x < ce);
             // f64(q) * f64(w) is exact, so contraction cannot change the sum
-            s.acc[cur[r].x - cb] += qv * (double)__uint_as_float(cur[r].y);
+            s.acc[acc_ix(cur[r].x - (uint32_t)cb)] += qv * (double)__uint_as_float(cur[r].y);
           }
           // long slices: the rest in batches of 8 loads in flight per thread
           constexpr int kB = 8;
@@ -675,7 +703,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
             for (int r = 0; r < kB; ++r) {
               if (v[r].x == 0xFFFFFFFFu) continue;
               HS_DCHECK(v[r].x >= cb && v[r].x < ce);
-              s.acc[v[r].x - cb] += qv * (double)__uint_as_float(v[r].y);
+              s.acc[acc_ix(v[r].x - (uint32_t)cb)] += qv * (double)__uint_as_float(v[r].y);
             }
           }
           __syncthreads();
@@ -684,8 +712,10 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
     }
 
     // ---- scores (recomputed where needed instead of held in 16 f64 registers) ----
-    auto score = [&](int j) -> double {
-      const double acc = (SP && nact > 0) ? s.acc[tid * kPPT + j] : 0.0;
+    auto acc_of = [&](int j) -> double {
+      return (SP && nact > 0) ? s.acc[acc_ix(tid * kPPT + j)] : 0.0;
+    };
+    auto score_with = [&](int j, double acc) -> double {
       if (a.raw_dense) return __dadd_rn(btot, __dmul_rn(scl, (double)tot[j]));
       if (DM != 0) {
         const double dn = __dadd_rn(__dadd_rn(btot, __dmul_rn(scl, (double)tot[j])), off);
@@ -693,6 +723,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
       }
       return acc;
     };
+    auto score = [&](int j) -> double { return score_with(j, acc_of(j)); };
 
     if (a.mode == S1_DUMP) {
 #pragma unroll
@@ -733,12 +764,16 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
     unsigned mask = 0;
     {
       const int have = s.ctl[2];
+      const int tlim = s.ctl[3];
       const Cand th = *s.th;
 #pragma unroll
       for (int j = 0; j < kPPT; ++j) {
         const int64_t pt = p0 + j;
         if (pt >= ce) continue;
-        const double sj = score(j);
+        const double aj = acc_of(j);
+        // integer pre-filter: no sparse part and a LUT total below tlim
+        if (DM != 0 && aj == 0.0 && (int)tot[j] < tlim) continue;
+        const double sj = score_with(j, aj);
         bool pass = !have || sj > th.s;
         if (!pass && sj == th.s) pass = a.order[pt] < th.tie;
         if (pass) mask |= 1u << j;
@@ -773,7 +808,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
         const int nr = block_sum(__popc(m), s.ctl + 4);
         if (nr == 0) continue;
         if (cnt_r + nr > a.cap) {
-          compact(s, a.k);
+          compact(s, a.k, DM != 0, btot, scl, off);
           const Cand th = *s.th;
           unsigned m2 = 0;
 #pragma unroll
@@ -813,7 +848,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
     return;
   }
   if (a.mode != S1_SELECT) return;
-  compact(s, a.k);  // best k of the tile, unordered (the merge sorts)
+  compact(s, a.k, false, 0.0, 0.0, 0.0);  // best k of the tile, unordered (the merge sorts)
   Cand* o = a.out + (q * a.ntiles + tile) * a.out_per_tile;
   const int keep = s.ctl[0];
   for (int i = tid; i < a.out_per_tile; i += blockDim.x) o[i] = i < keep ? s.buf[i] : worst_cand();
@@ -905,6 +940,21 @@ __global__ void __launch_bounds__(kBucketThreads) k_sparse_bucket(
     for (uint32_t j = tid; j < L; j += blockDim.x) atomicAdd(&cnt[__ldg(&post[b + j].x) >> 12], 1u);
   }
   __syncthreads();
+  {
+    // a chunk with very many entries is summed in O(entries^2) by stage 1's
+    // first-of-point pass: stream such queries instead
+    uint32_t mx = 0;
+    for (int c = tid; c < nchunks; c += blockDim.x) mx = max(mx, cnt[c]);
+    for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((tid & 31) == 0) scr[tid >> 5] = (int)mx;
+    __syncthreads();
+    for (int w = 0; w < kBucketThreads / 32; ++w) mx = max(mx, (uint32_t)scr[w]);
+    __syncthreads();
+    if (mx > 1024u) {
+      if (tid == 0) mode[q] = 0;
+      return;
+    }
+  }
   // exclusive scan of the histogram (segment per thread, then across threads)
   const int per = (nchunks + kBucketThreads - 1) / kBucketThreads;
   const int c0 = min(nchunks, tid * per), c1 = min(nchunks, c0 + per);
@@ -1073,13 +1123,26 @@ Stage1Plan plan_stage1(const DeviceIndex& ix, int64_t nq, int64_t k, int max_qnn
   if (mode == S1_SELECT) {
     // enough tiles to fill the GPU, tiles much larger than k so the per-tile
     // keep filters; the merge then sorts ntiles*k entries per query
-    int64_t ntiles = ceil_div(target_ctas, nq > 0 ? nq : 1);
+    const int64_t nqq = nq > 0 ? nq : 1;
     const int64_t min_tile_chunks = ceil_div(8 * k, kChunk);
-    const int64_t max_tiles_by_k = nchunks / (min_tile_chunks > 0 ? min_tile_chunks : 1);
-    if (ntiles > max_tiles_by_k) ntiles = max_tiles_by_k;
-    if (ntiles * k > 65536) ntiles = 65536 / (k > 0 ? k : 1);
-    if (ntiles < 1) ntiles = 1;
-    if (ntiles > nchunks) ntiles = nchunks;
+    int64_t max_tiles = nchunks / (min_tile_chunks > 0 ? min_tile_chunks : 1);
+    if (max_tiles * k > 65536) max_tiles = 65536 / (k > 0 ? k : 1);
+    if (max_tiles > nchunks) max_tiles = nchunks;
+    if (max_tiles < 1) max_tiles = 1;
+    // tiles per query: minimise (waves of resident CTAs) x (chunks per tile +
+    // a per-tile selection overhead of ~2 chunks) — wave quantisation of
+    // nq*ntiles CTAs against per-tile fill/compaction work
+    int64_t ntiles = 1;
+    double best = 1e300;
+    const int64_t t_lo = std::min<int64_t>(max_tiles, ceil_div(target_ctas, nqq));
+    for (int64_t t = t_lo; t <= std::min<int64_t>(max_tiles, 4 * t_lo + 8); ++t) {
+      const double waves = (double)ceil_div(nqq * t, target_ctas);
+      const double cost = waves * ((double)ceil_div(nchunks, t) + 2.0);
+      if (cost < best * 0.999) {
+        best = cost;
+        ntiles = t;
+      }
+    }
     const int64_t chunks_per_tile = ceil_div(nchunks, ntiles);
     p.tile_pts = chunks_per_tile * kChunk;
     p.ntiles = (int)ceil_div(ix.n, p.tile_pts);
