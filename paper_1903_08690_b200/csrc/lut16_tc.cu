@@ -21,13 +21,16 @@
 // to u16 (K <= 257 keeps them < 2^16) row-major [query][point] for the fused
 // stage-1 kernel, which adds the sparse part and selects.
 //
-// Warp roles (288 threads, one CTA per SM — it owns all 512 TMEM columns):
-//   warps 0-3  producers: thread = point lane; per K chunk of 8 subspaces one
-//              coalesced u32 load (8 codes), 32 one-hot words, one
-//              tcgen05.st.32x32b.x32 into an A ring slot, arrive `afull`;
-//   warps 4-7  epilogue: tcgen05.ld the finished accumulator, store u16,
-//              arrive `dempty`;
-//   warp 8     TMEM allocation; lane 0 issues the MMAs (<= 4 per chunk,
+// Warp roles (416 threads, one CTA per SM — it owns all 512 TMEM columns):
+//   warps 0-7  producers: thread = point lane (two warps per TMEM lane
+//              quadrant, alternate K chunks); per chunk of 8 subspaces one
+//              coalesced u32 load (8 codes, one block ahead), 32 one-hot
+//              words, one tcgen05.st.32x32b.x32 into an A ring slot, arrive
+//              `afull`;
+//   warps 8-11 epilogue: tcgen05.ld the finished accumulator, transpose
+//              through shared memory, TMA tensor store of u16 tiles, arrive
+//              `dempty`;
+//   warp 12    TMEM allocation; lane 0 issues the MMAs (<= 4 per chunk,
 //              K = 32 B = 2 subspaces each) and the tcgen05.commit arrivals.
 //
 // Shared-memory B layout (SWIZZLE_NONE, K-major canonical): 16-byte column
@@ -48,8 +51,8 @@ namespace {
 
 constexpr int kPM = 128;       // points per block (MMA M, TMEM lanes)
 constexpr int kKC = 8;         // subspaces per K chunk (4 MMAs, 32 TMEM columns of A)
-constexpr int kProd = 128;     // producer threads (warps 0-3)
-constexpr int kThreadsTc = 288;
+constexpr int kProd = 128;     // arrivals per A chunk (one producer warp per lane quadrant)
+constexpr int kThreadsTc = 416;  // 8 producer, 4 epilogue, 1 MMA warps
 constexpr int kTmemCols = 512;
 constexpr int kMaxNQ = 224;    // 2*NQ accumulator + >= 2 A slots of 32 columns <= 512
 constexpr size_t kStageBytes = 4 * 2 * 32 * 32 * 2;  // epilogue staging: 4 warps x 2 x 32x32 u16
@@ -74,6 +77,14 @@ __device__ __forceinline__ uint32_t idesc_u8(int n) {
   return (2u << 4)                 // c_format = S32
          | (0u << 7) | (0u << 10)  // a/b format = unsigned 8-bit
          | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(kPM >> 4) << 24);
+}
+
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.b32 %0, 1, 0, P;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
 }
 
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
@@ -175,6 +186,7 @@ __device__ __forceinline__ void onehot8(uint32_t w, int valid, uint32_t* r) {
   }
 }
 
+template <int MAXC>  // >= K chunks of 8 subspaces
 __global__ void __launch_bounds__(kThreadsTc, 1)
     k_lut16_tc(TcArgs a, const __grid_constant__ CUtensorMap tmap) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -194,7 +206,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
   if (it0 >= it1) return;
   const int nkc = (a.Kp + kKC - 1) / kKC;
 
-  if (warp == 8) {
+  if (warp == 12) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(tmem_slot)),
                  "r"(kTmemCols));
@@ -248,33 +260,55 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     }
     __syncthreads();
 
-    if (warp < 4) {
+    if (warp < 8) {
       // ---- producers: one-hot A chunks into the TMEM ring ----
-      const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+      // Two warps per TMEM lane quadrant take alternate K chunks, so one
+      // warp's tcgen05.st / barrier latency overlaps the other's generation.
+      const int quad = warp & 3, par = warp >> 2;
+      const uint32_t lane_base = (uint32_t)(quad * 32) << 16;
+      constexpr int HC = (MAXC + 1) / 2;
+      // this warp's code words of a block, loaded one block ahead so the
+      // global-load latency hides behind a whole block of MMAs
+      uint32_t nxt[HC];
+      auto load_block = [&](int64_t bi) {
+        const int64_t p = (b0 + bi) * kPM + quad * 32 + lane;
+        const bool live = bi < nblk && p < a.n;
+#pragma unroll
+        for (int j = 0; j < HC; ++j) {
+          const int c = 2 * j + par;
+          nxt[j] = (live && c < nkc) ? __ldg(a.hcodes + (int64_t)c * a.n + p) : 0u;
+        }
+      };
+      load_block(0);
       for (int64_t bi = 0; bi < nblk; ++bi) {
-        const int64_t p = (b0 + bi) * kPM + tid;
+        const int64_t p = (b0 + bi) * kPM + quad * 32 + lane;
         const bool live = p < a.n;
-        uint32_t wnext = live ? __ldg(a.hcodes + p) : 0u;
-        for (int c = 0; c < nkc; ++c) {
-          const uint32_t w = wnext;
-          if (c + 1 < nkc) wnext = live ? __ldg(a.hcodes + (int64_t)(c + 1) * a.n + p) : 0u;
-          uint32_t r[32];
-          onehot8(w, live ? min(kKC, a.K - c * kKC) : 0, r);
-          if (round > 0) {
-            mbar_wait(&aempty[slot], (round - 1) & 1u);
-            asm volatile("tcgen05.fence::after_thread_sync;");
+        uint32_t cur[HC];
+#pragma unroll
+        for (int j = 0; j < HC; ++j) cur[j] = nxt[j];
+        load_block(bi + 1);
+#pragma unroll
+        for (int c = 0; c < MAXC; ++c) {
+          if (c >= nkc) break;
+          if ((c & 1) == par) {
+            uint32_t r[32];
+            onehot8(cur[c >> 1], live ? min(kKC, a.K - c * kKC) : 0, r);
+            if (round > 0) {
+              mbar_wait(&aempty[slot], (round - 1) & 1u);
+              asm volatile("tcgen05.fence::after_thread_sync;");
+            }
+            TMEM_ST32(tmem_a + lane_base + (uint32_t)(slot * 32), r);
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            asm volatile("tcgen05.fence::before_thread_sync;");
+            mbar_arrive(&afull[slot]);
           }
-          TMEM_ST32(tmem_a + lane_base + (uint32_t)(slot * 32), r);
-          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-          asm volatile("tcgen05.fence::before_thread_sync;");
-          mbar_arrive(&afull[slot]);
           if (++slot == a.slots) {
             slot = 0;
             ++round;
           }
         }
       }
-    } else if (warp < 8) {
+    } else if (warp < 12) {
       // ---- epilogue: accumulator -> u16 totals [query][point] ----
       // Per 32x32 tile (32 points of this warp's lanes x 32 queries): the
       // tile is transposed through shared memory (conflict-free u16 stores,
@@ -312,10 +346,11 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
           ++ep_tile;
         }
       }
-    } else if (lane == 0) {
-      // ---- MMA issuer ----
+    } else {
+      // ---- MMA issuer: warp-uniform control flow (descriptors stay in
+      // uniform registers), one elected lane issues the MMAs and commits ----
       const uint32_t idesc = idesc_u8(NQ);
-      const uint32_t b_addr = smem_u32(sB);
+      const uint64_t bdesc0 = smem_desc(smem_u32(sB), (uint32_t)(NQ * 16), 128);
       for (int64_t bi = 0; bi < nblk; ++bi) {
         const int64_t bt = blk_it + bi;
         const int buf = (int)(bt & 1);
@@ -327,29 +362,34 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
         for (int c = 0; c < nkc; ++c) {
           mbar_wait(&afull[slot], round & 1u);
           asm volatile("tcgen05.fence::after_thread_sync;");
-          const int kc = min(kKC, a.Kp - c * kKC);  // even
-          for (int m = 0; m < kc / 2; ++m) {
-            const int k0 = c * kKC + 2 * m;
-            const uint64_t bd =
-                smem_desc(b_addr + (uint32_t)(k0 * NQ * 16), (uint32_t)(NQ * 16), 128);
-            mma_ts(d, tmem_a + (uint32_t)(slot * 32 + m * 8), bd, idesc,
-                   (c > 0 || m > 0) ? 1u : 0u);
+          const int npair = min(kKC, a.Kp - c * kKC) / 2;  // Kp even
+          const uint32_t ta = tmem_a + (uint32_t)(slot * 32);
+          // B start address advances by NQ*16 bytes per subspace: +NQ in the
+          // descriptor's (address >> 4) field
+          const uint64_t bd = bdesc0 + (uint64_t)(c * kKC * NQ);
+          if (elect_one()) {
+            mma_ts(d, ta, bd, idesc, c > 0 ? 1u : 0u);
+            if (npair > 1) mma_ts(d, ta + 8, bd + (uint64_t)(2 * NQ), idesc, 1u);
+            if (npair > 2) mma_ts(d, ta + 16, bd + (uint64_t)(4 * NQ), idesc, 1u);
+            if (npair > 3) mma_ts(d, ta + 24, bd + (uint64_t)(6 * NQ), idesc, 1u);
+            mma_commit(&aempty[slot]);
           }
-          mma_commit(&aempty[slot]);
+          __syncwarp();
           if (++slot == a.slots) {
             slot = 0;
             ++round;
           }
         }
-        mma_commit(&dfull[buf]);
+        if (elect_one()) mma_commit(&dfull[buf]);
+        __syncwarp();
       }
     }
     blk_it += nblk;
     seg += nblk;
   }
-  if (warp >= 4 && warp < 8 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  if (warp >= 8 && warp < 12 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   __syncthreads();
-  if (warp == 8) {
+  if (warp == 12) {
     asm volatile("tcgen05.fence::after_thread_sync;");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
                  "r"(kTmemCols));
@@ -438,7 +478,10 @@ int launch_lut16_tc(const DeviceIndex& ix, const uint8_t* luts, int64_t nq, uint
   if (ld % kPM != 0) HS_FAIL(HS_EINVAL, "tensor-core totals stride must be a multiple of 128");
   const size_t smem =
       (size_t)a.Kp * NQ * 16 + kStageBytes + (2 * a.slots + 4) * sizeof(uint64_t) + 16;
-  HS_CUDA(cudaFuncSetAttribute(k_lut16_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int nkc = (int)ceil_div(a.Kp, kKC);
+  void (*kern)(TcArgs, const CUtensorMap) =
+      nkc <= 8 ? k_lut16_tc<8> : nkc <= 16 ? k_lut16_tc<16> : k_lut16_tc<33>;
+  HS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   // totals [nq][ld] u16 as a 2-D tensor; 32x32 boxes, no swizzle
   CUtensorMap tmap;
   auto enc = encode_fn();
@@ -451,7 +494,7 @@ int launch_lut16_tc(const DeviceIndex& ix, const uint8_t* luts, int64_t nq, uint
           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
           CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     HS_FAIL(HS_ECUDA, "cuTensorMapEncodeTiled failed for the totals buffer");
-  k_lut16_tc<<<(unsigned)grid, kThreadsTc, smem, st>>>(a, tmap);
+  kern<<<(unsigned)grid, kThreadsTc, smem, st>>>(a, tmap);
   HS_CUDA(cudaGetLastError());
   return HS_OK;
 }

@@ -229,9 +229,18 @@ __device__ int dense_tlim(double ths, double btot, double scl, double off) {
   return lo;
 }
 
-__device__ void compact(Smem& s, int k, bool dense, double btot, double scl, double off) {
+// Offers are appended with the tie id unset (the original-id lookup is a
+// dependent global load that would stall the whole block at the offer
+// barrier); compaction resolves them in one parallel pass first.
+constexpr uint32_t kTieUnset = 0xFFFFFFFFu;
+
+__device__ void compact(Smem& s, int k, bool dense, double btot, double scl, double off,
+                        const uint32_t* __restrict__ order) {
   const int cnt = s.ctl[0];
   __syncthreads();  // every thread has read ctl[0]
+  for (int i = threadIdx.x; i < cnt; i += blockDim.x)
+    if (s.buf[i].tie == kTieUnset) s.buf[i].tie = __ldg(order + s.buf[i].slot);
+  __syncthreads();
   if (cnt <= k) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   unsigned* hist = reinterpret_cast<unsigned*>(s.bval);
@@ -446,11 +455,21 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
   }
   const uint2* vc = reinterpret_cast<const uint2*>(a.vcodes);
   const int64_t vrow = a.vstride >> 1;  // uint2 per subspace row
-  uint4 tnext0 = make_uint4(0u, 0u, 0u, 0u), tnext1 = tnext0;
-  if (DM == 2 && tile_lo + (int64_t)tid * kPPT < tile_hi) {
-    const uint4* src = reinterpret_cast<const uint4*>(a.tot16 + q * a.tot_ld + tile_lo + tid * kPPT);
-    tnext0 = __ldg(src);
-    tnext1 = __ldg(src + 1);
+  // u16 totals are prefetched two chunks ahead (tnext: next chunk, tnext2:
+  // the one after)
+  uint4 tnext0 = make_uint4(0u, 0u, 0u, 0u), tnext1 = tnext0, tnext20 = tnext0, tnext21 = tnext0;
+  if (DM == 2) {
+    const int64_t pa = tile_lo + (int64_t)tid * kPPT;
+    if (pa < tile_hi) {
+      const uint4* src = reinterpret_cast<const uint4*>(a.tot16 + q * a.tot_ld + pa);
+      tnext0 = __ldg(src);
+      tnext1 = __ldg(src + 1);
+    }
+    if (pa + kChunk < tile_hi) {
+      const uint4* src = reinterpret_cast<const uint4*>(a.tot16 + q * a.tot_ld + pa + kChunk);
+      tnext20 = __ldg(src);
+      tnext21 = __ldg(src + 1);
+    }
   }
   __syncthreads();
 
@@ -464,12 +483,14 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
 #pragma unroll
     for (int j = 0; j < kPPT; ++j) tot[j] = 0;
     if (DM == 2 && p0 < ce) {
-      // totals of this chunk were prefetched during the previous chunk
+      // totals of this chunk were prefetched two chunks ago
       const uint4 t0 = tnext0, t1 = tnext1;
-      if (p0 + kChunk < tile_hi) {
-        const uint4* nsrc = reinterpret_cast<const uint4*>(a.tot16 + q * a.tot_ld + p0 + kChunk);
-        tnext0 = __ldg(nsrc);
-        tnext1 = __ldg(nsrc + 1);
+      tnext0 = tnext20;
+      tnext1 = tnext21;
+      if (p0 + 2 * kChunk < tile_hi) {
+        const uint4* nsrc = reinterpret_cast<const uint4*>(a.tot16 + q * a.tot_ld + p0 + 2 * kChunk);
+        tnext20 = __ldg(nsrc);
+        tnext21 = __ldg(nsrc + 1);
       }
       const uint32_t w8[8] = {t0.x, t0.y, t0.z, t0.w, t1.x, t1.y, t1.z, t1.w};
 #pragma unroll
@@ -779,6 +800,9 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
         if (pass) mask |= 1u << j;
       }
     }
+    // nothing passes anywhere in the block (the steady state once the
+    // threshold has settled): one barrier, no counting
+    if (!__syncthreads_or(mask != 0u)) continue;
     // snapshot the count before block_sum's barriers: threads that pass the
     // room check start appending (atomicAdd on ctl[0]) right after it
     const int cnt0 = s.ctl[0];
@@ -794,7 +818,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
           Cand c;
           c.s = score(j);
           c.slot = (uint32_t)(p0 + j);
-          c.tie = a.order[p0 + j];
+          c.tie = kTieUnset;
           s.buf[pos++] = c;
         }
       }
@@ -808,7 +832,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
         const int nr = block_sum(__popc(m), s.ctl + 4);
         if (nr == 0) continue;
         if (cnt_r + nr > a.cap) {
-          compact(s, a.k, DM != 0, btot, scl, off);
+          compact(s, a.k, DM != 0, btot, scl, off, a.order);
           const Cand th = *s.th;
           unsigned m2 = 0;
 #pragma unroll
@@ -832,7 +856,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
             Cand c;
             c.s = score(jj);
             c.slot = (uint32_t)(p0 + jj);
-            c.tie = a.order[p0 + jj];
+            c.tie = kTieUnset;
             s.buf[pos++] = c;
           }
         }
@@ -848,7 +872,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
     return;
   }
   if (a.mode != S1_SELECT) return;
-  compact(s, a.k, false, 0.0, 0.0, 0.0);  // best k of the tile, unordered (the merge sorts)
+  compact(s, a.k, false, 0.0, 0.0, 0.0, a.order);  // best k of the tile, unordered (the merge sorts)
   Cand* o = a.out + (q * a.ntiles + tile) * a.out_per_tile;
   const int keep = s.ctl[0];
   for (int i = tid; i < a.out_per_tile; i += blockDim.x) o[i] = i < keep ? s.buf[i] : worst_cand();

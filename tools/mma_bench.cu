@@ -48,11 +48,14 @@ __global__ void k_bench(int iters, long long* out) {
     uint32_t r[32];
     for (int j = 0; j < 32; ++j) r[j] = j * tid;
     const uint32_t lb = (uint32_t)(((warp & 3) * 32) << 16);
+    long long cnt = 0;
     while (!done) {
+      ++cnt;
       asm volatile("tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(tmem + lb + 448),
         "r"(r[0]),"r"(r[1]),"r"(r[2]),"r"(r[3]),"r"(r[4]),"r"(r[5]),"r"(r[6]),"r"(r[7]),"r"(r[8]),"r"(r[9]),"r"(r[10]),"r"(r[11]),"r"(r[12]),"r"(r[13]),"r"(r[14]),"r"(r[15]),"r"(r[16]),"r"(r[17]),"r"(r[18]),"r"(r[19]),"r"(r[20]),"r"(r[21]),"r"(r[22]),"r"(r[23]),"r"(r[24]),"r"(r[25]),"r"(r[26]),"r"(r[27]),"r"(r[28]),"r"(r[29]),"r"(r[30]),"r"(r[31]) : "memory");
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
     }
+    if ((tid & 31) == 0 && blockIdx.x == 0) out[150 + warp] = cnt;
   }
   if (warp >= 5 && warp <= 8 && (MODE == 3 || MODE == 4)) {
     uint32_t acc = 0;
@@ -120,21 +123,22 @@ __global__ void k_bench(int iters, long long* out) {
 template <int KIND, bool TS, int LAYOUT, int N, int MODE = 0>
 void run(const char* name) {
   long long* d;
-  cudaMalloc(&d, sizeof(long long) * 149);
+  cudaMalloc(&d, sizeof(long long) * 160);
+  cudaMemset(d, 0, sizeof(long long) * 160);
   auto k = k_bench<KIND, TS, LAYOUT, N, MODE>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
   const int iters = 4096;
   k<<<148, 288, 100 * 1024>>>(iters, d);
   k<<<148, 288, 100 * 1024>>>(iters, d);
   cudaError_t e = cudaDeviceSynchronize();
-  long long h[148];
+  long long h[160];
   cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
   double avg = 0;
   for (int i = 0; i < 148; ++i) avg += h[i];
   avg /= 148;
   const double floor = 128.0 * N / 256.0;
-  printf("mode %d %-30s N=%3d  %7.1f cyc/MMA  (floor %5.1f)  %s\n", MODE, name, N, avg / iters, floor,
-         e == cudaSuccess ? "" : cudaGetErrorString(e));
+  printf("mode %d %-30s N=%3d  %7.1f cyc/MMA  (floor %5.1f)  sttm/warp %lld -> %.1f cyc/STTM.x32 %s\n", MODE, name, N, avg / iters, floor,
+         h[151], h[151] ? (double)h[0] / h[151] : 0.0, e == cudaSuccess ? "" : cudaGetErrorString(e));
   cudaFree(d);
 }
 
