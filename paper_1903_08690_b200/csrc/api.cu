@@ -61,7 +61,7 @@ void free_device_arrays(DeviceIndex* ix) {
                   ix->centers,  ix->vcodes,     ix->sq_lo,    ix->sq_step,    ix->sq_codes,
                   ix->wh_mean,  ix->wh_inv_t,   ix->ds_dense, ix->ds_indptr,  ix->ds_indices,
                   ix->ds_data,  ix->scratch,    ix->skip_row, ix->skip,     ix->io_dev,
-                  ix->hcodes};
+                  ix->hcodes,   ix->pcodes};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (ix->io_host) cudaFreeHost(ix->io_host);
@@ -150,7 +150,8 @@ struct Timer {
         ix->tms[it - ix->tnames.begin()] += ms;
       }
       if (nm == "map_dims" || nm == "lut_build" || nm == "sparse_bucket" || nm == "lut16_tc" ||
-          nm == "stage1" || nm == "merge")
+          nm == "stage1" || nm == "merge" || nm == "sample" || nm == "fuse" || nm == "fuse_select" ||
+          nm == "fallback")
         st3[0] += ms;
       else if (nm == "stage2") st3[1] += ms;
       else if (nm == "stage3") st3[2] += ms;
@@ -178,15 +179,47 @@ int run_search(DeviceIndex& ix, const hs_query_batch& qb, int64_t nnz, int max_q
     HS_FAIL(HS_EUNSUPPORTED, "overfetch*h above 8192 candidates is not supported");
   if (max_qnnz > 8192) HS_FAIL(HS_EUNSUPPORTED, "queries with more than 8192 sparse nonzeros");
 
-  // tensor-core LUT16 totals for large batches (>= kTcMinQueries queries)
+  // tensor-core LUT16 for large batches (>= kTcMinQueries queries): either
+  // threshold-filtered (fuse.cu: sample -> threshold -> filtered tensor-core
+  // pass -> candidate scoring) or, when that does not apply, u16 totals for
+  // every point followed by the full stage-1 scan
+  const int64_t d = ix.d_dense;
   const int64_t tc_ld = lut16_tc_ld(ix.n);
-  const bool use_tc = ix.d_dense > 0 && lut16_tc_supported(ix) && nq >= kTcMinQueries &&
+  const bool use_tc = d > 0 && lut16_tc_supported(ix) && nq >= kTcMinQueries &&
                       !getenv_flag("HSB200_NO_TC");
+  const bool use_buckets = nnz > 0 && ix.nnz_post > 0 && !getenv_flag("HSB200_NO_BUCKETS");
+  const bool sparse_part = nnz > 0 && ix.nnz_post > 0;
+  // sample size of the threshold pass and capacity of the filtered lists
+  // (HSB200_FUSE_SAMPLE / HSB200_FUSE_CAP: test knobs that shrink the sample
+  // and the list capacity so small indices exercise the filter and fallback)
+  const char* ev_s = std::getenv("HSB200_FUSE_SAMPLE");
+  const char* ev_c = std::getenv("HSB200_FUSE_CAP");
+  const int64_t m_min = ev_s ? std::max<int64_t>(128, std::atoll(ev_s)) : 65536;
+  // sample ~ k1*n/6000 points (=> ~6000 expected dense candidates per query)
+  const int64_t m_auto = std::max<int64_t>(
+      65536, (int64_t)((double)sz.k1 * (double)ix.n / 6000.0));
+  // (a whole number of stage-1 chunks, so the sample ends on a chunk boundary)
+  const int64_t cpts = stage1_chunk_points();
+  const int64_t m_s = std::min<int64_t>(
+      ix.n, ceil_div(std::max<int64_t>(ev_s ? m_min : m_auto, 4 * sz.k1), cpts) * cpts);
+  const bool use_fuse = use_tc && ix.K <= 256 && sz.k1 <= 4096 && ix.n >= 8 * m_s &&
+                        (!sparse_part || (use_buckets && ix.pcodes != nullptr)) &&
+                        !getenv_flag("HSB200_NO_FUSE");
+  const int64_t expect = (int64_t)((double)sz.k1 * (double)ix.n / (double)m_s);
+  int64_t Cf = use_fuse ? std::min<int64_t>(ix.n, ((std::max<int64_t>(16384, 4 * expect) + 1023) / 1024) * 1024) : 0;
+  if (use_fuse && ev_c) Cf = std::max<int64_t>(1, std::atoll(ev_c));
+  const int64_t capq_all = use_buckets ? bucket_capacity(ix) : 0;
+  const int64_t Mf = Cf + capq_all;
+  const int64_t ld_s = lut16_tc_ld(m_s);
+  const int64_t words = ceil_div(ix.n, 32);
   // query-chunk size bounded by scratch for the stage-1 per-tile outputs
   int64_t QB = std::min<int64_t>(nq, 2048);
-  if (use_tc) {  // u16 totals [QB][tc_ld]: under ~8 GB, whole tensor-core groups
+  if (use_tc) {
     const int64_t grp = lut16_tc_group(ix);
-    const int64_t cap = std::max<int64_t>(grp, (int64_t)(8.0e9 / (2.0 * tc_ld)) / grp * grp);
+    const double per_q = use_fuse
+        ? (double)Cf * 8 + (double)Mf * 16 + (double)ld_s * 2 + (sparse_part ? words * 4.0 : 0.0)
+        : 2.0 * (double)tc_ld;  // u16 totals [QB][tc_ld]
+    const int64_t cap = std::max<int64_t>(grp, (int64_t)(8.0e9 / per_q) / grp * grp);
     if (QB > cap) QB = cap;
   }
   int64_t s1_entries = 0;
@@ -198,66 +231,104 @@ int run_search(DeviceIndex& ix, const hs_query_batch& qb, int64_t nnz, int max_q
       const Stage1Plan p1 = plan_stage1(ix, last, sz.k1, max_qnnz, S1_SELECT);
       s1_entries = std::max<int64_t>(s1_entries, last * p1.ntiles * p1.out_per_tile);
     }
+    if (use_fuse) {
+      const Stage1Plan ps = plan_stage1(ix, QB, sz.k1, max_qnnz, S1_SELECT, m_s);
+      s1_entries = std::max<int64_t>(s1_entries, QB * ps.ntiles * ps.out_per_tile);
+      if (last) {
+        const Stage1Plan ps1 = plan_stage1(ix, last, sz.k1, max_qnnz, S1_SELECT, m_s);
+        s1_entries = std::max<int64_t>(s1_entries, last * ps1.ntiles * ps1.out_per_tile);
+      }
+    }
     if ((double)s1_entries * sizeof(Cand) <= 1.0e9 || QB == 1) break;
     QB = (QB + 1) / 2;
   }
-  const int64_t d = ix.d_dense;
   const int Kp16 = ix.Kp * 16;
   const int64_t nchunks = ceil_div(ix.n, stage1_chunk_points());
   const int64_t capq = bucket_capacity(ix);
-  const bool use_buckets = nnz > 0 && ix.nnz_post > 0 && !getenv_flag("HSB200_NO_BUCKETS");
   size_t need = 0;
+  auto carve = [&](auto& a) {
+    struct Ptrs {
+      uint32_t *lbeg, *lend;
+      double* qv;
+      int32_t* lidx;
+      double *qd, *qw;
+      uint8_t* luts;
+      double *btot, *scl, *off;
+      int* bad;
+      Cand *s1out, *cand1, *cand2;
+      SparseBuckets sb;
+      uint16_t* tot16;
+      // fused path
+      uint16_t* tot_s;
+      Cand* cand_s;
+      uint32_t* tlim;
+      uint2* list;
+      uint32_t* lcnt;
+      Cand* fout;
+      uint32_t* fcnt;
+      int* fallback;
+      uint32_t* bitmap;
+    } p{};
+    p.lbeg = a.template take<uint32_t>(nnz + 1);
+    p.lend = a.template take<uint32_t>(nnz + 1);
+    p.qv = a.template take<double>(nnz + 1);
+    p.lidx = a.template take<int32_t>(nnz + 1);
+    p.qd = a.template take<double>(QB * d + 1);
+    p.qw = a.template take<double>(QB * d + 1);
+    p.luts = a.template take<uint8_t>(QB * Kp16 + 16);
+    p.btot = a.template take<double>(QB);
+    p.scl = a.template take<double>(QB);
+    p.off = a.template take<double>(QB);
+    p.bad = a.template take<int>(QB);
+    p.s1out = a.template take<Cand>((size_t)s1_entries + 1);
+    p.cand1 = a.template take<Cand>(QB * sz.k1 + 1);
+    p.cand2 = a.template take<Cand>(QB * sz.k2 + 1);
+    if (use_buckets) {
+      p.sb.mode = a.template take<int>(QB);
+      p.sb.boff = a.template take<uint32_t>(QB * (nchunks + 1));
+      p.sb.slots = a.template take<uint32_t>(QB * capq);
+      p.sb.vals = a.template take<double>(QB * capq);
+      p.sb.capq = capq;
+      p.sb.nchunks = (int)nchunks;
+    }
+    if (use_tc && !use_fuse) p.tot16 = a.template take<uint16_t>(QB * tc_ld);
+    if (use_fuse) {
+      p.tot_s = a.template take<uint16_t>(QB * ld_s);
+      p.cand_s = a.template take<Cand>(QB * sz.k1 + 1);
+      p.tlim = a.template take<uint32_t>(QB);
+      p.list = a.template take<uint2>(QB * Cf);
+      p.lcnt = a.template take<uint32_t>(QB);
+      p.fout = a.template take<Cand>(QB * Mf);
+      p.fcnt = a.template take<uint32_t>(QB);
+      p.fallback = a.template take<int>(QB);
+      if (sparse_part) p.bitmap = a.template take<uint32_t>(QB * words);
+    }
+    return p;
+  };
   {
     Arena a{nullptr};
-    a.take<uint32_t>(nnz + 1);
-    a.take<uint32_t>(nnz + 1);
-    a.take<double>(nnz + 1);
-    a.take<int32_t>(nnz + 1);
-    a.take<double>(QB * d + 1);
-    a.take<double>(QB * d + 1);
-    a.take<uint8_t>(QB * Kp16 + 16);
-    a.take<double>(QB);
-    a.take<double>(QB);
-    a.take<double>(QB);
-    a.take<int>(QB);
-    a.take<Cand>((size_t)s1_entries + 1);
-    a.take<Cand>(QB * sz.k1 + 1);
-    a.take<Cand>(QB * sz.k2 + 1);
-    if (use_buckets) {
-      a.take<int>(QB);
-      a.take<uint32_t>(QB * (nchunks + 1));
-      a.take<uint32_t>(QB * capq);
-      a.take<double>(QB * capq);
-    }
-    if (use_tc) a.take<uint16_t>(QB * tc_ld);
+    carve(a);
     need = a.off + 1024;
   }
   HS_CHECK(ensure_scratch(ix, need));
-  Arena a{static_cast<char*>(ix.scratch)};
-  uint32_t* lbeg = a.take<uint32_t>(nnz + 1);
-  uint32_t* lend = a.take<uint32_t>(nnz + 1);
-  double* qv = a.take<double>(nnz + 1);
-  int32_t* lidx = a.take<int32_t>(nnz + 1);
-  double* qd = a.take<double>(QB * d + 1);
-  double* qw = a.take<double>(QB * d + 1);
-  uint8_t* luts = a.take<uint8_t>(QB * Kp16 + 16);
-  double* btot = a.take<double>(QB);
-  double* scl = a.take<double>(QB);
-  double* off = a.take<double>(QB);
-  int* bad = a.take<int>(QB);
-  Cand* s1out = a.take<Cand>((size_t)s1_entries + 1);
-  Cand* cand1 = a.take<Cand>(QB * sz.k1 + 1);
-  Cand* cand2 = a.take<Cand>(QB * sz.k2 + 1);
-  SparseBuckets sb;
-  if (use_buckets) {
-    sb.mode = a.take<int>(QB);
-    sb.boff = a.take<uint32_t>(QB * (nchunks + 1));
-    sb.slots = a.take<uint32_t>(QB * capq);
-    sb.vals = a.take<double>(QB * capq);
-    sb.capq = capq;
-    sb.nchunks = (int)nchunks;
-  }
-  uint16_t* tot16 = use_tc ? a.take<uint16_t>(QB * tc_ld) : nullptr;
+  Arena arena{static_cast<char*>(ix.scratch)};
+  auto P = carve(arena);
+  uint32_t* lbeg = P.lbeg;
+  uint32_t* lend = P.lend;
+  double* qv = P.qv;
+  int32_t* lidx = P.lidx;
+  double* qd = P.qd;
+  double* qw = P.qw;
+  uint8_t* luts = P.luts;
+  double* btot = P.btot;
+  double* scl = P.scl;
+  double* off = P.off;
+  int* bad = P.bad;
+  Cand* s1out = P.s1out;
+  Cand* cand1 = P.cand1;
+  Cand* cand2 = P.cand2;
+  SparseBuckets sb = P.sb;
+  uint16_t* tot16 = P.tot16;
 
   if (tm) tm->mark("begin");
   QueryView all;
@@ -270,6 +341,8 @@ int run_search(DeviceIndex& ix, const hs_query_batch& qb, int64_t nnz, int max_q
   ix.launches += nnz > 0 ? 1 : 0;
   if (tm) tm->mark("map_dims");
   if (d > 0) HS_CUDA(cudaMemsetAsync(bad, 0, sizeof(int) * QB, st));
+  if (use_fuse && sparse_part)
+    HS_CUDA(cudaMemsetAsync(P.bitmap, 0, sizeof(uint32_t) * QB * words, st));
 
   for (int64_t q0 = 0; q0 < nq; q0 += QB) {
     const int64_t nqc = std::min(QB, nq - q0);
@@ -284,9 +357,8 @@ int run_search(DeviceIndex& ix, const hs_query_batch& qb, int64_t nnz, int max_q
     if (d > 0) {
       launch_lut_build(ix, qc.dense, nqc, qd, qw, luts, btot, scl, off, bad, st);
       HS_CUDA(cudaGetLastError());
+      ix.launches += 1;
       if (tm) tm->mark("lut_build");
-    } else if (params->exact_final_rerank) {
-      // no dense part: qd unused
     }
     if (use_buckets) {
       launch_sparse_bucket(ix, qc, lbeg, lend, qv, sb, st);
@@ -295,18 +367,56 @@ int run_search(DeviceIndex& ix, const hs_query_batch& qb, int64_t nnz, int max_q
       if (tm) tm->mark("sparse_bucket");
     }
     const bool tc_chunk = use_tc && nqc >= kTcMinQueries;
-    if (tc_chunk) {
-      HS_CHECK(launch_lut16_tc(ix, luts, nqc, tot16, tc_ld, st));
+    if (tc_chunk && use_fuse) {
+      // 1. exact top-k1 of the first m_s points -> threshold
+      HS_CHECK(launch_lut16_tc(ix, luts, nqc, P.tot_s, ld_s, st, m_s));
+      Stage1Plan ps = plan_stage1(ix, nqc, sz.k1, max_qnnz, S1_SELECT, m_s);
+      ps.sparse = nnz > 0;
+      HS_CHECK(launch_stage1(ix, qc, ps, lbeg, lend, qv, lidx, luts, btot, scl, off, s1out,
+                             nullptr, st, nullptr, false, use_buckets ? &sb : nullptr, P.tot_s,
+                             ld_s));
+      HS_CHECK(launch_select_topk(s1out, nqc, (int64_t)ps.ntiles * ps.out_per_tile, sz.k1,
+                                  P.cand_s, st));
+      launch_tlim(P.cand_s, nqc, (int)sz.k1, btot, scl, off, P.tlim, st);
+      ix.launches += 4;
+      if (tm) tm->mark("sample");
+      // 2. filtered tensor-core pass over every point
+      HS_CHECK(launch_lut16_filter(ix, luts, nqc, P.tlim, P.list, P.lcnt, Cf, st));
       ix.launches += 1;
       if (tm) tm->mark("lut16_tc");
+      // 3. candidate scoring (+ touched points) and exact top-k1
+      HS_CHECK(launch_fuse_cands(ix, nqc, luts, btot, scl, off, P.list, P.lcnt, Cf,
+                                 sparse_part ? &sb : nullptr, P.bitmap, P.fout, Mf, P.fcnt,
+                                 P.fallback, P.cand_s, (int)sz.k1, st));
+      if (tm) tm->mark("fuse");
+      HS_CHECK(launch_select_topk(P.fout, nqc, Mf, sz.k1, cand1, st, P.fcnt));
+      ix.launches += 2;
+      if (tm) tm->mark("fuse_select");
+      // 4. flagged queries (overflow / streamed postings): unfiltered stage 1
+      Stage1Plan pf = pc;
+      pf.qmask = P.fallback;
+      HS_CHECK(launch_stage1(ix, qc, pf, lbeg, lend, qv, lidx, luts, btot, scl, off, s1out,
+                             nullptr, st, nullptr, false, use_buckets ? &sb : nullptr));
+      HS_CHECK(launch_select_topk(s1out, nqc, (int64_t)pf.ntiles * pf.out_per_tile, sz.k1,
+                                  cand1, st, nullptr, P.fallback));
+      ix.launches += 2;
+      if (tm) tm->mark("fallback");
+    } else {
+      if (tc_chunk) {
+        HS_CHECK(launch_lut16_tc(ix, luts, nqc, tot16, tc_ld, st));
+        ix.launches += 1;
+        if (tm) tm->mark("lut16_tc");
+      }
+      ix.launches += 2;  // stage1, merge
+      HS_CHECK(launch_stage1(ix, qc, pc, lbeg, lend, qv, lidx, luts, btot, scl, off, s1out,
+                             nullptr, st, nullptr, false, use_buckets ? &sb : nullptr,
+                             tc_chunk ? tot16 : nullptr, tc_ld));
+      if (tm) tm->mark("stage1");
+      HS_CHECK(launch_select_topk(s1out, nqc, (int64_t)pc.ntiles * pc.out_per_tile, sz.k1,
+                                  cand1, st));
+      if (tm) tm->mark("merge");
     }
-    ix.launches += (d > 0 ? 1 : 0) + 4;  // lut_build, stage1, merge, stage2, stage3
-    HS_CHECK(launch_stage1(ix, qc, pc, lbeg, lend, qv, lidx, luts, btot, scl, off, s1out, nullptr, st,
-                           nullptr, false, use_buckets ? &sb : nullptr,
-                           tc_chunk ? tot16 : nullptr, tc_ld));
-    if (tm) tm->mark("stage1");
-    HS_CHECK(launch_select_topk(s1out, nqc, (int64_t)pc.ntiles * pc.out_per_tile, sz.k1, cand1, st));
-    if (tm) tm->mark("merge");
+    ix.launches += 2;  // stage2, stage3
     launch_stage2(ix, cand1, nqc, (int)sz.k1, (int)sz.k2, qw, cand2, st);
     HS_CUDA(cudaGetLastError());
     if (tm) tm->mark("stage2");
@@ -535,6 +645,10 @@ int hs_index_create(const hs_index_desc* ds, int device, hs_index_t* out) {
       launch_to_vertical(tmp, n, K, ix->vstride, ix->vcodes, 0);
       HS_CHECK(dalloc(*ix, &ix->hcodes, (size_t)ceil_div(K, 8) * n));
       launch_to_hcodes(tmp, n, K, ix->hcodes, 0);
+      if (ds->n_active > 0) {  // point-major rows for the filtered stage 1's sparse part
+        HS_CHECK(dalloc(*ix, &ix->pcodes, (size_t)pcodes_row(ix->npairs) * n));
+        launch_to_pcodes(tmp, n, ix->npairs, ix->pcodes, 0);
+      }
       HS_CUDA(cudaDeviceSynchronize());
       cudaFree(tmp);
     }

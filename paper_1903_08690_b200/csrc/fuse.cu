@@ -1,0 +1,244 @@
+// fuse.cu — the threshold-filtered stage 1 (tensor-core path, large batches).
+//
+// Stage 1 keeps, per query, the exact top-k1 of
+//     score(p) = acc(p) + ((bias_total + scale*total(p)) + offset)
+// over all points (pipeline.py:192-203 then select_topk, pipeline.py:165-189).
+// Materialising every u16 total costs 2 bytes per (point, query) written and
+// read back; instead:
+//   1. sample: the exact top-k1 of the first `m` points (same kernels as the
+//      full stage 1) gives T[q] = its k1-th best score.  Any subset's k1-th
+//      best is <= the full k1-th best, so every true top-k1 point scores >= T.
+//   2. k_tlim: tlim[q] = the smallest u16 total whose dense-only score reaches
+//      T (the f64 ops are monotone in the total);
+//   3. the tensor-core pass in filter mode emits only (point, total) with
+//      total >= tlim[q] — every point without a sparse part that can still
+//      reach the top-k1;
+//   4. k_fuse_cands scores the union of those and of the points the query's
+//      postings touch (their accumulators summed in the reference's ascending
+//      dim order), dropping dense candidates the postings touch (they are
+//      scored with their sparse part), and
+//   5. the variable-length selection keeps the exact top-k1.
+// A query whose candidate list overflowed, or whose postings were not
+// bucketed, is flagged and rerun through the unfiltered stage 1.
+#include "kernels.cuh"
+
+namespace hs {
+
+namespace {
+
+constexpr int kFuseThreads = 256;
+
+__device__ __forceinline__ double dense_score(double btot, double scl, double off, uint32_t t) {
+  return __dadd_rn(__dadd_rn(btot, __dmul_rn(scl, (double)t)), off);
+}
+
+__global__ void k_tlim(const Cand* __restrict__ cand_s, int64_t nq, int k,
+                       const double* __restrict__ btot, const double* __restrict__ scl,
+                       const double* __restrict__ off, uint32_t* __restrict__ tlim) {
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= nq) return;
+  const double T = cand_s[q * k + (k - 1)].s;  // -inf when the sample had < k points
+  const double b = btot[q], s = scl[q], o = off ? off[q] : 0.0;
+  int lo = 0, hi = 65536;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (dense_score(b, s, o, (uint32_t)mid) >= T) hi = mid;
+    else lo = mid + 1;
+  }
+  tlim[q] = (uint32_t)lo;
+}
+
+struct FuseArgs {
+  int64_t n;
+  int Kp, npairs;
+  int64_t prow;                 // bytes per pcodes row (multiple of 4)
+  const uint8_t* pcodes;        // [n][prow]
+  const uint8_t* luts;          // [nq][Kp][16]
+  const double* btot;
+  const double* scl;
+  const double* off;
+  const uint32_t* order;
+  const uint2* list;            // [nq][cap]
+  const uint32_t* cnt;          // [nq]
+  int64_t cap;
+  // buckets (sparse)
+  const int* bmode;
+  const uint32_t* boff;
+  const uint32_t* bslots;
+  const double* bvals;
+  int64_t capq;
+  int nchunks;
+  uint32_t* bitmap;             // [nq][words] all zero on entry and exit
+  int64_t words;
+  Cand* out;                    // [nq][M]
+  int64_t M;
+  uint32_t* out_cnt;            // [nq]
+  int* fallback;                // [nq]
+  const Cand* cand_s;           // [nq][k1] sample top-k1: [k1-1] is the threshold
+  int k1;
+};
+
+template <bool SP>
+__global__ void __launch_bounds__(kFuseThreads) k_fuse_cands(FuseArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  uint8_t* lut = smem_raw;  // [Kp][16]
+  __shared__ uint32_t s_cnt;
+  const int64_t q = blockIdx.x;
+  const int tid = threadIdx.x;
+  const uint32_t nd = a.cnt[q];
+  const int mode = SP ? a.bmode[q] : 2;
+  if (nd > (uint32_t)a.cap || mode == 0) {  // overflow / streamed postings: unfiltered rerun
+    if (tid == 0) {
+      a.fallback[q] = 1;
+      a.out_cnt[q] = 0;
+    }
+    return;
+  }
+  if (tid == 0) {
+    a.fallback[q] = 0;
+    s_cnt = 0;
+  }
+  const double b = a.btot[q], s = a.scl[q], o = a.off ? a.off[q] : 0.0;
+  const double T = a.cand_s[q * a.k1 + (a.k1 - 1)].s;  // no top-k1 point scores below
+  Cand* out = a.out + q * a.M;
+  uint32_t* bm = SP ? a.bitmap + q * a.words : nullptr;
+  const uint32_t* qb = SP ? a.boff + q * (int64_t)(a.nchunks + 1) : nullptr;
+  const uint32_t* qs = SP ? a.bslots + q * a.capq : nullptr;
+  const double* qv = SP ? a.bvals + q * a.capq : nullptr;
+  const uint32_t E = (SP && mode == 1) ? qb[a.nchunks] : 0u;
+  if (SP) {
+    const uint4* src = reinterpret_cast<const uint4*>(a.luts + q * (int64_t)a.Kp * 16);
+    for (int i = tid; i < a.Kp; i += blockDim.x) reinterpret_cast<uint4*>(lut)[i] = src[i];
+  }
+  __syncthreads();
+
+  if (SP && E > 0) {
+    // touched points: the first entry of a point inside its chunk's bucket
+    // (entries ascend in dim there) sums the point's products in order
+    for (uint32_t e = tid; e < E; e += blockDim.x) {
+      int lo = 0, hi = a.nchunks;  // largest c with qb[c] <= e
+      while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (qb[mid] <= e) lo = mid;
+        else hi = mid;
+      }
+      const uint32_t s0 = qb[lo], s1 = qb[lo + 1];
+      const uint32_t sl = qs[e];
+      bool first = true;
+      for (uint32_t j = s0; j < e && first; ++j) first = qs[j] != sl;
+      if (!first) continue;
+      double acc = 0.0;
+      acc += qv[e];
+      for (uint32_t j = e + 1; j < s1; ++j)
+        if (qs[j] == sl) acc += qv[j];
+      atomicOr(bm + (sl >> 5), 1u << (sl & 31));
+      // the point's LUT16 total from its codes (exact integer sum)
+      const uint32_t* row = reinterpret_cast<const uint32_t*>(a.pcodes + (int64_t)sl * a.prow);
+      uint32_t t = 0;
+      for (int w = 0; w * 4 < a.npairs; ++w) {
+        const uint32_t v = __ldg(row + w);
+#pragma unroll
+        for (int bb = 0; bb < 4; ++bb) {
+          const int pair = w * 4 + bb;
+          if (pair < a.npairs) {
+            const uint32_t byte = (v >> (8 * bb)) & 0xFFu;
+            t += lut[(2 * pair) * 16 + (byte & 15u)];
+            t += lut[(2 * pair + 1) * 16 + (byte >> 4)];  // padding row of odd K is zero
+          }
+        }
+      }
+      Cand c;
+      c.s = __dadd_rn(acc, dense_score(b, s, o, t));
+      if (!(c.s >= T)) continue;  // below the sample threshold (still marked touched)
+      c.tie = __ldg(a.order + sl);
+      c.slot = sl;
+      out[atomicAdd(&s_cnt, 1u)] = c;
+    }
+  }
+  __syncthreads();
+  // dense candidates without a sparse part
+  const uint2* lst = a.list + q * a.cap;
+  for (uint32_t i = tid; i < nd; i += blockDim.x) {
+    const uint2 pt = lst[i];
+    if (SP && E > 0 && (bm[pt.x >> 5] >> (pt.x & 31) & 1u)) continue;
+    Cand c;
+    c.s = __dadd_rn(0.0, dense_score(b, s, o, pt.y));
+    c.tie = __ldg(a.order + pt.x);
+    c.slot = pt.x;
+    out[atomicAdd(&s_cnt, 1u)] = c;
+  }
+  __syncthreads();
+  if (SP && E > 0)
+    for (uint32_t e = tid; e < E; e += blockDim.x) bm[qs[e] >> 5] = 0u;
+  if (tid == 0) a.out_cnt[q] = s_cnt;
+}
+
+// pair-major packed codes -> point-major rows of `prow` bytes
+__global__ void k_to_pcodes(const uint8_t* __restrict__ packed, int64_t n, int npairs,
+                            int64_t prow, uint8_t* __restrict__ pc) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  for (int j = 0; j < prow; ++j) pc[p * prow + j] = j < npairs ? packed[(int64_t)j * n + p] : 0;
+}
+
+}  // namespace
+
+int64_t pcodes_row(int npairs) { return ((int64_t)npairs + 3) / 4 * 4; }
+
+void launch_to_pcodes(const uint8_t* packed, int64_t n, int npairs, uint8_t* pc, cudaStream_t st) {
+  if (n <= 0) return;
+  k_to_pcodes<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(packed, n, npairs, pcodes_row(npairs), pc);
+}
+
+void launch_tlim(const Cand* cand_s, int64_t nq, int k, const double* btot, const double* scl,
+                 const double* off, uint32_t* tlim, cudaStream_t st) {
+  if (nq <= 0) return;
+  k_tlim<<<(unsigned)ceil_div(nq, 128), 128, 0, st>>>(cand_s, nq, k, btot, scl, off, tlim);
+}
+
+int launch_fuse_cands(const DeviceIndex& ix, int64_t nq, const uint8_t* luts, const double* btot,
+                      const double* scl, const double* off, const uint2* list,
+                      const uint32_t* cnt, int64_t cap, const SparseBuckets* sb,
+                      uint32_t* bitmap, Cand* out, int64_t M, uint32_t* out_cnt, int* fallback,
+                      const Cand* cand_s, int k1, cudaStream_t st) {
+  if (nq <= 0) return HS_OK;
+  FuseArgs a;
+  a.cand_s = cand_s;
+  a.k1 = k1;
+  a.n = ix.n;
+  a.Kp = ix.Kp;
+  a.npairs = ix.npairs;
+  a.prow = pcodes_row(ix.npairs);
+  a.pcodes = ix.pcodes;
+  a.luts = luts;
+  a.btot = btot;
+  a.scl = scl;
+  a.off = off;
+  a.order = ix.order;
+  a.list = list;
+  a.cnt = cnt;
+  a.cap = cap;
+  a.bmode = sb ? sb->mode : nullptr;
+  a.boff = sb ? sb->boff : nullptr;
+  a.bslots = sb ? sb->slots : nullptr;
+  a.bvals = sb ? sb->vals : nullptr;
+  a.capq = sb ? sb->capq : 0;
+  a.nchunks = sb ? sb->nchunks : 0;
+  a.bitmap = bitmap;
+  a.words = ceil_div(ix.n, 32);
+  a.out = out;
+  a.M = M;
+  a.out_cnt = out_cnt;
+  a.fallback = fallback;
+  const size_t smem = (size_t)ix.Kp * 16;
+  if (sb) {
+    if (!ix.pcodes) HS_FAIL(HS_EUNSUPPORTED, "filtered stage 1 needs point-major codes");
+    k_fuse_cands<true><<<(unsigned)nq, kFuseThreads, smem, st>>>(a);
+  } else {
+    k_fuse_cands<false><<<(unsigned)nq, kFuseThreads, smem, st>>>(a);
+  }
+  HS_CUDA(cudaGetLastError());
+  return HS_OK;
+}
+
+}  // namespace hs

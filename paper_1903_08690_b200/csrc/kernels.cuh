@@ -44,6 +44,7 @@ struct DeviceIndex {
   float* centers = nullptr;
   uint32_t* vcodes = nullptr;  // [K][vstride] vertical nibble planes (stage1.cu)
   uint32_t* hcodes = nullptr;  // [ceil(K/8)][n] 8 codes per point word (lut16_tc.cu)
+  uint8_t* pcodes = nullptr;   // [n][pcodes_row] point-major packed codes (fuse.cu)
   int64_t vstride = 0;
   int has_sq = 0;
   float *sq_lo = nullptr, *sq_step = nullptr;
@@ -114,6 +115,8 @@ struct Stage1Plan {
   bool use_dense = true;  // DUMP: include the dense part
   bool sparse_only_acc = false;  // DUMP: raw accumulator (no weights, no dense)
   bool sparse = true;     // the batch has sparse nonzeros to stream
+  int64_t n_limit = -1;   // scan points [0, n_limit) only (< 0: all)
+  const int* qmask = nullptr;  // if set, only queries with qmask[q] != 0 run
 };
 // per-query postings bucketed by 4096-slot chunk (stable: ascending dim then
 // slot inside a bucket) with exact f64 products; mode[q] = 1 when query q
@@ -135,7 +138,8 @@ int stage1_chunk_points();
 int64_t vertical_stride(int64_t n);
 void launch_to_vertical(const uint8_t* packed, int64_t n, int K, int64_t vstride, uint32_t* v,
                         cudaStream_t st);
-Stage1Plan plan_stage1(const DeviceIndex& ix, int64_t nq, int64_t k, int max_qnnz, int mode);
+Stage1Plan plan_stage1(const DeviceIndex& ix, int64_t nq, int64_t k, int max_qnnz, int mode,
+                       int64_t n_limit = -1);
 size_t stage1_smem_bytes(const DeviceIndex& ix, const Stage1Plan& p);
 void launch_map_dims(const DeviceIndex& ix, const QueryView& q, int64_t nnz, bool use_weight,
                      uint32_t* lbeg, uint32_t* lend, double* qv, int32_t* lidx,
@@ -153,12 +157,33 @@ bool lut16_tc_supported(const DeviceIndex& ix);
 int64_t lut16_tc_ld(int64_t n);
 int64_t lut16_tc_group(const DeviceIndex& ix);  // queries per tensor-core group
 void launch_to_hcodes(const uint8_t* packed, int64_t n, int K, uint32_t* h, cudaStream_t st);
+// totals mode: u16 totals [nq][ld] of points [0, n_limit) (n_limit < 0: all)
 int launch_lut16_tc(const DeviceIndex& ix, const uint8_t* luts, int64_t nq, uint16_t* tot,
-                    int64_t ld, cudaStream_t st);
+                    int64_t ld, cudaStream_t st, int64_t n_limit = -1);
+// filter mode: (point, total) pairs with total >= tlim[q] appended to
+// list[q][0..cap) in no particular order; cnt[q] = number of passes (> cap:
+// overflow, the list holds an arbitrary subset)
+int launch_lut16_filter(const DeviceIndex& ix, const uint8_t* luts, int64_t nq,
+                        const uint32_t* tlim, uint2* list, uint32_t* cnt, int64_t cap,
+                        cudaStream_t st);
+
+// fuse.cu (threshold-filtered stage 1 on the tensor-core path)
+int64_t pcodes_row(int npairs);
+void launch_to_pcodes(const uint8_t* packed, int64_t n, int npairs, uint8_t* pc, cudaStream_t st);
+void launch_tlim(const Cand* cand_s, int64_t nq, int k, const double* btot, const double* scl,
+                 const double* off, uint32_t* tlim, cudaStream_t st);
+int launch_fuse_cands(const DeviceIndex& ix, int64_t nq, const uint8_t* luts, const double* btot,
+                      const double* scl, const double* off, const uint2* list,
+                      const uint32_t* cnt, int64_t cap, const SparseBuckets* sb,
+                      uint32_t* bitmap, Cand* out, int64_t M, uint32_t* out_cnt, int* fallback,
+                      const Cand* cand_s, int k1, cudaStream_t st);
 
 // select.cu
+// best k of each query's row in[q][0..m) (or [0..counts[q]) when counts is
+// given), sorted by (score desc, tie asc); rows with qmask[q] == 0 are skipped
 int launch_select_topk(const Cand* in, int64_t nq, int64_t m, int64_t k, Cand* out,
-                       cudaStream_t st);
+                       cudaStream_t st, const uint32_t* counts = nullptr,
+                       const int* qmask = nullptr);
 void launch_scores_to_cands(const double* scores, const int64_t* tie_ids, int64_t nq,
                             int64_t n, Cand* out, cudaStream_t st);
 void launch_cands_to_positions(const Cand* c, int64_t nq, int64_t k, int64_t* out,

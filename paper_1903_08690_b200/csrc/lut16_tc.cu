@@ -41,6 +41,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstring>
 #include <mutex>
 
 #include "kernels.cuh"
@@ -163,8 +164,15 @@ struct TcArgs {
   int slots;               // A ring slots (32 TMEM columns each)
   const uint32_t* hcodes;  // [ceil(K/8)][n]: nibble s = code of subspace 8c+s
   const uint8_t* luts;     // [nq][Kp][16]
-  uint16_t* tot;           // [nq][ld] u16 totals
+  uint16_t* tot;           // [nq][ld] u16 totals (totals mode)
   int64_t ld;
+  int64_t stride;          // hcodes row stride (points of the whole index)
+  // filter mode: emit (point, total) with total >= tlim[q] into list[q][cap]
+  const uint32_t* tlim;    // [nq]
+  uint2* list;             // [nq][cap]
+  uint32_t* cnt;           // [nq] (may exceed cap: overflow)
+  int64_t cap;
+  uint32_t tmax;           // 255*K + 1: no total reaches it
   int64_t ngroups;
   int64_t nblocks;         // point blocks of 128
   int64_t items_per_cta;   // contiguous (group, block) items per CTA
@@ -186,13 +194,14 @@ __device__ __forceinline__ void onehot8(uint32_t w, int valid, uint32_t* r) {
   }
 }
 
-template <int MAXC>  // >= K chunks of 8 subspaces
+template <int MAXC, bool FILTER>  // MAXC >= K chunks of 8 subspaces
 __global__ void __launch_bounds__(kThreadsTc, 1)
     k_lut16_tc(TcArgs a, const __grid_constant__ CUtensorMap tmap) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   const int NQ = a.nq_grp;
   unsigned char* sB = smem_raw;  // [Kp][NQ][16]
   uint16_t* sStage = reinterpret_cast<uint16_t*>(sB + (size_t)a.Kp * NQ * 16);  // epilogue staging
+  uint32_t* sTlim = reinterpret_cast<uint32_t*>(sStage);  // filter mode: [NQ] thresholds
   uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(sStage) + kStageBytes);
   uint64_t* afull = bars;              // [slots] producers -> MMA (count 128)
   uint64_t* aempty = afull + a.slots;  // [slots] MMA commit -> producers
@@ -256,6 +265,17 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
           v = __ldg(reinterpret_cast<const uint4*>(a.luts + ((q0 + q) * a.Kp + k) * 16));
         *reinterpret_cast<uint4*>(sB + (size_t)i * 16) = v;
       }
+      if (FILTER)  // pairs of u16 thresholds (host guarantees 255*K + 1 <= 0xFFFF)
+        for (int i = tid; i < NQ / 2; i += blockDim.x) {
+          uint32_t w = 0;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int64_t q = q0 + 2 * i + h;
+            const uint32_t t = q < a.nq ? min(__ldg(a.tlim + q), a.tmax) : a.tmax;
+            w |= t << (16 * h);
+          }
+          sTlim[i] = w;
+        }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
     __syncthreads();
@@ -276,7 +296,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
 #pragma unroll
         for (int j = 0; j < HC; ++j) {
           const int c = 2 * j + par;
-          nxt[j] = (live && c < nkc) ? __ldg(a.hcodes + (int64_t)c * a.n + p) : 0u;
+          nxt[j] = (live && c < nkc) ? __ldg(a.hcodes + (int64_t)c * a.stride + p) : 0u;
         }
       };
       load_block(0);
@@ -330,6 +350,38 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
           if (c + 32 >= NQ) {  // accumulator fully read: release it to the MMA
             asm volatile("tcgen05.fence::before_thread_sync;");
             mbar_arrive(&dempty[buf]);
+          }
+          if (FILTER) {
+            // emit the (point, total) pairs at or above the query's threshold:
+            // packed u16x2 compares against the group's packed thresholds,
+            // then each lane appends its (rare) passes with one atomic each
+            const int64_t p = pbase + lane;
+            uint32_t pm = 0;  // bit j: column c+j passes
+            if (p < a.n) {
+              const uint4* tl4 = reinterpret_cast<const uint4*>(sTlim + (c >> 1));
+#pragma unroll
+              for (int g = 0; g < 4; ++g) {
+                const uint4 t4 = tl4[g];
+                const uint32_t tw[4] = {t4.x, t4.y, t4.z, t4.w};
+#pragma unroll
+                for (int h = 0; h < 4; ++h) {
+                  const int j = 8 * g + 2 * h;
+                  const uint32_t v = __vcmpgeu2(r[j] | (r[j + 1] << 16), tw[h]);
+                  pm |= ((v & 1u) | ((v >> 15) & 2u)) << j;
+                }
+              }
+            }
+            while (pm) {
+              const int j = __ffs(pm) - 1;
+              pm &= pm - 1;
+              const int64_t q = q0 + c + j;
+              const uint32_t pos = atomicAdd(a.cnt + q, 1u);
+              uint32_t val = 0;
+#pragma unroll
+              for (int jj = 0; jj < 32; ++jj) val = jj == j ? r[jj] : val;
+              if (pos < (uint32_t)a.cap) a.list[q * a.cap + pos] = make_uint2((uint32_t)p, val);
+            }
+            continue;
           }
           const int sb = (int)(ep_tile & 1);
           if (ep_tile >= 2 && lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
@@ -387,7 +439,8 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     blk_it += nblk;
     seg += nblk;
   }
-  if (warp >= 8 && warp < 12 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  if (!FILTER && warp >= 8 && warp < 12 && lane == 0)
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   __syncthreads();
   if (warp == 12) {
     asm volatile("tcgen05.fence::after_thread_sync;");
@@ -451,13 +504,18 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-int launch_lut16_tc(const DeviceIndex& ix, const uint8_t* luts, int64_t nq, uint16_t* tot,
-                    int64_t ld, cudaStream_t st) {
-  if (nq <= 0 || ix.n <= 0) return HS_OK;
+namespace {
+
+int launch_tc(const DeviceIndex& ix, const uint8_t* luts, int64_t nq, int64_t n_limit,
+              uint16_t* tot, int64_t ld, const uint32_t* tlim, uint2* list, uint32_t* cnt,
+              int64_t cap, cudaStream_t st) {
+  const int64_t n = n_limit >= 0 ? std::min(n_limit, ix.n) : ix.n;
+  if (nq <= 0 || n <= 0) return HS_OK;
   if (!lut16_tc_supported(ix)) HS_FAIL(HS_EUNSUPPORTED, "tensor-core LUT16 unsupported for this index");
+  const bool filter = list != nullptr;
   const int NQ = pick_nq(ix.Kp, nq);
   TcArgs a;
-  a.n = ix.n;
+  a.n = n;
   a.nq = nq;
   a.K = ix.K;
   a.Kp = ix.Kp;
@@ -467,36 +525,61 @@ int launch_lut16_tc(const DeviceIndex& ix, const uint8_t* luts, int64_t nq, uint
   a.luts = luts;
   a.tot = tot;
   a.ld = ld;
+  a.stride = ix.n;
+  a.tlim = tlim;
+  a.list = list;
+  a.cnt = cnt;
+  a.cap = cap;
+  a.tmax = 255u * (uint32_t)ix.K + 1u;
+  if (filter && a.tmax > 0xFFFFu) HS_FAIL(HS_EUNSUPPORTED, "filtered tensor-core pass needs K <= 256");
   a.ngroups = ceil_div(nq, NQ);
-  a.nblocks = ceil_div(ix.n, kPM);
+  a.nblocks = ceil_div(n, kPM);
   // one CTA per SM (it owns all of TMEM), equal contiguous shares of the
   // (group, block) items
   const int64_t items = a.ngroups * a.nblocks;
   const int64_t ctas = std::min<int64_t>(kNumSMs, items);
   a.items_per_cta = ceil_div(items, ctas);
   const int64_t grid = ceil_div(items, a.items_per_cta);
-  if (ld % kPM != 0) HS_FAIL(HS_EINVAL, "tensor-core totals stride must be a multiple of 128");
   const size_t smem =
       (size_t)a.Kp * NQ * 16 + kStageBytes + (2 * a.slots + 4) * sizeof(uint64_t) + 16;
   const int nkc = (int)ceil_div(a.Kp, kKC);
-  void (*kern)(TcArgs, const CUtensorMap) =
-      nkc <= 8 ? k_lut16_tc<8> : nkc <= 16 ? k_lut16_tc<16> : k_lut16_tc<33>;
+  void (*kern)(TcArgs, const CUtensorMap);
+  if (filter) kern = nkc <= 8 ? k_lut16_tc<8, true> : nkc <= 16 ? k_lut16_tc<16, true> : k_lut16_tc<33, true>;
+  else kern = nkc <= 8 ? k_lut16_tc<8, false> : nkc <= 16 ? k_lut16_tc<16, false> : k_lut16_tc<33, false>;
   HS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  // totals [nq][ld] u16 as a 2-D tensor; 32x32 boxes, no swizzle
   CUtensorMap tmap;
-  auto enc = encode_fn();
-  if (!enc) HS_FAIL(HS_ECUDA, "cuTensorMapEncodeTiled unavailable");
-  const cuuint64_t gdim[2] = {(cuuint64_t)ld, (cuuint64_t)nq};
-  const cuuint64_t gstride[1] = {(cuuint64_t)ld * sizeof(uint16_t)};
-  const cuuint32_t box[2] = {32, 32};
-  const cuuint32_t estride[2] = {1, 1};
-  if (enc(&tmap, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, tot, gdim, gstride, box, estride,
-          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-          CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-    HS_FAIL(HS_ECUDA, "cuTensorMapEncodeTiled failed for the totals buffer");
+  std::memset(&tmap, 0, sizeof(tmap));
+  if (!filter) {
+    if (ld % kPM != 0) HS_FAIL(HS_EINVAL, "tensor-core totals stride must be a multiple of 128");
+    // totals [nq][ld] u16 as a 2-D tensor; 32x32 boxes, no swizzle
+    auto enc = encode_fn();
+    if (!enc) HS_FAIL(HS_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    const cuuint64_t gdim[2] = {(cuuint64_t)ld, (cuuint64_t)nq};
+    const cuuint64_t gstride[1] = {(cuuint64_t)ld * sizeof(uint16_t)};
+    const cuuint32_t box[2] = {32, 32};
+    const cuuint32_t estride[2] = {1, 1};
+    if (enc(&tmap, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, tot, gdim, gstride, box, estride,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      HS_FAIL(HS_ECUDA, "cuTensorMapEncodeTiled failed for the totals buffer");
+  }
   kern<<<(unsigned)grid, kThreadsTc, smem, st>>>(a, tmap);
   HS_CUDA(cudaGetLastError());
   return HS_OK;
+}
+
+}  // namespace
+
+int launch_lut16_tc(const DeviceIndex& ix, const uint8_t* luts, int64_t nq, uint16_t* tot,
+                    int64_t ld, cudaStream_t st, int64_t n_limit) {
+  return launch_tc(ix, luts, nq, n_limit, tot, ld, nullptr, nullptr, nullptr, 0, st);
+}
+
+int launch_lut16_filter(const DeviceIndex& ix, const uint8_t* luts, int64_t nq,
+                        const uint32_t* tlim, uint2* list, uint32_t* cnt, int64_t cap,
+                        cudaStream_t st) {
+  HS_CUDA(cudaMemsetAsync(cnt, 0, sizeof(uint32_t) * nq, st));
+  return launch_tc(ix, luts, nq, -1, nullptr, 0, tlim, list, cnt, cap, st);
 }
 
 }  // namespace hs

@@ -16,12 +16,16 @@ constexpr int kSelThreads = 512;
 constexpr int kCap = 8192;  // 128 KB of candidates in shared memory
 
 __global__ void __launch_bounds__(kSelThreads) k_select_smem(const Cand* __restrict__ in,
-                                                             int64_t m, int k,
-                                                             Cand* __restrict__ out) {
+                                                             int64_t m_row, int k,
+                                                             Cand* __restrict__ out,
+                                                             const uint32_t* __restrict__ counts,
+                                                             const int* __restrict__ qmask) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Cand* buf = reinterpret_cast<Cand*>(smem_raw);
   const int64_t q = blockIdx.x;
-  const Cand* src = in + q * m;
+  if (qmask && qmask[q] == 0) return;
+  const Cand* src = in + q * m_row;
+  const int64_t m = counts ? min((int64_t)counts[q], m_row) : m_row;
   int have = 0;
   int64_t pos = 0;
   do {
@@ -36,6 +40,7 @@ __global__ void __launch_bounds__(kSelThreads) k_select_smem(const Cand* __restr
     pos += take;
     have = tot < k ? tot : k;
   } while (pos < m);
+  if (m == 0) have = 0;
   for (int i = threadIdx.x; i < k; i += blockDim.x) out[q * k + i] = i < have ? buf[i] : worst_cand();
 }
 
@@ -131,13 +136,16 @@ __global__ void __launch_bounds__(kSelThreads) k_shard_merge(
 }  // namespace
 
 int launch_select_topk(const Cand* in, int64_t nq, int64_t m, int64_t k, Cand* out,
-                       cudaStream_t st) {
+                       cudaStream_t st, const uint32_t* counts, const int* qmask) {
   if (nq <= 0 || k <= 0) return HS_OK;
+  if (counts || qmask) {
+    if (k > kCap / 2) HS_FAIL(HS_EUNSUPPORTED, "variable-length selection needs k <= 4096");
+  }
   if (k <= kCap / 2) {
     const size_t smem = sizeof(Cand) * kCap;
     HS_CUDA(cudaFuncSetAttribute(k_select_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem));
-    k_select_smem<<<(unsigned)nq, kSelThreads, smem, st>>>(in, m, (int)k, out);
+    k_select_smem<<<(unsigned)nq, kSelThreads, smem, st>>>(in, m, (int)k, out, counts, qmask);
     HS_CUDA(cudaGetLastError());
     return HS_OK;
   }

@@ -89,6 +89,7 @@ struct Stage1Args {
   const uint16_t* tot16;
   int64_t tot_ld;
   int exp_flags;       // dev experiments (HSB200_EXP): 1 no dense, 2 no sparse, 4 no offers
+  const int* qmask;    // only queries with qmask[q] != 0 run (null: all)
 };
 
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t s) {
@@ -376,6 +377,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
   const int tile = blockIdx.y;
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
+  if (a.qmask && a.qmask[q] == 0) return;
 
   // ---- carve shared memory ----
   Smem s;
@@ -953,7 +955,11 @@ __global__ void __launch_bounds__(kBucketThreads) k_sparse_bucket(
   int64_t E = 0;
   for (int w = 0; w < kBucketThreads / 32; ++w) E += scr[w];
   __syncthreads();
-  if (E == 0 || E > capq || E > 96LL * nchunks) {
+  if (E == 0) {
+    if (tid == 0) mode[q] = 2;  // no postings at all
+    return;
+  }
+  if (E > capq || E > 96LL * nchunks) {
     if (tid == 0) mode[q] = 0;  // stream this query's lists in stage 1
     return;
   }
@@ -1136,11 +1142,14 @@ void launch_to_vertical(const uint8_t* packed, int64_t n, int K, int64_t vstride
   k_to_vertical<<<grid, 256, 0, st>>>(packed, n, K, vstride, v);
 }
 
-Stage1Plan plan_stage1(const DeviceIndex& ix, int64_t nq, int64_t k, int max_qnnz, int mode) {
+Stage1Plan plan_stage1(const DeviceIndex& ix, int64_t nq, int64_t k, int max_qnnz, int mode,
+                       int64_t n_limit) {
   Stage1Plan p;
   p.mode = mode;
   p.max_qnnz = max_qnnz < 1 ? 1 : max_qnnz;
-  const int64_t nchunks = ceil_div(ix.n, kChunk);
+  const int64_t n = n_limit >= 0 ? std::min(n_limit, ix.n) : ix.n;
+  p.n_limit = n;
+  const int64_t nchunks = ceil_div(n, kChunk);
   // one wave of resident CTAs (3 per SM): more tiles per query cost more in
   // per-tile selection than they save in wave quantisation (measured)
   const int64_t target_ctas = 3LL * kNumSMs;
@@ -1169,7 +1178,7 @@ Stage1Plan plan_stage1(const DeviceIndex& ix, int64_t nq, int64_t k, int max_qnn
     }
     const int64_t chunks_per_tile = ceil_div(nchunks, ntiles);
     p.tile_pts = chunks_per_tile * kChunk;
-    p.ntiles = (int)ceil_div(ix.n, p.tile_pts);
+    p.ntiles = (int)ceil_div(n, p.tile_pts);
     if (k >= p.tile_pts) {
       p.mode = S1_EMIT_ALL;
       p.out_per_tile = p.tile_pts;
@@ -1183,7 +1192,7 @@ Stage1Plan plan_stage1(const DeviceIndex& ix, int64_t nq, int64_t k, int max_qnn
     if (ntiles > nchunks) ntiles = nchunks;
     if (ntiles < 1) ntiles = 1;
     p.tile_pts = ceil_div(nchunks, ntiles) * kChunk;
-    p.ntiles = (int)ceil_div(ix.n, p.tile_pts);
+    p.ntiles = (int)ceil_div(n, p.tile_pts);
     p.out_per_tile = (mode == S1_EMIT_ALL) ? p.tile_pts : 0;
   }
   if (p.ntiles < 1) p.ntiles = 1;
@@ -1219,7 +1228,8 @@ int launch_stage1(const DeviceIndex& ix, const QueryView& q, const Stage1Plan& p
                   const uint16_t* tot16, int64_t tot_ld) {
   if (q.nq <= 0 || ix.n <= 0) return HS_OK;
   Stage1Args a;
-  a.n = ix.n;
+  a.n = p.n_limit >= 0 ? std::min(p.n_limit, ix.n) : ix.n;
+  a.qmask = p.qmask;
   a.tile_pts = p.tile_pts;
   a.mode = p.mode;
   a.k = p.k;

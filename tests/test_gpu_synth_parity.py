@@ -145,3 +145,34 @@ def test_tensor_core_lut16_path_matches_oracle_and_prmt(name, n, nq, monkeypatch
         ids, sc, _ = O.search_topk(idx, *O.query_parts(qs, i), s["h"], **kw)
         assert tc[i].ids.tolist() == ids.tolist()
         np.testing.assert_allclose(tc[i].scores, sc, rtol=1e-9)
+
+
+@pytest.mark.parametrize("name,n,nq,sample,cap", [
+    ("cfg2", 60_000, 200, 4096, None),   # hybrid: filtered dense + touched points
+    ("cfg3", 80_000, 150, 4096, None),   # dense only
+    ("cfg2", 60_000, 130, 2048, 64),     # tiny lists: overflowed queries rerun unfiltered
+])
+def test_threshold_filtered_stage1_matches_unfiltered_and_oracle(name, n, nq, sample, cap,
+                                                                 monkeypatch):
+    """The filtered tensor-core stage 1 (sample threshold -> filter epilogue ->
+    candidate scoring) must select exactly what the unfiltered scan selects."""
+    ds, qs, cfg, idx = _scaled(name, n, nq)
+    s = cfg.search
+    kw = dict(overfetch=s["overfetch"], retain=s["retain"],
+              exact_final_rerank=s["exact_final_rerank"])
+    monkeypatch.setenv("HSB200_FUSE_SAMPLE", str(sample))
+    if cap:
+        monkeypatch.setenv("HSB200_FUSE_CAP", str(cap))
+    dev = hs.device_index(idx)
+    dev.set_timing(True)
+    fused = hs.search_batch(idx, qs, s["h"], **kw)
+    assert "fuse" in dev.kernel_times()  # the filtered path ran
+    monkeypatch.setenv("HSB200_NO_FUSE", "1")
+    ref = hs.search_batch(idx, qs, s["h"], **kw)
+    for a, b in zip(fused, ref):
+        assert a.ids.tolist() == b.ids.tolist()
+        assert a.scores.tolist() == b.scores.tolist()
+    for i in range(0, qs.n, max(1, qs.n // 5)):
+        ids, sc, _ = O.search_topk(idx, *O.query_parts(qs, i), s["h"], **kw)
+        assert fused[i].ids.tolist() == ids.tolist()
+        np.testing.assert_allclose(fused[i].scores, sc, rtol=1e-9)
