@@ -206,21 +206,44 @@ int run_search(DeviceIndex& ix, const hs_query_batch& qb, int64_t nnz, int max_q
                         (!sparse_part || (use_buckets && ix.pcodes != nullptr)) &&
                         !getenv_flag("HSB200_NO_FUSE");
   const int64_t expect = (int64_t)((double)sz.k1 * (double)ix.n / (double)m_s);
-  int64_t Cf = use_fuse ? std::min<int64_t>(ix.n, ((std::max<int64_t>(16384, 4 * expect) + 1023) / 1024) * 1024) : 0;
-  if (use_fuse && ev_c) Cf = std::max<int64_t>(1, std::atoll(ev_c));
+  // per-(query, tensor-core CTA) list segments: ~4x the expected passes of
+  // the largest share of a query's points one CTA covers, + 64
+  int64_t QB = std::min<int64_t>(nq, 2048);
+  int64_t nseg = 0, Cf = 0;
+  auto seg_cap = [&](int64_t qb) {
+    double frac = 1.0;
+    lut16_filter_layout(ix, qb, &nseg, &frac);
+    Cf = ((int64_t)(4.0 * (double)expect * frac) + 64 + 31) / 32 * 32;
+    if (ev_c) Cf = std::max<int64_t>(1, std::atoll(ev_c));
+  };
+  if (use_fuse) seg_cap(QB);
   const int64_t capq_all = use_buckets ? bucket_capacity(ix) : 0;
-  const int64_t Mf = Cf + capq_all;
+  // scored candidates: every dense pass (<= the segments) + touched points
+  auto cand_rows = [&]() { return std::min<int64_t>(Cf * nseg, ix.n) + capq_all; };
+  int64_t Mf = use_fuse ? cand_rows() : 0;
   const int64_t ld_s = lut16_tc_ld(m_s);
   const int64_t words = ceil_div(ix.n, 32);
   // query-chunk size bounded by scratch for the stage-1 per-tile outputs
-  int64_t QB = std::min<int64_t>(nq, 2048);
   if (use_tc) {
     const int64_t grp = lut16_tc_group(ix);
     const double per_q = use_fuse
-        ? (double)Cf * 8 + (double)Mf * 16 + (double)ld_s * 2 + (sparse_part ? words * 4.0 : 0.0)
+        ? (double)Cf * nseg * 8 + (double)Mf * 16 + (double)ld_s * 2 +
+              (sparse_part ? words * 4.0 : 0.0)
         : 2.0 * (double)tc_ld;  // u16 totals [QB][tc_ld]
     const int64_t cap = std::max<int64_t>(grp, (int64_t)(8.0e9 / per_q) / grp * grp);
     if (QB > cap) QB = cap;
+  }
+  if (use_fuse) {  // layout of the final chunk size (segments depend on it)
+    int64_t worst_seg = 0, worst_cf = 0;
+    for (int64_t qb : {QB, nq % QB}) {
+      if (qb <= 0) continue;
+      seg_cap(qb);
+      worst_seg = std::max(worst_seg, nseg);
+      worst_cf = std::max(worst_cf, Cf);
+    }
+    nseg = worst_seg;
+    Cf = worst_cf;
+    Mf = cand_rows();
   }
   int64_t s1_entries = 0;
   for (;;) {
@@ -296,8 +319,8 @@ int run_search(DeviceIndex& ix, const hs_query_batch& qb, int64_t nnz, int max_q
       p.tot_s = a.template take<uint16_t>(QB * ld_s);
       p.cand_s = a.template take<Cand>(QB * sz.k1 + 1);
       p.tlim = a.template take<uint32_t>(QB);
-      p.list = a.template take<uint2>(QB * Cf);
-      p.lcnt = a.template take<uint32_t>(QB);
+      p.list = a.template take<uint2>(QB * nseg * Cf);
+      p.lcnt = a.template take<uint32_t>(QB * nseg);
       p.fout = a.template take<Cand>(QB * Mf);
       p.fcnt = a.template take<uint32_t>(QB);
       p.fallback = a.template take<int>(QB);
@@ -385,7 +408,10 @@ int run_search(DeviceIndex& ix, const hs_query_batch& qb, int64_t nnz, int max_q
       ix.launches += 1;
       if (tm) tm->mark("lut16_tc");
       // 3. candidate scoring (+ touched points) and exact top-k1
-      HS_CHECK(launch_fuse_cands(ix, nqc, luts, btot, scl, off, P.list, P.lcnt, Cf,
+      int64_t nseg_c = 0;
+      double frac_c = 1.0;
+      lut16_filter_layout(ix, nqc, &nseg_c, &frac_c);
+      HS_CHECK(launch_fuse_cands(ix, nqc, luts, btot, scl, off, P.list, P.lcnt, Cf, (int)nseg_c,
                                  sparse_part ? &sb : nullptr, P.bitmap, P.fout, Mf, P.fcnt,
                                  P.fallback, P.cand_s, (int)sz.k1, st));
       if (tm) tm->mark("fuse");

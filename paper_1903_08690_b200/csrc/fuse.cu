@@ -58,9 +58,10 @@ struct FuseArgs {
   const double* scl;
   const double* off;
   const uint32_t* order;
-  const uint2* list;            // [nq][cap]
-  const uint32_t* cnt;          // [nq]
+  const uint2* list;            // [nq][nseg][cap]
+  const uint32_t* cnt;          // [nq][nseg]
   int64_t cap;
+  int nseg;
   // buckets (sparse)
   const int* bmode;
   const uint32_t* boff;
@@ -83,11 +84,25 @@ __global__ void __launch_bounds__(kFuseThreads) k_fuse_cands(FuseArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   uint8_t* lut = smem_raw;  // [Kp][16]
   __shared__ uint32_t s_cnt;
+  __shared__ uint32_t s_pre[kNumSMs + 2];  // prefix of the segment counts
+  __shared__ int s_over;
   const int64_t q = blockIdx.x;
   const int tid = threadIdx.x;
-  const uint32_t nd = a.cnt[q];
+  if (tid == 0) s_over = 0;
+  __syncthreads();
+  if (tid < a.nseg && a.cnt[q * a.nseg + tid] > (uint32_t)a.cap) s_over = 1;
+  if (tid == 0) {
+    uint32_t run = 0;
+    for (int c = 0; c < a.nseg; ++c) {
+      s_pre[c] = run;
+      run += min(a.cnt[q * a.nseg + c], (uint32_t)a.cap);
+    }
+    s_pre[a.nseg] = run;
+  }
+  __syncthreads();
+  const uint32_t nd = s_pre[a.nseg];
   const int mode = SP ? a.bmode[q] : 2;
-  if (nd > (uint32_t)a.cap || mode == 0) {  // overflow / streamed postings: unfiltered rerun
+  if (s_over || mode == 0) {  // overflow / streamed postings: unfiltered rerun
     if (tid == 0) {
       a.fallback[q] = 1;
       a.out_cnt[q] = 0;
@@ -157,9 +172,15 @@ __global__ void __launch_bounds__(kFuseThreads) k_fuse_cands(FuseArgs a) {
   }
   __syncthreads();
   // dense candidates without a sparse part
-  const uint2* lst = a.list + q * a.cap;
+  const uint2* lst = a.list + q * a.nseg * a.cap;
   for (uint32_t i = tid; i < nd; i += blockDim.x) {
-    const uint2 pt = lst[i];
+    int lo = 0, hi = a.nseg;  // segment of flat index i: largest c with s_pre[c] <= i
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (s_pre[mid] <= i) lo = mid;
+      else hi = mid;
+    }
+    const uint2 pt = lst[(int64_t)lo * a.cap + (i - s_pre[lo])];
     if (SP && E > 0 && (bm[pt.x >> 5] >> (pt.x & 31) & 1u)) continue;
     Cand c;
     c.s = __dadd_rn(0.0, dense_score(b, s, o, pt.y));
@@ -198,7 +219,7 @@ void launch_tlim(const Cand* cand_s, int64_t nq, int k, const double* btot, cons
 
 int launch_fuse_cands(const DeviceIndex& ix, int64_t nq, const uint8_t* luts, const double* btot,
                       const double* scl, const double* off, const uint2* list,
-                      const uint32_t* cnt, int64_t cap, const SparseBuckets* sb,
+                      const uint32_t* cnt, int64_t cap, int nseg, const SparseBuckets* sb,
                       uint32_t* bitmap, Cand* out, int64_t M, uint32_t* out_cnt, int* fallback,
                       const Cand* cand_s, int k1, cudaStream_t st) {
   if (nq <= 0) return HS_OK;
@@ -218,6 +239,8 @@ int launch_fuse_cands(const DeviceIndex& ix, int64_t nq, const uint8_t* luts, co
   a.list = list;
   a.cnt = cnt;
   a.cap = cap;
+  a.nseg = nseg;
+  if (nseg > kNumSMs + 1) HS_FAIL(HS_EINVAL, "too many list segments");
   a.bmode = sb ? sb->mode : nullptr;
   a.boff = sb ? sb->boff : nullptr;
   a.bslots = sb ? sb->slots : nullptr;

@@ -156,13 +156,17 @@ int launch_stage1(const DeviceIndex& ix, const QueryView& q, const Stage1Plan& p
 bool lut16_tc_supported(const DeviceIndex& ix);
 int64_t lut16_tc_ld(int64_t n);
 int64_t lut16_tc_group(const DeviceIndex& ix);  // queries per tensor-core group
+// filter-mode list layout for a batch of nq queries: segments per query and
+// the largest fraction of a query's points one segment (CTA) covers
+void lut16_filter_layout(const DeviceIndex& ix, int64_t nq, int64_t* nseg, double* frac);
 void launch_to_hcodes(const uint8_t* packed, int64_t n, int K, uint32_t* h, cudaStream_t st);
 // totals mode: u16 totals [nq][ld] of points [0, n_limit) (n_limit < 0: all)
 int launch_lut16_tc(const DeviceIndex& ix, const uint8_t* luts, int64_t nq, uint16_t* tot,
                     int64_t ld, cudaStream_t st, int64_t n_limit = -1);
-// filter mode: (point, total) pairs with total >= tlim[q] appended to
-// list[q][0..cap) in no particular order; cnt[q] = number of passes (> cap:
-// overflow, the list holds an arbitrary subset)
+// filter mode: (point, total) pairs with total >= tlim[q], appended to CTA-
+// private segments list[q][s][0..cap) (s < kNumSMs) in no particular order;
+// cnt[q][s] = passes of segment s (> cap: overflow, the segment holds an
+// arbitrary subset); s < nseg of lut16_filter_layout
 int launch_lut16_filter(const DeviceIndex& ix, const uint8_t* luts, int64_t nq,
                         const uint32_t* tlim, uint2* list, uint32_t* cnt, int64_t cap,
                         cudaStream_t st);
@@ -174,7 +178,7 @@ void launch_tlim(const Cand* cand_s, int64_t nq, int k, const double* btot, cons
                  const double* off, uint32_t* tlim, cudaStream_t st);
 int launch_fuse_cands(const DeviceIndex& ix, int64_t nq, const uint8_t* luts, const double* btot,
                       const double* scl, const double* off, const uint2* list,
-                      const uint32_t* cnt, int64_t cap, const SparseBuckets* sb,
+                      const uint32_t* cnt, int64_t cap, int nseg, const SparseBuckets* sb,
                       uint32_t* bitmap, Cand* out, int64_t M, uint32_t* out_cnt, int* fallback,
                       const Cand* cand_s, int k1, cudaStream_t st);
 

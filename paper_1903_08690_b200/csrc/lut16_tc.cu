@@ -167,11 +167,13 @@ struct TcArgs {
   uint16_t* tot;           // [nq][ld] u16 totals (totals mode)
   int64_t ld;
   int64_t stride;          // hcodes row stride (points of the whole index)
-  // filter mode: emit (point, total) with total >= tlim[q] into list[q][cap]
+  // filter mode: emit (point, total) with total >= tlim[q] into CTA-private
+  // segments list[q][cta][cap] with counts cnt[q][cta] (> cap: overflow)
   const uint32_t* tlim;    // [nq]
-  uint2* list;             // [nq][cap]
-  uint32_t* cnt;           // [nq] (may exceed cap: overflow)
+  uint2* list;             // [nq][nseg][cap]
+  uint32_t* cnt;           // [nq][nseg]
   int64_t cap;
+  int nseg;                // segment stride (>= grid size)
   uint32_t tmax;           // 255*K + 1: no total reaches it
   int64_t ngroups;
   int64_t nblocks;         // point blocks of 128
@@ -201,7 +203,8 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
   const int NQ = a.nq_grp;
   unsigned char* sB = smem_raw;  // [Kp][NQ][16]
   uint16_t* sStage = reinterpret_cast<uint16_t*>(sB + (size_t)a.Kp * NQ * 16);  // epilogue staging
-  uint32_t* sTlim = reinterpret_cast<uint32_t*>(sStage);  // filter mode: [NQ] thresholds
+  uint32_t* sTlim = reinterpret_cast<uint32_t*>(sStage);  // filter mode: [NQ/2] packed thresholds
+  uint32_t* sCnt = sTlim + 128;                            // filter mode: [NQ] segment counts
   uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(sStage) + kStageBytes);
   uint64_t* afull = bars;              // [slots] producers -> MMA (count 128)
   uint64_t* aempty = afull + a.slots;  // [slots] MMA commit -> producers
@@ -252,6 +255,8 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     const int64_t b1 = min(a.nblocks, b0 + (it1 - seg));
     const int64_t q0 = g * NQ;
     const int64_t nblk = b1 - b0;
+    // this CTA's list segment among the CTAs covering group g
+    const int64_t seg_id = (int64_t)blockIdx.x - (g * a.nblocks) / a.items_per_cta;
     // ---- B: the group's tables, [k][q][16].  Safe to overwrite: the
     // previous segment's epilogue waited for its last dfull commit, which
     // tracks every earlier MMA, before reaching this barrier.
@@ -276,6 +281,8 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
           }
           sTlim[i] = w;
         }
+      if (FILTER)
+        for (int i = tid; i < NQ; i += blockDim.x) sCnt[i] = 0u;
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
     __syncthreads();
@@ -375,11 +382,12 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
               const int j = __ffs(pm) - 1;
               pm &= pm - 1;
               const int64_t q = q0 + c + j;
-              const uint32_t pos = atomicAdd(a.cnt + q, 1u);
+              const uint32_t pos = atomicAdd(sCnt + c + j, 1u);  // this CTA's segment of q
               uint32_t val = 0;
 #pragma unroll
               for (int jj = 0; jj < 32; ++jj) val = jj == j ? r[jj] : val;
-              if (pos < (uint32_t)a.cap) a.list[q * a.cap + pos] = make_uint2((uint32_t)p, val);
+              if (pos < (uint32_t)a.cap)
+                a.list[(q * a.nseg + seg_id) * a.cap + pos] = make_uint2((uint32_t)p, val);
             }
             continue;
           }
@@ -438,6 +446,11 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     }
     blk_it += nblk;
     seg += nblk;
+    if (FILTER) {  // publish this CTA's segment counts of the group
+      __syncthreads();
+      for (int i = tid; i < NQ; i += blockDim.x)
+        if (q0 + i < a.nq) a.cnt[(q0 + i) * a.nseg + seg_id] = sCnt[i];
+    }
   }
   if (!FILTER && warp >= 8 && warp < 12 && lane == 0)
     asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
@@ -483,6 +496,7 @@ int64_t lut16_tc_ld(int64_t n) { return ((n + kPM - 1) / kPM) * kPM; }
 
 int64_t lut16_tc_group(const DeviceIndex& ix) { return pick_nq(ix.Kp, 1LL << 40); }
 
+
 void launch_to_hcodes(const uint8_t* packed, int64_t n, int K, uint32_t* h, cudaStream_t st) {
   if (n <= 0 || K <= 0) return;
   const int nkc = (K + kKC - 1) / kKC;
@@ -506,6 +520,27 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 namespace {
 
+struct TcLayout {
+  int NQ;
+  int64_t ngroups, nblocks, items_per_cta, grid, nseg;
+};
+
+TcLayout tc_layout(const DeviceIndex& ix, int64_t nq, int64_t n) {
+  TcLayout L;
+  L.NQ = pick_nq(ix.Kp, nq);
+  L.ngroups = ceil_div(nq, L.NQ);
+  L.nblocks = ceil_div(n, kPM);
+  // one CTA per SM (it owns all of TMEM), equal contiguous shares of the
+  // (group, block) items
+  const int64_t items = L.ngroups * L.nblocks;
+  const int64_t ctas = std::min<int64_t>(kNumSMs, items);
+  L.items_per_cta = ceil_div(items, ctas);
+  L.grid = ceil_div(items, L.items_per_cta);
+  // CTAs covering one group: its items span at most this many CTA ranges
+  L.nseg = std::min<int64_t>(L.grid, ceil_div(L.nblocks, L.items_per_cta) + 1);
+  return L;
+}
+
 int launch_tc(const DeviceIndex& ix, const uint8_t* luts, int64_t nq, int64_t n_limit,
               uint16_t* tot, int64_t ld, const uint32_t* tlim, uint2* list, uint32_t* cnt,
               int64_t cap, cudaStream_t st) {
@@ -513,7 +548,8 @@ int launch_tc(const DeviceIndex& ix, const uint8_t* luts, int64_t nq, int64_t n_
   if (nq <= 0 || n <= 0) return HS_OK;
   if (!lut16_tc_supported(ix)) HS_FAIL(HS_EUNSUPPORTED, "tensor-core LUT16 unsupported for this index");
   const bool filter = list != nullptr;
-  const int NQ = pick_nq(ix.Kp, nq);
+  const TcLayout L = tc_layout(ix, nq, n);
+  const int NQ = L.NQ;
   TcArgs a;
   a.n = n;
   a.nq = nq;
@@ -530,16 +566,13 @@ int launch_tc(const DeviceIndex& ix, const uint8_t* luts, int64_t nq, int64_t n_
   a.list = list;
   a.cnt = cnt;
   a.cap = cap;
+  a.nseg = (int)L.nseg;
   a.tmax = 255u * (uint32_t)ix.K + 1u;
   if (filter && a.tmax > 0xFFFFu) HS_FAIL(HS_EUNSUPPORTED, "filtered tensor-core pass needs K <= 256");
-  a.ngroups = ceil_div(nq, NQ);
-  a.nblocks = ceil_div(n, kPM);
-  // one CTA per SM (it owns all of TMEM), equal contiguous shares of the
-  // (group, block) items
-  const int64_t items = a.ngroups * a.nblocks;
-  const int64_t ctas = std::min<int64_t>(kNumSMs, items);
-  a.items_per_cta = ceil_div(items, ctas);
-  const int64_t grid = ceil_div(items, a.items_per_cta);
+  a.ngroups = L.ngroups;
+  a.nblocks = L.nblocks;
+  a.items_per_cta = L.items_per_cta;
+  const int64_t grid = L.grid;
   const size_t smem =
       (size_t)a.Kp * NQ * 16 + kStageBytes + (2 * a.slots + 4) * sizeof(uint64_t) + 16;
   const int nkc = (int)ceil_div(a.Kp, kKC);
@@ -575,10 +608,16 @@ int launch_lut16_tc(const DeviceIndex& ix, const uint8_t* luts, int64_t nq, uint
   return launch_tc(ix, luts, nq, n_limit, tot, ld, nullptr, nullptr, nullptr, 0, st);
 }
 
+void lut16_filter_layout(const DeviceIndex& ix, int64_t nq, int64_t* nseg, double* frac) {
+  const TcLayout L = tc_layout(ix, nq, ix.n);
+  *nseg = L.nseg;
+  *frac = std::min(1.0, (double)L.items_per_cta / (double)L.nblocks);
+}
+
 int launch_lut16_filter(const DeviceIndex& ix, const uint8_t* luts, int64_t nq,
                         const uint32_t* tlim, uint2* list, uint32_t* cnt, int64_t cap,
                         cudaStream_t st) {
-  HS_CUDA(cudaMemsetAsync(cnt, 0, sizeof(uint32_t) * nq, st));
+  HS_CUDA(cudaMemsetAsync(cnt, 0, sizeof(uint32_t) * nq * tc_layout(ix, nq, ix.n).nseg, st));
   return launch_tc(ix, luts, nq, -1, nullptr, 0, tlim, list, cnt, cap, st);
 }
 

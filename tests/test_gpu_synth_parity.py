@@ -150,7 +150,7 @@ def test_tensor_core_lut16_path_matches_oracle_and_prmt(name, n, nq, monkeypatch
 @pytest.mark.parametrize("name,n,nq,sample,cap", [
     ("cfg2", 60_000, 200, 4096, None),   # hybrid: filtered dense + touched points
     ("cfg3", 80_000, 150, 4096, None),   # dense only
-    ("cfg2", 60_000, 130, 2048, 64),     # tiny lists: overflowed queries rerun unfiltered
+    ("cfg2", 60_000, 130, 2048, 1),      # tiny list segments: overflowed queries rerun unfiltered
 ])
 def test_threshold_filtered_stage1_matches_unfiltered_and_oracle(name, n, nq, sample, cap,
                                                                  monkeypatch):
