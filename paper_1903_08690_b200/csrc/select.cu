@@ -44,6 +44,92 @@ __global__ void __launch_bounds__(kSelThreads) k_select_smem(const Cand* __restr
   for (int i = threadIdx.x; i < k; i += blockDim.x) out[q * k + i] = i < have ? buf[i] : worst_cand();
 }
 
+// Exact top-k of a variable-length row by radix select: 8-bit digits of the
+// order-preserving score key from the top (early exit once the boundary bin
+// is taken whole), then, for exact score ties at the boundary, digits of the
+// tie id from the bottom; the k selected entries are gathered and sorted.
+// Reads the row once per digit (typically 2-3), no full sort of the row.
+constexpr int kRsThreads = 512;
+
+__global__ void __launch_bounds__(kRsThreads) k_select_radix(const Cand* __restrict__ in,
+                                                             int64_t m_row, int k,
+                                                             Cand* __restrict__ out,
+                                                             const uint32_t* __restrict__ counts,
+                                                             const int* __restrict__ qmask) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Cand* buf = reinterpret_cast<Cand*>(smem_raw);  // [P] selected entries
+  __shared__ unsigned hist[256];
+  __shared__ int ctl[16];
+  const int64_t q = blockIdx.x;
+  if (qmask && qmask[q] == 0) return;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const Cand* src = in + q * m_row;
+  const int64_t m = counts ? min((int64_t)counts[q], m_row) : m_row;
+  int P = 1;
+  while (P < k) P <<= 1;
+  unsigned long long prefix = 0, pmask = 0;
+  bool whole = true;
+  uint32_t tie_lim = 0xFFFFFFFFu;
+  if (m > k) {
+    int need = k;
+    whole = false;
+    for (int shift = 56; shift >= 0; shift -= 8) {
+      for (int i = tid; i < 256; i += blockDim.x) hist[i] = 0;
+      __syncthreads();
+      for (int64_t i = tid; i < m; i += blockDim.x) {
+        const unsigned long long key = score_key(src[i].s);
+        if ((key & pmask) == prefix) atomicAdd(&hist[(key >> shift) & 255], 1u);
+      }
+      __syncthreads();
+      if (warp == 0) find_bin(hist, need, true, ctl);
+      __syncthreads();
+      prefix |= (unsigned long long)ctl[0] << shift;
+      pmask |= 0xFFull << shift;
+      need = ctl[1];
+      whole = ctl[2] == need;
+      __syncthreads();
+      if (whole) break;
+    }
+    if (!whole) {  // the `need` smallest tie ids among key == prefix
+      uint32_t tpre = 0, tmask = 0;
+      for (int shift = 24; shift >= 0; shift -= 8) {
+        for (int i = tid; i < 256; i += blockDim.x) hist[i] = 0;
+        __syncthreads();
+        for (int64_t i = tid; i < m; i += blockDim.x) {
+          const Cand e = src[i];
+          if (score_key(e.s) == prefix && (e.tie & tmask) == tpre)
+            atomicAdd(&hist[(e.tie >> shift) & 255], 1u);
+        }
+        __syncthreads();
+        if (warp == 0) find_bin(hist, need, false, ctl);
+        __syncthreads();
+        tpre |= (uint32_t)ctl[0] << shift;
+        tmask |= 0xFFu << shift;
+        need = ctl[1];
+        __syncthreads();
+      }
+      tie_lim = tpre;
+    }
+  }
+  if (tid == 0) ctl[8] = 0;
+  __syncthreads();
+  for (int64_t i = tid; i < m; i += blockDim.x) {
+    const Cand e = src[i];
+    bool keep = true;
+    if (m > k) {
+      const unsigned long long key = score_key(e.s) & pmask;
+      keep = key > prefix || (key == prefix && (whole || e.tie <= tie_lim));
+    }
+    if (keep) buf[atomicAdd(&ctl[8], 1)] = e;
+  }
+  __syncthreads();
+  const int kept = ctl[8];
+  for (int i = kept + tid; i < P; i += blockDim.x) buf[i] = worst_cand();
+  __syncthreads();
+  bitonic_sort_block(buf, P);
+  for (int i = tid; i < k; i += blockDim.x) out[q * k + i] = i < kept ? buf[i] : worst_cand();
+}
+
 __global__ void k_pad_copy(const Cand* __restrict__ in, int64_t m, int64_t P, int64_t nq,
                            Cand* __restrict__ out) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -140,6 +226,14 @@ int launch_select_topk(const Cand* in, int64_t nq, int64_t m, int64_t k, Cand* o
   if (nq <= 0 || k <= 0) return HS_OK;
   if (counts || qmask) {
     if (k > kCap / 2) HS_FAIL(HS_EUNSUPPORTED, "variable-length selection needs k <= 4096");
+    int P = 1;
+    while (P < k) P <<= 1;
+    const size_t smem = sizeof(Cand) * P;
+    HS_CUDA(cudaFuncSetAttribute(k_select_radix, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem));
+    k_select_radix<<<(unsigned)nq, kRsThreads, smem, st>>>(in, m, (int)k, out, counts, qmask);
+    HS_CUDA(cudaGetLastError());
+    return HS_OK;
   }
   if (k <= kCap / 2) {
     const size_t smem = sizeof(Cand) * kCap;

@@ -164,49 +164,6 @@ struct Smem {
   int* ctl;         // [0]=cnt [2]=have_th [4..12]=warp sums
 };
 
-// Order-preserving 64-bit key of an f64 score (-0.0 folded into +0.0: the
-// reference compares them equal and breaks the tie by id).
-__device__ __forceinline__ unsigned long long score_key(double x) {
-  const unsigned long long b = (unsigned long long)__double_as_longlong(x + 0.0);
-  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
-}
-
-// Warp 0 helper: among 256 bins, walking bins in the given direction (desc =
-// from 255 down), find the bin where the running count reaches `need`.
-// Writes bin, the count still needed inside it, and the bin's size to ctl[12..14].
-__device__ __forceinline__ void find_bin(const unsigned* hist, int need, bool desc, int* out) {
-  const int lane = threadIdx.x & 31;
-  unsigned c[8];
-  unsigned tot = 0;
-#pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    const int bin = desc ? 255 - (lane * 8 + j) : lane * 8 + j;
-    c[j] = hist[bin];
-    tot += c[j];
-  }
-  unsigned incl = tot;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const unsigned v = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += v;
-  }
-  const unsigned excl = incl - tot;
-  const bool here = excl < (unsigned)need && incl >= (unsigned)need;
-  if (here) {
-    unsigned run = excl;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      if (run + c[j] >= (unsigned)need) {
-        out[0] = desc ? 255 - (lane * 8 + j) : lane * 8 + j;
-        out[1] = need - (int)run;
-        out[2] = (int)c[j];
-        break;
-      }
-      run += c[j];
-    }
-  }
-}
-
 // Keep the best k of buf[0..cnt) by (score desc, original id asc) and set the
 // running threshold to the k-th best.  Radix select over the score key (8-bit
 // digits, early exit when a whole bin is taken) then, for exact score ties at
