@@ -21,17 +21,19 @@
 // to u16 (K <= 257 keeps them < 2^16) row-major [query][point] for the fused
 // stage-1 kernel, which adds the sparse part and selects.
 //
-// Warp roles (416 threads, one CTA per SM — it owns all 512 TMEM columns):
-//   warps 0-7  producers: thread = point lane (two warps per TMEM lane
-//              quadrant, alternate K chunks); per chunk of 8 subspaces one
-//              coalesced u32 load (8 codes, one block ahead), 32 one-hot
-//              words, one tcgen05.st.32x32b.x32 into an A ring slot, arrive
-//              `afull`;
-//   warps 8-11 epilogue: tcgen05.ld the finished accumulator, transpose
-//              through shared memory, TMA tensor store of u16 tiles, arrive
-//              `dempty`;
-//   warp 12    TMEM allocation; lane 0 issues the MMAs (<= 4 per chunk,
-//              K = 32 B = 2 subspaces each) and the tcgen05.commit arrivals.
+// Warp roles (544 threads, one CTA per SM — it owns all 512 TMEM columns):
+//   warps 0-7   producers: thread = point lane (two warps per TMEM lane
+//               quadrant, alternate K chunks); per chunk of 8 subspaces one
+//               coalesced u32 load (8 codes, one block ahead), 32 one-hot
+//               words, one tcgen05.st.32x32b.x32 into an A ring slot, arrive
+//               `afull`;
+//   warps 8-15  epilogue (two per lane quadrant, alternate 32-column tiles):
+//               tcgen05.ld the finished accumulator, then either transpose
+//               through shared memory + TMA tensor store of u16 tiles
+//               (totals mode) or compare against the queries' thresholds and
+//               append the passes (filter mode); arrive `dempty`;
+//   warp 16     TMEM allocation; one elected lane issues the MMAs (<= 4 per
+//               chunk, K = 32 B = 2 subspaces each) and the commits.
 //
 // Shared-memory B layout (SWIZZLE_NONE, K-major canonical): 16-byte column
 // block k (= subspace) holds the NQ query rows contiguously, so 8-row core
@@ -41,6 +43,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -53,11 +56,12 @@ namespace {
 constexpr int kPM = 128;       // points per block (MMA M, TMEM lanes)
 constexpr int kKC = 8;         // subspaces per K chunk (4 MMAs, 32 TMEM columns of A)
 constexpr int kProd = 128;     // arrivals per A chunk (one producer warp per lane quadrant)
-constexpr int kThreadsTc = 416;  // 8 producer, 4 epilogue, 1 MMA warps
+constexpr int kEpi = 256;        // epilogue threads (warps 8-15): dempty arrivals per block
+constexpr int kThreadsTc = 544;  // 8 producer, 8 epilogue, 1 MMA warps
 constexpr int kTmemCols = 512;
 constexpr int kMaxNQ = 224;    // 2*NQ accumulator + >= 2 A slots of 32 columns <= 512
-constexpr size_t kStageBytes = 4 * 2 * 32 * 32 * 2;  // epilogue staging: 4 warps x 2 x 32x32 u16
-constexpr size_t kSmemBudget = 200 * 1024;          // resident B (the group's tables)
+constexpr size_t kStageBytes = 8 * 2 * 32 * 32 * 2;  // epilogue staging: 8 warps x 2 x 32x32 u16
+constexpr size_t kSmemBudget = 194 * 1024;          // resident B (the group's tables)
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -174,6 +178,7 @@ struct TcArgs {
   uint32_t* cnt;           // [nq][nseg]
   int64_t cap;
   int nseg;                // segment stride (>= grid size)
+  int exp;                 // dev profiling knobs (HSB200_TC_EXP), results invalid when set
   uint32_t tmax;           // 255*K + 1: no total reaches it
   int64_t ngroups;
   int64_t nblocks;         // point blocks of 128
@@ -218,7 +223,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
   if (it0 >= it1) return;
   const int nkc = (a.Kp + kKC - 1) / kKC;
 
-  if (warp == 12) {
+  if (warp == 16) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(tmem_slot)),
                  "r"(kTmemCols));
@@ -231,7 +236,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&dfull[b], 1);
-      mbar_init(&dempty[b], kProd);
+      mbar_init(&dempty[b], kEpi);
     }
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
@@ -324,8 +329,10 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
               mbar_wait(&aempty[slot], (round - 1) & 1u);
               asm volatile("tcgen05.fence::after_thread_sync;");
             }
-            TMEM_ST32(tmem_a + lane_base + (uint32_t)(slot * 32), r);
-            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            if (!(a.exp & 2)) {
+              TMEM_ST32(tmem_a + lane_base + (uint32_t)(slot * 32), r);
+              asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            }
             asm volatile("tcgen05.fence::before_thread_sync;");
             mbar_arrive(&afull[slot]);
           }
@@ -335,36 +342,44 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
           }
         }
       }
-    } else if (warp < 12) {
+    } else if (warp < 16) {
       // ---- epilogue: accumulator -> u16 totals [query][point] ----
+      // Two warps per TMEM lane quadrant take alternate 32-column tiles.
       // Per 32x32 tile (32 points of this warp's lanes x 32 queries): the
       // tile is transposed through shared memory (conflict-free u16 stores,
       // one query row per 64 B) and one lane hands it to the TMA engine as a
       // 2-D tensor store; two staging buffers per warp.
-      const int quad = warp & 3;
+      const int quad = warp & 3, half = (warp >> 2) & 1;
       const uint32_t lane_base = (uint32_t)(quad * 32) << 16;
-      uint16_t* stg = sStage + quad * 2 * 1024;
+      uint16_t* stg = sStage + (warp - 8) * 2 * 1024;
       for (int64_t bi = 0; bi < nblk; ++bi) {
         const int64_t bt = blk_it + bi;
         const int buf = (int)(bt & 1);
         mbar_wait(&dfull[buf], (uint32_t)((bt >> 1) & 1));
         asm volatile("tcgen05.fence::after_thread_sync;");
         const int64_t pbase = (b0 + bi) * kPM + quad * 32;
-        for (int c = 0; c < NQ; c += 32) {
+        if (half * 32 >= NQ) {  // no tile of this block for this warp
+          asm volatile("tcgen05.fence::before_thread_sync;");
+          mbar_arrive(&dempty[buf]);
+        }
+        for (int c = half * 32; c < NQ; c += 64) {
           uint32_t r[32];
           TMEM_LD32(tmem + lane_base + (uint32_t)(buf * NQ + c), r);
           asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-          if (c + 32 >= NQ) {  // accumulator fully read: release it to the MMA
+          if (c + 64 >= NQ) {  // this warp's part of the accumulator read: release
             asm volatile("tcgen05.fence::before_thread_sync;");
             mbar_arrive(&dempty[buf]);
           }
+          if (a.exp & 1) continue;  // profiling knob: drain only
           if (FILTER) {
             // emit the (point, total) pairs at or above the query's threshold:
             // packed u16x2 compares against the group's packed thresholds,
             // then each lane appends its (rare) passes with one atomic each
             const int64_t p = pbase + lane;
             uint32_t pm = 0;  // bit j: column c+j passes
-            if (p < a.n) {
+            uint32_t vc[16];
+            uint32_t any = 0;
+            {
               const uint4* tl4 = reinterpret_cast<const uint4*>(sTlim + (c >> 1));
 #pragma unroll
               for (int g = 0; g < 4; ++g) {
@@ -373,10 +388,15 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
 #pragma unroll
                 for (int h = 0; h < 4; ++h) {
                   const int j = 8 * g + 2 * h;
-                  const uint32_t v = __vcmpgeu2(r[j] | (r[j + 1] << 16), tw[h]);
-                  pm |= ((v & 1u) | ((v >> 15) & 2u)) << j;
+                  vc[j >> 1] = __vcmpgeu2(__byte_perm(r[j], r[j + 1], 0x5410), tw[h]);
+                  any |= vc[j >> 1];
                 }
               }
+            }
+            if (any != 0u && p < a.n) {  // rare: expand the lane's pass mask
+#pragma unroll
+              for (int i = 0; i < 16; ++i)
+                pm |= ((vc[i] & 1u) | ((vc[i] >> 15) & 2u)) << (2 * i);
             }
             while (pm) {
               const int j = __ffs(pm) - 1;
@@ -452,10 +472,10 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
         if (q0 + i < a.nq) a.cnt[(q0 + i) * a.nseg + seg_id] = sCnt[i];
     }
   }
-  if (!FILTER && warp >= 8 && warp < 12 && lane == 0)
+  if (!FILTER && warp >= 8 && warp < 16 && lane == 0)
     asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   __syncthreads();
-  if (warp == 12) {
+  if (warp == 16) {
     asm volatile("tcgen05.fence::after_thread_sync;");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
                  "r"(kTmemCols));
@@ -567,6 +587,7 @@ int launch_tc(const DeviceIndex& ix, const uint8_t* luts, int64_t nq, int64_t n_
   a.cnt = cnt;
   a.cap = cap;
   a.nseg = (int)L.nseg;
+  a.exp = std::getenv("HSB200_TC_EXP") ? std::atoi(std::getenv("HSB200_TC_EXP")) : 0;
   a.tmax = 255u * (uint32_t)ix.K + 1u;
   if (filter && a.tmax > 0xFFFFu) HS_FAIL(HS_EUNSUPPORTED, "filtered tensor-core pass needs K <= 256");
   a.ngroups = L.ngroups;
