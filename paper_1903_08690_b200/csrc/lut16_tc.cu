@@ -54,7 +54,7 @@ namespace hs {
 namespace {
 
 constexpr int kPM = 128;       // points per block (MMA M, TMEM lanes)
-constexpr int kKC = 8;         // subspaces per K chunk (4 MMAs, 32 TMEM columns of A)
+constexpr int kKC = 8;         // subspaces per code word (8 nibbles)
 constexpr int kProd = 128;     // arrivals per A chunk (one producer warp per lane quadrant)
 constexpr int kEpi = 256;        // epilogue threads (warps 8-15): dempty arrivals per block
 constexpr int kThreadsTc = 544;  // 8 producer, 8 epilogue, 1 MMA warps
@@ -201,7 +201,10 @@ __device__ __forceinline__ void onehot8(uint32_t w, int valid, uint32_t* r) {
   }
 }
 
-template <int MAXC, bool FILTER>  // MAXC >= K chunks of 8 subspaces
+// MAXC >= code words (8 subspaces each) per point; KC = subspaces per A ring
+// slot (8: 32 TMEM columns, 4 MMAs; 16: 64 columns, 8 MMAs — fewer handoffs
+// per MMA when N is small)
+template <int MAXC, bool FILTER, int KC>
 __global__ void __launch_bounds__(kThreadsTc, 1)
     k_lut16_tc(TcArgs a, const __grid_constant__ CUtensorMap tmap) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -221,7 +224,10 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
   const int64_t it0 = (int64_t)blockIdx.x * a.items_per_cta;
   const int64_t it1 = min(a.ngroups * a.nblocks, it0 + a.items_per_cta);
   if (it0 >= it1) return;
-  const int nkc = (a.Kp + kKC - 1) / kKC;
+  constexpr int NW = KC / kKC;       // code words per chunk
+  constexpr int SC = 4 * KC;         // TMEM columns per A slot
+  const int nkc = (a.Kp + KC - 1) / KC;  // chunks per block
+  const int nwords = (a.Kp + kKC - 1) / kKC;
 
   if (warp == 16) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -298,41 +304,43 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
       // warp's tcgen05.st / barrier latency overlaps the other's generation.
       const int quad = warp & 3, par = warp >> 2;
       const uint32_t lane_base = (uint32_t)(quad * 32) << 16;
-      constexpr int HC = (MAXC + 1) / 2;
-      // this warp's code words of a block, loaded one block ahead so the
-      // global-load latency hides behind a whole block of MMAs
-      uint32_t nxt[HC];
+      // this warp's code words of a block (words of its chunks; others 0),
+      // loaded one block ahead so the load latency hides behind the MMAs
+      constexpr int NCH = (MAXC + NW - 1) / NW;    // max chunks per block
+      constexpr int OW = ((NCH + 1) / 2) * NW;     // words of this warp's chunks
+      uint32_t nxt[OW];                            // own chunk oc = c/2: words oc*NW + h
       auto load_block = [&](int64_t bi) {
         const int64_t p = (b0 + bi) * kPM + quad * 32 + lane;
         const bool live = bi < nblk && p < a.n;
 #pragma unroll
-        for (int j = 0; j < HC; ++j) {
-          const int c = 2 * j + par;
-          nxt[j] = (live && c < nkc) ? __ldg(a.hcodes + (int64_t)c * a.stride + p) : 0u;
+        for (int i = 0; i < OW; ++i) {
+          const int w = (2 * (i / NW) + par) * NW + (i % NW);
+          nxt[i] = (live && w < nwords) ? __ldg(a.hcodes + (int64_t)w * a.stride + p) : 0u;
         }
       };
       load_block(0);
       for (int64_t bi = 0; bi < nblk; ++bi) {
         const int64_t p = (b0 + bi) * kPM + quad * 32 + lane;
         const bool live = p < a.n;
-        uint32_t cur[HC];
+        uint32_t cur[OW];
 #pragma unroll
-        for (int j = 0; j < HC; ++j) cur[j] = nxt[j];
+        for (int i = 0; i < OW; ++i) cur[i] = nxt[i];
         load_block(bi + 1);
 #pragma unroll
-        for (int c = 0; c < MAXC; ++c) {
+        for (int c = 0; c < NCH; ++c) {
           if (c >= nkc) break;
           if ((c & 1) == par) {
-            uint32_t r[32];
-            onehot8(cur[c >> 1], live ? min(kKC, a.K - c * kKC) : 0, r);
             if (round > 0) {
               mbar_wait(&aempty[slot], (round - 1) & 1u);
               asm volatile("tcgen05.fence::after_thread_sync;");
             }
-            if (!(a.exp & 2)) {
-              TMEM_ST32(tmem_a + lane_base + (uint32_t)(slot * 32), r);
-              asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+#pragma unroll
+            for (int h = 0; h < NW; ++h) {  // 32 columns (8 subspaces) per store
+              uint32_t r[32];
+              onehot8(cur[(c >> 1) * NW + h], live ? min(kKC, a.K - (c * NW + h) * kKC) : 0, r);
+              if (!(a.exp & 2)) TMEM_ST32(tmem_a + lane_base + (uint32_t)(slot * SC + 32 * h), r);
             }
+            if (!(a.exp & 2)) asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
             asm volatile("tcgen05.fence::before_thread_sync;");
             mbar_arrive(&afull[slot]);
           }
@@ -442,16 +450,16 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
         for (int c = 0; c < nkc; ++c) {
           mbar_wait(&afull[slot], round & 1u);
           asm volatile("tcgen05.fence::after_thread_sync;");
-          const int npair = min(kKC, a.Kp - c * kKC) / 2;  // Kp even
-          const uint32_t ta = tmem_a + (uint32_t)(slot * 32);
+          const int npair = min(KC, a.Kp - c * KC) / 2;  // Kp even
+          const uint32_t ta = tmem_a + (uint32_t)(slot * SC);
           // B start address advances by NQ*16 bytes per subspace: +NQ in the
           // descriptor's (address >> 4) field
-          const uint64_t bd = bdesc0 + (uint64_t)(c * kKC * NQ);
+          const uint64_t bd = bdesc0 + (uint64_t)(c * KC * NQ);
           if (elect_one()) {
             mma_ts(d, ta, bd, idesc, c > 0 ? 1u : 0u);
-            if (npair > 1) mma_ts(d, ta + 8, bd + (uint64_t)(2 * NQ), idesc, 1u);
-            if (npair > 2) mma_ts(d, ta + 16, bd + (uint64_t)(4 * NQ), idesc, 1u);
-            if (npair > 3) mma_ts(d, ta + 24, bd + (uint64_t)(6 * NQ), idesc, 1u);
+#pragma unroll
+            for (int m = 1; m < KC / 2; ++m)
+              if (npair > m) mma_ts(d, ta + 8 * m, bd + (uint64_t)(2 * m * NQ), idesc, 1u);
             mma_commit(&aempty[slot]);
           }
           __syncwarp();
@@ -576,7 +584,9 @@ int launch_tc(const DeviceIndex& ix, const uint8_t* luts, int64_t nq, int64_t n_
   a.K = ix.K;
   a.Kp = ix.Kp;
   a.nq_grp = NQ;
-  a.slots = std::min(8, (kTmemCols - 2 * NQ) / 32);
+  const int nw = (int)ceil_div(a.Kp, kKC);
+  const int KCsel = (nw > 8 && nw <= 16) ? 16 : 8;  // wide slots for the K<=128, N<=128 case
+  a.slots = std::min(8, (kTmemCols - 2 * NQ) / (4 * KCsel));
   a.hcodes = ix.hcodes;
   a.luts = luts;
   a.tot = tot;
@@ -596,10 +606,11 @@ int launch_tc(const DeviceIndex& ix, const uint8_t* luts, int64_t nq, int64_t n_
   const int64_t grid = L.grid;
   const size_t smem =
       (size_t)a.Kp * NQ * 16 + kStageBytes + (2 * a.slots + 4) * sizeof(uint64_t) + 16;
-  const int nkc = (int)ceil_div(a.Kp, kKC);
   void (*kern)(TcArgs, const CUtensorMap);
-  if (filter) kern = nkc <= 8 ? k_lut16_tc<8, true> : nkc <= 16 ? k_lut16_tc<16, true> : k_lut16_tc<33, true>;
-  else kern = nkc <= 8 ? k_lut16_tc<8, false> : nkc <= 16 ? k_lut16_tc<16, false> : k_lut16_tc<33, false>;
+  if (filter)
+    kern = nw <= 8 ? k_lut16_tc<8, true, 8> : nw <= 16 ? k_lut16_tc<16, true, 16> : k_lut16_tc<33, true, 8>;
+  else
+    kern = nw <= 8 ? k_lut16_tc<8, false, 8> : nw <= 16 ? k_lut16_tc<16, false, 16> : k_lut16_tc<33, false, 8>;
   HS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   CUtensorMap tmap;
   std::memset(&tmap, 0, sizeof(tmap));
