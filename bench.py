@@ -51,6 +51,34 @@ def _peaks():
         return 6650.0, "fallback"
 
 
+def _tensor_peak():
+    """Dense u8 tensor peak: 2x the measured bf16 rate (tcgen05 kind::i8 issues in
+    the same cycles per MMA as kind::f16 with twice the K; tools/mma_bench.cu)."""
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return 2.0 * float(p["bf16_tflops"]), "2x measured bf16 (MEASURED_PEAKS.json)"
+    except Exception:
+        return 4500.0, "nominal dense int8 (fallback)"
+
+
+def _traffic(workload):
+    """ncu-measured DRAM bytes per launch of the dominant kernel, if captured
+    (profiles/<round>/traffic_<workload>.json, written by tools/ncu_traffic.py)."""
+    import glob
+
+    for path in sorted(glob.glob(os.path.join(REPO, "profiles", "*", f"traffic_{workload}.json")),
+                       reverse=True):
+        try:
+            with open(path) as f:
+                t = json.load(f)
+            t["source"] = os.path.relpath(path, REPO)
+            return t
+        except Exception:
+            continue
+    return {}
+
+
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled during the timed region."""
 
@@ -391,8 +419,12 @@ def main():
         rec = [len(np.intersect1d(res_ids[i, :10], t_ids[i])) / 10 for i in range(truth_q)]
         recall = float(np.mean(rec))
 
-    # ---- roofline of the dominant kernel (fused stage 1) ----
-    peak, peak_kind = _peaks()
+    # ---- roofline of the dominant kernel ----
+    # tensor-core path (cfg2/cfg3): k_lut16_tc, bound by the tensor cores:
+    #   algorithmic work = the one-hot LUT16 product, 2*N*Q*16K u8 ops per step
+    # posting-stream path (cfg4 / small batches): k_stage1, bound by HBM:
+    #   algorithmic bytes = 8 B per streamed posting (+ N*ceil(K/2) code bytes
+    #   per query when the CUDA-core LUT16 scan runs), SURVEY 8(d)
     di = idx.dense_index
     npairs = (di.codes.n_subspaces + 1) // 2 if di is not None else 0
     K = di.codes.n_subspaces if di is not None else 0
@@ -404,23 +436,41 @@ def main():
     hit = (len(sidx.dims) > 0) & (sidx.dims[pos] == qs.sparse.indices) if len(sidx.dims) else \
         np.zeros(qs.sparse.nnz, bool)
     postings = int(lens[pos][hit].sum()) if len(sidx.dims) else 0
-    alg_bytes = nq * (idx.n * npairs + K * 16) + 8 * postings
+    tc_ms = ktimes.get("lut16_tc")
     s1_ms = ktimes.get("stage1")
-    per_query_bytes = (idx.n * npairs + K * 16) + 8 * postings / max(nq, 1)
     roof = None
-    if s1_ms:
+    traffic = _traffic(args.workload)
+    if tc_ms and K:
+        ops = 2.0 * idx.n * nq * 16 * K
+        tpeak, tkind = _tensor_peak()
+        achieved = ops / (tc_ms / 1e3) / 1e12
+        roof = {"bound": "tensor", "achieved": achieved, "peak": tpeak, "unit": "TFLOP/s",
+                "frac": achieved / tpeak, "traffic": traffic.get("dram_bytes_per_launch"),
+                "kernel": "k_lut16_tc (tcgen05 kind::i8, threshold-filter epilogue)",
+                "peak_kind": tkind, "ops_per_step": ops, "kernel_ms_per_step": tc_ms,
+                "traffic_source": traffic.get("source"),
+                "note": "u8 ops of the one-hot x LUT product (2*N*Q*16*K per step); the "
+                        "kernel writes only threshold-passing candidates, so its HBM "
+                        "traffic is the code stream, not the N*Q score matrix"}
+    elif s1_ms:
+        alg_bytes = 8 * postings + (nq * idx.n * npairs if K else 0)
+        peak, peak_kind = _peaks()
         achieved = alg_bytes / (s1_ms / 1e3) / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": None, "kernel": "k_stage1 (fused)",
-                "peak_kind": peak_kind,
-                "alg_bytes_per_launch": alg_bytes,
-                "note": "alg bytes = Q*(N*ceil(K/2) codes + K*16 LUT) + 8 B/posting; Qb=1 "
-                        "(each query streams the codes; repeats hit L2)"}
-        if qb1:
-            a1 = per_query_bytes / (qb1 / 1e3) / 1e9
-            roof["qb1"] = {"stage1_ms": qb1, "alg_bytes": per_query_bytes, "achieved": a1,
-                           "frac": a1 / peak,
-                           "note": "one query per launch, L2 flushed before each launch"}
+                "frac": achieved / peak, "traffic": traffic.get("dram_bytes_per_launch"),
+                "kernel": "k_stage1 (posting stream + selection)", "peak_kind": peak_kind,
+                "alg_bytes_per_step": alg_bytes, "kernel_ms_per_step": s1_ms,
+                "traffic_source": traffic.get("source"),
+                "note": "alg bytes = 8 B per streamed posting (u32 id + f32 weight)"
+                        + (" + N*ceil(K/2) code bytes per query" if K else "")}
+    if roof is not None and qb1:
+        peak, peak_kind = _peaks()
+        per_query_bytes = (idx.n * npairs + K * 16) + 8 * postings / max(nq, 1)
+        a1 = per_query_bytes / (qb1 / 1e3) / 1e9
+        roof["qb1"] = {"stage1_ms": qb1, "alg_bytes": per_query_bytes, "achieved_gbs": a1,
+                       "peak_gbs": peak, "frac": a1 / peak,
+                       "note": "latency path: one query per launch (CUDA-core LUT16 + "
+                               "posting stream, HBM-bound), L2 flushed before each launch"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
