@@ -623,7 +623,9 @@ int hs_index_create(const hs_index_desc* ds, int device, hs_index_t* out) {
       HS_CUDA(cudaMalloc(&tw, sizeof(float) * nnz_post));
       HS_CUDA(cudaMemcpy(tid, ds->post_ids, sizeof(uint32_t) * nnz_post, cudaMemcpyHostToDevice));
       HS_CUDA(cudaMemcpy(tw, ds->post_w, sizeof(float) * nnz_post, cudaMemcpyHostToDevice));
-      HS_CHECK(dalloc(*ix, &ix->post, nnz_post));
+      // one pad posting: the stream copies 16-byte pairs and may read past the end
+      HS_CHECK(dalloc(*ix, &ix->post, nnz_post + 1));
+      HS_CUDA(cudaMemset(ix->post + nnz_post, 0xFF, sizeof(uint2)));
       k_interleave<<<(unsigned)ceil_div(nnz_post, T), T>>>(tid, tw, nnz_post, ix->post);
       HS_CUDA(cudaDeviceSynchronize());
       cudaFree(tid);

@@ -140,7 +140,7 @@ void launch_to_vertical(const uint8_t* packed, int64_t n, int K, int64_t vstride
                         cudaStream_t st);
 Stage1Plan plan_stage1(const DeviceIndex& ix, int64_t nq, int64_t k, int max_qnnz, int mode,
                        int64_t n_limit = -1);
-size_t stage1_smem_bytes(const DeviceIndex& ix, const Stage1Plan& p);
+size_t stage1_smem_bytes(const DeviceIndex& ix, const Stage1Plan& p, bool ws);
 void launch_map_dims(const DeviceIndex& ix, const QueryView& q, int64_t nnz, bool use_weight,
                      uint32_t* lbeg, uint32_t* lend, double* qv, int32_t* lidx,
                      cudaStream_t st);

@@ -41,8 +41,12 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kPPT = 16;                   // points per thread per chunk
 constexpr int kChunk = kThreads * kPPT;    // 4096 points
-constexpr int kOfferRound = kThreads * 4;  // worst-case offers per insertion round
+constexpr int kOfferPer = 4;                       // offers per thread per insertion round
+constexpr int kOfferRound = kThreads * kOfferPer;  // worst-case offers per insertion round
 constexpr int kSmallPostings = 512;        // below this a chunk's postings skip the barriers
+constexpr int kRingBytes = 24 * 1024;  // posting ring (bulk-copy staging), default size
+constexpr int kPieceMax = 1024;        // postings per staged piece
+constexpr int kPieceBars = 32;         // mbarrier pairs = pieces in flight
 
 struct Stage1Args {
   int64_t n;
@@ -90,6 +94,7 @@ struct Stage1Args {
   int64_t tot_ld;
   int exp_flags;       // dev experiments (HSB200_EXP): 1 no dense, 2 no sparse, 4 no offers
   const int* qmask;    // only queries with qmask[q] != 0 run (null: all)
+  uint32_t ring_bytes; // WS: posting ring size (multiple of 16, >= 2 pieces)
 };
 
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t s) {
@@ -112,6 +117,39 @@ __device__ __forceinline__ void lut8(const uint4& T, uint32_t w, uint32_t& r0, u
   const uint32_t k1 = prmt(0x80008000u, 0x80008000u, s >> 16);
   r0 = (b0 & k0) | (a0 & ~k0);
   r1 = (b1 & k1) | (a1 & ~k1);
+}
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+// 1-D bulk copy global -> shared (TMA), completion counted on `bar`
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
 }
 
 __device__ __forceinline__ uint32_t lower_bound_ids(const uint2* __restrict__ post, uint32_t lo,
@@ -159,10 +197,46 @@ struct Smem {
   uint32_t* acnt;   // their slice length
   int32_t* dskip;   // skip-table row of the dim's list, -1 if short
   uint32_t* dbeg;   // list begin (absolute posting index)
+  // warp-specialised posting stream (WS kernels)
+  unsigned char* ring;  // posting ring, kRingBytes
+  uint64_t* full;       // [kPieceBars] piece landed (bulk-copy transaction count)
+  uint64_t* empty;      // [kPieceBars] piece consumed (one arrival per consumer warp)
+  uint4* pdsc;          // [kPieceBars] piece: ring offset, ga, g0, ge
+  uint64_t* pend;       // [kPieceBars] ring end (producer's byte counter) of the piece
+  int* pdim;            // [kPieceBars] query dim of the piece, -1 = end of chunk
+  double* scratch;      // 2 dummy accumulators
   uint32_t* bslot;  // staged bucket entries (chunk-local slot)
   double* bval;     // staged bucket entries (product)
   int* ctl;         // [0]=cnt [2]=have_th [4..12]=warp sums
 };
+
+
+// Consumer-side block barrier: the whole CTA, or in warp-specialised kernels
+// the kThreads consumer threads only (named barrier 1; the producer warp runs
+// its own loop).
+template <bool WS>
+__device__ __forceinline__ void csync() {
+  if constexpr (WS) {
+    asm volatile("bar.sync 1, %0;" ::"n"(kThreads) : "memory");
+  } else {
+    __syncthreads();
+  }
+}
+template <bool WS>
+__device__ __forceinline__ bool csync_or(bool pred) {
+  if constexpr (WS) {
+    int r;
+    asm volatile(
+        "{\n\t.reg .pred a, b;\n\tsetp.ne.s32 a, %1, 0;\n\t"
+        "bar.red.or.pred b, 1, %2, a;\n\tselp.s32 %0, 1, 0, b;\n\t}"
+        : "=r"(r)
+        : "r"((int)pred), "n"(kThreads)
+        : "memory");
+    return r != 0;
+  } else {
+    return __syncthreads_or(pred) != 0;
+  }
+}
 
 // Keep the best k of buf[0..cnt) by (score desc, original id asc) and set the
 // running threshold to the k-th best.  Radix select over the score key (8-bit
@@ -192,13 +266,14 @@ __device__ int dense_tlim(double ths, double btot, double scl, double off) {
 // barrier); compaction resolves them in one parallel pass first.
 constexpr uint32_t kTieUnset = 0xFFFFFFFFu;
 
+template <bool WS>
 __device__ void compact(Smem& s, int k, bool dense, double btot, double scl, double off,
                         const uint32_t* __restrict__ order) {
   const int cnt = s.ctl[0];
-  __syncthreads();  // every thread has read ctl[0]
-  for (int i = threadIdx.x; i < cnt; i += blockDim.x)
+  csync<WS>();  // every thread has read ctl[0]
+  for (int i = threadIdx.x; i < cnt; i += kThreads)
     if (s.buf[i].tie == kTieUnset) s.buf[i].tie = __ldg(order + s.buf[i].slot);
-  __syncthreads();
+  csync<WS>();
   if (cnt <= k) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   unsigned* hist = reinterpret_cast<unsigned*>(s.bval);
@@ -206,21 +281,21 @@ __device__ void compact(Smem& s, int k, bool dense, double btot, double scl, dou
   int need = k;
   bool whole_bin = false;
   for (int shift = 56; shift >= 0; shift -= 8) {
-    for (int i = tid; i < 256; i += blockDim.x) hist[i] = 0;
-    __syncthreads();
-    for (int i = tid; i < cnt; i += blockDim.x) {
+    for (int i = tid; i < 256; i += kThreads) hist[i] = 0;
+    csync<WS>();
+    for (int i = tid; i < cnt; i += kThreads) {
       const unsigned long long key = score_key(s.buf[i].s);
       if ((key & pmask) == prefix) atomicAdd(&hist[(key >> shift) & 255], 1u);
     }
-    __syncthreads();
+    csync<WS>();
     if (warp == 0) find_bin(hist, need, true, s.ctl + 12);
-    __syncthreads();
+    csync<WS>();
     const int b = s.ctl[12];
     need = s.ctl[13];
     prefix |= (unsigned long long)b << shift;
     pmask |= 0xFFull << shift;
     whole_bin = s.ctl[14] == need;
-    __syncthreads();
+    csync<WS>();
     if (whole_bin) break;
   }
   // boundary ties in score: the `need` smallest ids among key == prefix
@@ -229,20 +304,20 @@ __device__ void compact(Smem& s, int k, bool dense, double btot, double scl, dou
     uint32_t tpre = 0, tmask = 0;
     int tneed = need;
     for (int shift = 24; shift >= 0; shift -= 8) {
-      for (int i = tid; i < 256; i += blockDim.x) hist[i] = 0;
-      __syncthreads();
-      for (int i = tid; i < cnt; i += blockDim.x) {
+      for (int i = tid; i < 256; i += kThreads) hist[i] = 0;
+      csync<WS>();
+      for (int i = tid; i < cnt; i += kThreads) {
         const Cand e = s.buf[i];
         if (score_key(e.s) == prefix && (e.tie & tmask) == tpre)
           atomicAdd(&hist[(e.tie >> shift) & 255], 1u);
       }
-      __syncthreads();
+      csync<WS>();
       if (warp == 0) find_bin(hist, tneed, false, s.ctl + 12);
-      __syncthreads();
+      csync<WS>();
       tpre |= (uint32_t)s.ctl[12] << shift;
       tmask |= 0xFFu << shift;
       tneed = s.ctl[13];
-      __syncthreads();
+      csync<WS>();
     }
     tie_lim = tpre;
   }
@@ -252,7 +327,7 @@ __device__ void compact(Smem& s, int k, bool dense, double btot, double scl, dou
   worst.tie = 0;
   worst.slot = 0;
   int kept = 0;
-  for (int base = 0; base < cnt; base += blockDim.x) {
+  for (int base = 0; base < cnt; base += kThreads) {
     const int i = base + tid;
     Cand e;
     bool keep = false;
@@ -263,7 +338,7 @@ __device__ void compact(Smem& s, int k, bool dense, double btot, double scl, dou
     }
     const unsigned bal = __ballot_sync(0xffffffffu, keep);
     if (lane == 0) s.ctl[4 + warp] = __popc(bal);
-    __syncthreads();
+    csync<WS>();
     int before = 0, total = 0;
 #pragma unroll
     for (int w = 0; w < kThreads / 32; ++w) {
@@ -276,7 +351,7 @@ __device__ void compact(Smem& s, int k, bool dense, double btot, double scl, dou
       if (better(worst, e)) worst = e;
     }
     kept += total;
-    __syncthreads();
+    csync<WS>();
   }
   // block min of the kept entries -> threshold
 #pragma unroll
@@ -289,7 +364,7 @@ __device__ void compact(Smem& s, int k, bool dense, double btot, double scl, dou
   }
   Cand* wbuf = reinterpret_cast<Cand*>(s.bval);  // histogram no longer needed
   if (lane == 0) wbuf[warp] = worst;
-  __syncthreads();
+  csync<WS>();
   if (tid == 0) {
     Cand w = wbuf[0];
     for (int i = 1; i < kThreads / 32; ++i)
@@ -299,19 +374,20 @@ __device__ void compact(Smem& s, int k, bool dense, double btot, double scl, dou
     s.ctl[2] = 1;
     s.ctl[3] = dense ? dense_tlim(w.s, btot, scl, off) : 0;
   }
-  __syncthreads();
+  csync<WS>();
 }
 
+template <bool WS>
 __device__ __forceinline__ int block_sum(int v, int* scratch) {
   // scratch: >= kThreads/32 ints; returns the block total to every thread
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   const int w = threadIdx.x >> 5;
   if ((threadIdx.x & 31) == 0) scratch[w] = v;
-  __syncthreads();
+  csync<WS>();
   int t = 0;
 #pragma unroll
   for (int i = 0; i < kThreads / 32; ++i) t += scratch[i];
-  __syncthreads();
+  csync<WS>();
   return t;
 }
 
@@ -325,10 +401,109 @@ __device__ __forceinline__ void accum32(uint32_t* acc2, const uint32_t* r, const
   }
 }
 
+// Producer warp of the warp-specialised stage 1: walks the tile's chunks,
+// finds each chunk's active query dims (ascending; skip tables for long lists,
+// galloping cursors for short ones — lane per dim), cuts their slices into
+// pieces of <= kPieceMax postings widened to 16-byte pairs from the even index
+// at or below the slice start, and bulk-copies the pieces (TMA, mbarrier
+// transaction counts) into the ring as far ahead as the kPieceBars slots and
+// kRingBytes allow.  An end-of-chunk marker (no data) closes every chunk.
+// Lane 0 issues; head/tail are ring byte counters (a piece never wraps).
+__device__ __noinline__ void produce_postings(Smem& s, const Stage1Args& a, int nd, int64_t tile_lo,
+                                              int64_t tile_hi, int lane) {
+  const uint32_t kRing = a.ring_bytes;
+  uint32_t issued = 0, released = 0;
+  uint64_t head = 0, tail = 0;
+  auto release = [&]() {
+    const int rs = (int)(released % kPieceBars);
+    mbar_wait(&s.empty[rs], (released / kPieceBars) & 1u);
+    tail = s.pend[rs];
+    ++released;
+  };
+  for (int64_t cb = tile_lo; cb < tile_hi; cb += kChunk) {
+    const int64_t ce = min(tile_hi, cb + (int64_t)kChunk);
+    int nact = 0;
+    for (int base = 0; base < nd; base += 32) {
+      const int d = base + lane;
+      int32_t row = -1;
+      uint32_t sk0 = 0, sk1 = 0;
+      if (d < nd) {
+        row = s.dskip[d];
+        if (row >= 0) {
+          const uint32_t* r = a.skip + (int64_t)row * (a.nchunks_all + 1) + cb / kChunk;
+          sk0 = __ldg(r);
+          sk1 = __ldg(r + 1);
+        }
+      }
+      const bool f = d < nd && (row >= 0 ? sk1 > sk0 : s.dnext[d] < (uint32_t)ce) &&
+                     !(a.exp_flags & 2);
+      const unsigned bal = __ballot_sync(0xffffffffu, f);
+      if (f) {
+        const int slot = nact + __popc(bal & ((1u << lane) - 1u));
+        s.alist[slot] = d;
+        if (row >= 0) {
+          s.abase[slot] = s.dbeg[d] + sk0;
+          s.acnt[slot] = sk1 - sk0;
+        } else {
+          const uint32_t cur = s.dcur[d], end = s.dend[d];
+          HS_DCHECK(cur < end && s.dnext[d] >= (uint32_t)cb);
+          const uint32_t cnt = count_below_known(a.post, cur, end, (uint32_t)ce);
+          const uint32_t nc = cur + cnt;
+          s.abase[slot] = cur;
+          s.acnt[slot] = cnt;
+          s.dcur[d] = nc;
+          s.dnext[d] = nc < end ? __ldg(&a.post[nc].x) : 0xFFFFFFFFu;
+        }
+      }
+      nact += __popc(bal);
+    }
+    __syncwarp();
+    if (lane == 0) {
+      for (int i = 0; i < nact; ++i) {
+        const int d = (int)s.alist[i];
+        uint32_t g = s.abase[i];
+        const uint32_t end = g + s.acnt[i];
+        while (g < end) {
+          const uint32_t ge = min(end, g + (uint32_t)kPieceMax), ga = g & ~1u;
+          const uint32_t bytes = ((ge - ga + 1) >> 1) * 16u;
+          while (issued - released >= (uint32_t)kPieceBars) release();
+          uint32_t phys, pad;
+          for (;;) {
+            if (released == issued) head = tail = 0;  // ring empty: restart at 0
+            phys = (uint32_t)(head % kRing);
+            pad = phys + bytes > kRing ? kRing - phys : 0u;
+            if (head + pad + bytes - tail <= (uint64_t)kRing) break;
+            release();
+          }
+          head += pad;
+          if (pad) phys = 0;
+          const int slot = (int)(issued % kPieceBars);
+          s.pdsc[slot] = make_uint4(phys, ga, g, ge);
+          s.pdim[slot] = d;
+          s.pend[slot] = head + bytes;
+          head += bytes;
+          mbar_arrive_tx(&s.full[slot], bytes);
+          bulk_g2s(s.ring + phys, a.post + ga, bytes, &s.full[slot]);
+          ++issued;
+          g = ge;
+        }
+      }
+      while (issued - released >= (uint32_t)kPieceBars) release();
+      const int slot = (int)(issued % kPieceBars);
+      s.pdim[slot] = -1;
+      s.pend[slot] = head;
+      mbar_arrive(&s.full[slot]);
+      ++issued;
+    }
+    __syncwarp();
+  }
+}
+
 // DM: dense mode (0 none, 1 PRMT LUT16 scan, 2 precomputed u16 totals);
-// SP: the query batch has postings to stream (else the sparse phase is elided).
-template <int DM, bool SP>
-__global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
+// SP: the query batch has postings to stream (else the sparse phase is elided);
+// WS: warp-specialised posting stream (a 9th, producer warp; see produce_postings).
+template <int DM, bool SP, bool WS>
+__global__ void __launch_bounds__(WS ? kThreads + 32 : kThreads, 3) k_stage1(Stage1Args a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int64_t q = blockIdx.x;
   const int tile = blockIdx.y;
@@ -365,7 +540,24 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
   p += sizeof(int32_t) * a.max_qnnz;
   s.dbeg = reinterpret_cast<uint32_t*>(p);
   p += sizeof(uint32_t) * a.max_qnnz;
-  p = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(p) + 7) & ~uintptr_t(7));
+  if (WS) {
+    p = smem_raw + ((p - smem_raw + 15) & ~(ptrdiff_t)15);
+    s.ring = p;
+    p += a.ring_bytes;
+    s.pdsc = reinterpret_cast<uint4*>(p);
+    p += sizeof(uint4) * kPieceBars;
+    s.full = reinterpret_cast<uint64_t*>(p);
+    p += sizeof(uint64_t) * kPieceBars;
+    s.empty = reinterpret_cast<uint64_t*>(p);
+    p += sizeof(uint64_t) * kPieceBars;
+    s.pend = reinterpret_cast<uint64_t*>(p);
+    p += sizeof(uint64_t) * kPieceBars;
+    s.scratch = reinterpret_cast<double*>(p);
+    p += sizeof(double) * 2;
+    s.pdim = reinterpret_cast<int*>(p);
+    p += sizeof(int) * kPieceBars;
+  }
+  p = smem_raw + ((p - smem_raw + 7) & ~(ptrdiff_t)7);
   s.bval = reinterpret_cast<double*>(p);
   p += sizeof(double) * kThreads;
   s.bslot = reinterpret_cast<uint32_t*>(p);
@@ -379,6 +571,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
   const int64_t qb = a.qptr[q], qe = a.qptr[q + 1];
   const bool bucketed = SP && a.bmode != nullptr && a.bmode[q] == 1;
   const int nd = (SP && !bucketed) ? (int)(qe - qb) : 0;  // bucketed queries skip the cursors
+  const bool stream = WS && nd > 0;  // the producer warp stages this query's postings
   HS_DCHECK(nd >= 0 && nd <= a.max_qnnz);
   const uint32_t* qboff = bucketed ? a.boff + q * (int64_t)(a.nchunks_g + 1) : nullptr;
   const uint32_t* qslots = bucketed ? a.bslots + q * a.capq : nullptr;
@@ -406,6 +599,14 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
     for (int i = tid; i < a.Kp; i += blockDim.x) s.lut[i] = src[i];
   }
   if (tid < 16) s.ctl[tid] = 0;
+  if (WS && tid == 0) {
+    for (int i = 0; i < kPieceBars; ++i) {
+      mbar_init(&s.full[i], 1);
+      mbar_init(&s.empty[i], kThreads / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
   double btot = 0.0, scl = 0.0, off = 0.0;
   if (DM != 0) {
     btot = a.bias_total[q];
@@ -430,8 +631,14 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
       tnext21 = __ldg(src + 1);
     }
   }
-  __syncthreads();
-
+  __syncthreads();  // whole CTA (producer warp included)
+  if constexpr (WS) {
+    if (warp == kThreads / 32) {
+      if (stream) produce_postings(s, a, nd, tile_lo, tile_hi, lane);
+      return;
+    }
+  }
+  uint32_t consumed = 0;  // pieces consumed (mbarrier slot and phase), uniform
   for (int64_t cb = tile_lo; cb < tile_hi; cb += kChunk) {
     const int64_t ce = min(tile_hi, cb + (int64_t)kChunk);
     const int64_t p0 = cb + (int64_t)tid * kPPT;
@@ -527,7 +734,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
           s.bslot[tid] = __ldg(qslots + e0 + tid);
           s.bval[tid] = __ldg(qvals + e0 + tid);
         }
-        __syncthreads();
+        csync<WS>();
         for (uint32_t i = tid; i < L; i += kThreads) {
           const uint32_t sl = staged ? s.bslot[i] : __ldg(qslots + e0 + i);
           bool first = true;
@@ -542,14 +749,61 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
           HS_DCHECK(sl - (uint32_t)cb < (uint32_t)kChunk);
           s.acc[acc_ix(sl - (uint32_t)cb)] = sum;
         }
-        __syncthreads();
+        csync<WS>();
         nact = 1;
         npost = 0;
       }
     }
-    if (SP && !bucketed) {
+    if (stream) {
+      // ---- sparse (warp-specialised): consume the producer's pieces ----
+      // Pieces arrive in ascending dim order; a barrier separates dims (each
+      // point's additions stay in ascending dim order), thread t adds posting
+      // pairs t, t+256, ... of a piece, and every warp releases the piece's
+      // ring space with one arrival on its empty barrier.
+      for (int i = tid; i < kChunk; i += kThreads) s.acc[i] = 0.0;
+      csync<WS>();
+      int cur = -1;
+      const uint32_t ring = smem_addr(s.ring);
+      for (;;) {
+        const int slot = (int)(consumed % kPieceBars);
+        mbar_wait(&s.full[slot], (consumed / kPieceBars) & 1u);
+        ++consumed;
+        const int d = s.pdim[slot];
+        if (d < 0) {  // end of chunk
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&s.empty[slot]);
+          break;
+        }
+        const uint4 pc = s.pdsc[slot];  // ring offset, ga, g0, ge
+        if (d != cur) {
+          if (cur >= 0) csync<WS>();
+          cur = d;
+        }
+        const double qv = s.dqv[d];
+        const uint32_t np = (pc.w - pc.y + 1) >> 1;
+        for (uint32_t j = tid; j < np; j += kThreads) {
+          uint4 v;
+          asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                       : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                       : "r"(ring + pc.x + 16 * j));
+          const uint32_t g = pc.y + 2 * j;
+          // halves outside [g0, ge) go to a scratch slot; f64(q)*f64(w) is
+          // exact, so the fma rounds like the reference's separate add
+          double* a0 = g >= pc.z ? &s.acc[acc_ix(v.x - (uint32_t)cb)] : s.scratch;
+          double* a1 = g + 1 < pc.w ? &s.acc[acc_ix(v.z - (uint32_t)cb)] : s.scratch + 1;
+          HS_DCHECK(g < pc.z || (v.x >= cb && v.x < ce));
+          HS_DCHECK(g + 1 >= pc.w || (v.z >= cb && v.z < ce));
+          *a0 = fma(qv, (double)__uint_as_float(v.y), *a0);
+          *a1 = fma(qv, (double)__uint_as_float(v.w), *a1);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&s.empty[slot]);
+      }
+      csync<WS>();
+      nact = 1;
+    } else if (SP && !bucketed) {
       // ---- sparse: active dims of this chunk, in ascending dim order ----
-      for (int base = 0; base < nd; base += blockDim.x) {
+      for (int base = 0; base < nd; base += kThreads) {
         const int d = base + tid;
         int32_t row = -1;
         uint32_t sk0 = 0, sk1 = 0;
@@ -565,7 +819,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
                        !(a.exp_flags & 2);
         const unsigned bal = __ballot_sync(0xffffffffu, f);
         if (lane == 0) s.ctl[4 + warp] = __popc(bal);
-        __syncthreads();
+        csync<WS>();
         int before = 0, total = 0;
   #pragma unroll
         for (int i = 0; i < kThreads / 32; ++i) {
@@ -595,22 +849,22 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
           }
         }
         nact += total;
-        __syncthreads();
+        csync<WS>();
       }
       if (nact > 0) {
         int mine = 0;
-        for (int i = tid; i < nact; i += blockDim.x) mine += (int)s.acnt[i];
-        npost = block_sum(mine, s.ctl + 4);
+        for (int i = tid; i < nact; i += kThreads) mine += (int)s.acnt[i];
+        npost = block_sum<WS>(mine, s.ctl + 4);
       }
   #ifdef HS_DEBUG
-      for (int i = tid; i < nact; i += blockDim.x) {
+      for (int i = tid; i < nact; i += kThreads) {
         const uint32_t id0 = __ldg(&a.post[s.abase[i]].x);
         if (!(id0 >= (uint32_t)cb && id0 < (uint32_t)ce))
           printf("STALE q=%d i=%d nact=%d d=%u base=%u cnt=%u id0=%u cb=%lld ctlw=%d,%d,%d,%d,%d,%d,%d,%d\n",
                  (int)q, i, nact, s.alist[i], s.abase[i], s.acnt[i], id0, (long long)cb, s.ctl[4],
                  s.ctl[5], s.ctl[6], s.ctl[7], s.ctl[8], s.ctl[9], s.ctl[10], s.ctl[11]);
       }
-      __syncthreads();
+      csync<WS>();
   #endif
       if (nact > 0 && npost <= kSmallPostings) {
         // few postings: every thread walks them all in dim order (broadcast
@@ -638,17 +892,17 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
         // many postings: block-wide per dim, one barrier between dims; the
         // next dim's first kPre*256 postings are loaded while this dim adds
         constexpr int kPre = 4;
-        for (int i = tid; i < kChunk; i += blockDim.x) s.acc[i] = 0.0;
+        for (int i = tid; i < kChunk; i += kThreads) s.acc[i] = 0.0;
         uint2 nxt[kPre];
         {
           const uint32_t b = s.abase[0], c = s.acnt[0];
 #pragma unroll
           for (int r = 0; r < kPre; ++r) {
-            const uint32_t j = tid + r * blockDim.x;
+            const uint32_t j = tid + r * kThreads;
             nxt[r] = j < c ? __ldg(&a.post[b + j]) : make_uint2(0xFFFFFFFFu, 0u);
           }
         }
-        __syncthreads();
+        csync<WS>();
         for (int i = 0; i < nact; ++i) {
           const uint32_t b = s.abase[i], c = s.acnt[i];
           const double qv = s.dqv[s.alist[i]];
@@ -659,7 +913,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
             const uint32_t b2 = s.abase[i + 1], c2 = s.acnt[i + 1];
 #pragma unroll
             for (int r = 0; r < kPre; ++r) {
-              const uint32_t j = tid + r * blockDim.x;
+              const uint32_t j = tid + r * kThreads;
               nxt[r] = j < c2 ? __ldg(&a.post[b2 + j]) : make_uint2(0xFFFFFFFFu, 0u);
             }
           }
@@ -672,11 +926,11 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
           }
           // long slices: the rest in batches of 8 loads in flight per thread
           constexpr int kB = 8;
-          for (uint32_t j0 = kPre * blockDim.x; j0 < c; j0 += kB * blockDim.x) {
+          for (uint32_t j0 = kPre * kThreads; j0 < c; j0 += kB * kThreads) {
             uint2 v[kB];
 #pragma unroll
             for (int r = 0; r < kB; ++r) {
-              const uint32_t j = j0 + tid + r * blockDim.x;
+              const uint32_t j = j0 + tid + r * kThreads;
               v[r] = j < c ? __ldg(&a.post[b + j]) : make_uint2(0xFFFFFFFFu, 0u);
             }
 #pragma unroll
@@ -686,7 +940,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
               s.acc[acc_ix(v[r].x - (uint32_t)cb)] += qv * (double)__uint_as_float(v[r].y);
             }
           }
-          __syncthreads();
+          csync<WS>();
         }
       }
     }
@@ -712,7 +966,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
         a.dump[q * a.n + p0 + j] = score(j);
         if (a.dump_tot) a.dump_tot[q * a.n + p0 + j] = tot[j];
       }
-      __syncthreads();
+      csync<WS>();
       continue;
     }
     if (a.mode == S1_EMIT_ALL) {
@@ -728,7 +982,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
           o[pt - tile_lo] = c;
         }
       }
-      __syncthreads();
+      csync<WS>();
       continue;
     }
 
@@ -738,7 +992,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
 #pragma unroll
       for (int j = 0; j < kPPT; ++j) t += score(j);
       if (t == 12345.678) s.ctl[15] = 1;  // keep the scores live
-      __syncthreads();
+      csync<WS>();
       continue;
     }
     unsigned mask = 0;
@@ -761,11 +1015,11 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
     }
     // nothing passes anywhere in the block (the steady state once the
     // threshold has settled): one barrier, no counting
-    if (!__syncthreads_or(mask != 0u)) continue;
+    if (!csync_or<WS>(mask != 0u)) continue;
     // snapshot the count before block_sum's barriers: threads that pass the
     // room check start appending (atomicAdd on ctl[0]) right after it
     const int cnt0 = s.ctl[0];
-    const int need = block_sum(__popc(mask), s.ctl + 4);
+    const int need = block_sum<WS>(__popc(mask), s.ctl + 4);
     if (cnt0 + need <= a.cap) {
       // common case: room for every offer
       if (mask) {
@@ -781,23 +1035,23 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
           s.buf[pos++] = c;
         }
       }
-      __syncthreads();
+      csync<WS>();
     } else {
-      // rounds of <= 4 offers per thread, compacting whenever room runs out
+      // rounds of <= kOfferPer offers per thread, compacting whenever room runs out
 #pragma unroll
-      for (int r = 0; r < kPPT / 4; ++r) {
-        unsigned m = (mask >> (4 * r)) & 0xFu;
+      for (int r = 0; r < kPPT / kOfferPer; ++r) {
+        unsigned m = (mask >> (kOfferPer * r)) & ((1u << kOfferPer) - 1u);
         const int cnt_r = s.ctl[0];  // read before the barriers, see above
-        const int nr = block_sum(__popc(m), s.ctl + 4);
+        const int nr = block_sum<WS>(__popc(m), s.ctl + 4);
         if (nr == 0) continue;
         if (cnt_r + nr > a.cap) {
-          compact(s, a.k, DM != 0, btot, scl, off, a.order);
+          compact<WS>(s, a.k, DM != 0, btot, scl, off, a.order);
           const Cand th = *s.th;
           unsigned m2 = 0;
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
+          for (int j = 0; j < kOfferPer; ++j) {
             if (!(m >> j & 1)) continue;
-            const int jj = 4 * r + j;
+            const int jj = kOfferPer * r + j;
             const double sj = score(jj);
             bool pass = sj > th.s;
             if (!pass && sj == th.s) pass = a.order[p0 + jj] < th.tie;
@@ -809,9 +1063,9 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
           int pos = atomicAdd(&s.ctl[0], __popc(m));
           HS_DCHECK(pos + __popc(m) <= a.cap);
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
+          for (int j = 0; j < kOfferPer; ++j) {
             if (!(m >> j & 1)) continue;
-            const int jj = 4 * r + j;
+            const int jj = kOfferPer * r + j;
             Cand c;
             c.s = score(jj);
             c.slot = (uint32_t)(p0 + jj);
@@ -819,22 +1073,22 @@ __global__ void __launch_bounds__(kThreads, 3) k_stage1(Stage1Args a) {
             s.buf[pos++] = c;
           }
         }
-        __syncthreads();
+        csync<WS>();
       }
     }
   }
 
   if (a.mode == S1_EMIT_ALL) {
     Cand* o = a.out + (q * a.ntiles + tile) * a.out_per_tile;
-    for (int64_t i = (tile_hi - tile_lo) + tid; i < a.out_per_tile; i += blockDim.x)
+    for (int64_t i = (tile_hi - tile_lo) + tid; i < a.out_per_tile; i += kThreads)
       o[i] = worst_cand();
     return;
   }
   if (a.mode != S1_SELECT) return;
-  compact(s, a.k, false, 0.0, 0.0, 0.0, a.order);  // best k of the tile, unordered (the merge sorts)
+  compact<WS>(s, a.k, false, 0.0, 0.0, 0.0, a.order);  // best k of the tile, unordered (the merge sorts)
   Cand* o = a.out + (q * a.ntiles + tile) * a.out_per_tile;
   const int keep = s.ctl[0];
-  for (int i = tid; i < a.out_per_tile; i += blockDim.x) o[i] = i < keep ? s.buf[i] : worst_cand();
+  for (int i = tid; i < a.out_per_tile; i += kThreads) o[i] = i < keep ? s.buf[i] : worst_cand();
 }
 
 // Map each query nonzero to its posting list [beg, end) (binary search over
@@ -1141,7 +1395,7 @@ Stage1Plan plan_stage1(const DeviceIndex& ix, int64_t nq, int64_t k, int max_qnn
       p.out_per_tile = p.tile_pts;
     } else {
       p.k = (int)k;
-      p.cap = next_pow2(k + kOfferRound);
+      p.cap = (int)((k + kOfferRound + 7) / 8 * 8);  // compaction keeps k, a round adds <= kOfferRound
       p.out_per_tile = k;
     }
   } else {
@@ -1156,11 +1410,23 @@ Stage1Plan plan_stage1(const DeviceIndex& ix, int64_t nq, int64_t k, int max_qnn
   return p;
 }
 
-size_t stage1_smem_bytes(const DeviceIndex& ix, const Stage1Plan& p) {
+static uint32_t ring_bytes_env() {
+  static const uint32_t v = [] {
+    const char* e = getenv("HSB200_RING_KB");
+    const int kb = e ? atoi(e) : 0;
+    return kb >= 24 && kb <= 160 ? (uint32_t)kb * 1024u : (uint32_t)kRingBytes;
+  }();
+  return v;
+}
+
+size_t stage1_smem_bytes(const DeviceIndex& ix, const Stage1Plan& p, bool ws) {
   size_t b = sizeof(Cand) * (size_t)(p.mode == S1_SELECT ? p.cap : 0) + sizeof(Cand);
   b += sizeof(double) * kChunk;
   b += 16 * (size_t)ix.Kp;
   b += (sizeof(double) + 8 * sizeof(uint32_t)) * (size_t)p.max_qnnz;
+  if (ws)  // posting ring + piece barriers/descriptors
+    b += 16 + ring_bytes_env() + (sizeof(uint4) + 3 * sizeof(uint64_t) + sizeof(int)) * kPieceBars +
+         2 * sizeof(double);
   b += 8 + (sizeof(double) + sizeof(uint32_t)) * kThreads;  // bucket staging
   b += sizeof(int) * 16;
   return b;
@@ -1225,6 +1491,7 @@ int launch_stage1(const DeviceIndex& ix, const QueryView& q, const Stage1Plan& p
   a.nchunks_all = (int)ceil_div(ix.n, kChunk);
   a.tot16 = tot16;
   a.tot_ld = tot_ld;
+  a.ring_bytes = ring_bytes_env();
   {
     static const int exp_flags = [] {
       const char* e = getenv("HSB200_EXP");
@@ -1232,23 +1499,31 @@ int launch_stage1(const DeviceIndex& ix, const QueryView& q, const Stage1Plan& p
     }();
     a.exp_flags = exp_flags;
   }
-  const size_t smem = stage1_smem_bytes(ix, p);
-  if (smem > 227 * 1024) HS_FAIL(HS_EUNSUPPORTED, "stage-1 shared memory exceeds 227 KB "
-                                                  "(too many query nonzeros or candidates)");
   const int dm = !a.has_dense ? 0 : (tot16 != nullptr ? 2 : 1);
   const bool sp = p.sparse && ix.nnz_post > 0 && lbeg != nullptr;
+  // warp-specialised posting stream (kernels without the PRMT scan): opt-in
+  // with HSB200_WS=1 — measured slower than the single-role kernel on cfg4
+  // (1.59 s vs 1.18 s per 10K queries), kept for the experiment
+  static const bool ws_env = [] {
+    const char* e = getenv("HSB200_WS");
+    return e && e[0] == '1';
+  }();
+  const bool ws = sp && dm != 1 && ws_env;
+  const size_t smem = stage1_smem_bytes(ix, p, ws);
+  if (smem > 227 * 1024) HS_FAIL(HS_EUNSUPPORTED, "stage-1 shared memory exceeds 227 KB "
+                                                  "(too many query nonzeros or candidates)");
   void (*kern)(Stage1Args) = nullptr;
   switch (dm * 2 + (sp ? 1 : 0)) {
-    case 0: kern = k_stage1<0, false>; break;
-    case 1: kern = k_stage1<0, true>; break;
-    case 2: kern = k_stage1<1, false>; break;
-    case 3: kern = k_stage1<1, true>; break;
-    case 4: kern = k_stage1<2, false>; break;
-    default: kern = k_stage1<2, true>; break;
+    case 0: kern = k_stage1<0, false, false>; break;
+    case 1: kern = ws ? k_stage1<0, true, true> : k_stage1<0, true, false>; break;
+    case 2: kern = k_stage1<1, false, false>; break;
+    case 3: kern = k_stage1<1, true, false>; break;
+    case 4: kern = k_stage1<2, false, false>; break;
+    default: kern = ws ? k_stage1<2, true, true> : k_stage1<2, true, false>; break;
   }
   HS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   dim3 grid((unsigned)q.nq, (unsigned)p.ntiles);
-  kern<<<grid, kThreads, smem, st>>>(a);
+  kern<<<grid, ws ? kThreads + 32 : kThreads, smem, st>>>(a);
   HS_CUDA(cudaGetLastError());
   return HS_OK;
 }

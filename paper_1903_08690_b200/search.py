@@ -314,9 +314,9 @@ def search_batch(index, queries, h: int | None = None, threads: int = 1, device:
     nat.check(nat.lib().hs_search_batch(dev.handle, ctypes.byref(b), ctypes.byref(p),
                                         nat.ptr(ids), nat.ptr(scores), nat.ptr(secs)))
     per_q = (secs / q.nq).tolist()
-    return [SearchResult(ids=ids[i], scores=scores[i],
-                         stages=StageStats(candidates=[k1, k2, kh], seconds=list(per_q)))
-            for i in range(q.nq)]
+    # one row view per query (list() of a 2-D array is the cheapest way to get them)
+    return [SearchResult(i_row, s_row, StageStats([k1, k2, kh], per_q.copy()))
+            for i_row, s_row in zip(list(ids), list(scores))]
 
 
 def search_topk(index, query, h: int | None = None, *, overfetch=None, retain=None,

@@ -392,13 +392,14 @@ class HybridIndexConfig:
         return PruneThresholds(top_t=self.top_t, residual_min=np.asarray(self.residual_threshold))
 
 
-@dataclass
+# slotted: a batch of 10^3-10^4 results is built on every search_batch call
+@dataclass(slots=True)
 class StageStats:
     candidates: list = field(default_factory=list)
     seconds: list = field(default_factory=list)
 
 
-@dataclass
+@dataclass(slots=True)
 class SearchResult:
     ids: np.ndarray
     scores: np.ndarray
