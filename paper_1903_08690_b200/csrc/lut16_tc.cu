@@ -21,18 +21,20 @@
 // to u16 (K <= 257 keeps them < 2^16) row-major [query][point] for the fused
 // stage-1 kernel, which adds the sparse part and selects.
 //
-// Warp roles (544 threads, one CTA per SM — it owns all 512 TMEM columns):
-//   warps 0-7   producers: thread = point lane (two warps per TMEM lane
-//               quadrant, alternate K chunks); per chunk of 8 subspaces one
-//               coalesced u32 load (8 codes, one block ahead), 32 one-hot
-//               words, one tcgen05.st.32x32b.x32 into an A ring slot, arrive
-//               `afull`;
-//   warps 8-15  epilogue (two per lane quadrant, alternate 32-column tiles):
-//               tcgen05.ld the finished accumulator, then either transpose
-//               through shared memory + TMA tensor store of u16 tiles
-//               (totals mode) or compare against the queries' thresholds and
-//               append the passes (filter mode); arrive `dempty`;
-//   warp 16     TMEM allocation; one elected lane issues the MMAs (<= 4 per
+// Warp roles (672 threads, one CTA per SM — it owns all 512 TMEM columns):
+//   warps 0-11  producers: thread = point lane (three warps per TMEM lane
+//               quadrant, K chunks round-robin — the one-hot generation is
+//               latency-bound per warp, so it needs the warps); per 8
+//               subspaces one coalesced u32 load (8 codes, one block ahead),
+//               32 one-hot words (one clamped funnel shift each), one
+//               tcgen05.st.32x32b.x32 into an A ring slot, arrive `afull`;
+//   warps 12-19 epilogue (two per lane quadrant, alternate 32-column
+//               tiles): tcgen05.ld the finished
+//               accumulator, then either transpose through shared memory +
+//               TMA tensor store of u16 tiles (totals mode) or compare
+//               against the queries' thresholds and append the passes
+//               (filter mode); arrive `dempty`;
+//   warp 20     TMEM allocation; one elected lane issues the MMAs (<= 8 per
 //               chunk, K = 32 B = 2 subspaces each) and the commits.
 //
 // Shared-memory B layout (SWIZZLE_NONE, K-major canonical): 16-byte column
@@ -56,11 +58,17 @@ namespace {
 constexpr int kPM = 128;       // points per block (MMA M, TMEM lanes)
 constexpr int kKC = 8;         // subspaces per code word (8 nibbles)
 constexpr int kProd = 128;     // arrivals per A chunk (one producer warp per lane quadrant)
-constexpr int kEpi = 256;        // epilogue threads (warps 8-15): dempty arrivals per block
-constexpr int kThreadsTc = 544;  // 8 producer, 8 epilogue, 1 MMA warps
+constexpr int kNPar = 3;       // producer warps per TMEM lane quadrant (round-robin over chunks)
+constexpr int kEpiPar = 2;     // epilogue warps per lane quadrant (alternate 32-column tiles)
+constexpr int kProdWarps = 4 * kNPar;
+constexpr int kEpiWarp0 = kProdWarps;      // a multiple of 4: warp & 3 = lane quadrant
+constexpr int kMmaWarp = kEpiWarp0 + 4 * kEpiPar;
+constexpr int kEpi = 128 * kEpiPar;        // epilogue threads: dempty arrivals per block
+constexpr int kThreadsTc = 32 * (kMmaWarp + 1);  // 12 producer, 8 epilogue, 1 MMA warps
+static_assert(kEpiWarp0 % 4 == 0, "epilogue warps must start on a lane-quadrant boundary");
 constexpr int kTmemCols = 512;
 constexpr int kMaxNQ = 224;    // 2*NQ accumulator + >= 2 A slots of 32 columns <= 512
-constexpr size_t kStageBytes = 8 * 2 * 32 * 32 * 2;  // epilogue staging: 8 warps x 2 x 32x32 u16
+constexpr size_t kStageBytes = 4 * kEpiPar * 2 * 32 * 32 * 2;  // epilogue staging: 2 x 32x32 u16 per warp
 constexpr size_t kSmemBudget = 194 * 1024;          // resident B (the group's tables)
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -178,12 +186,26 @@ struct TcArgs {
   uint32_t* cnt;           // [nq][nseg]
   int64_t cap;
   int nseg;                // segment stride (>= grid size)
-  int exp;                 // dev profiling knobs (HSB200_TC_EXP), results invalid when set
+  int exp;                 // dev profiling knobs (HSB200_TC_EXP: 1 epilogue drain only, 2 no TMEM
+                           // stores, 8 no MMAs, 16 per-warp wait cycles), results invalid when set
   uint32_t tmax;           // 255*K + 1: no total reaches it
   int64_t ngroups;
   int64_t nblocks;         // point blocks of 128
   int64_t items_per_cta;   // contiguous (group, block) items per CTA
 };
+
+// One-hot words of 8 full subspaces: word 4s + i = 1 << (8*code - 32*i) when
+// that shift is in [0, 32), else 0 — one clamped funnel shift per word (an
+// out-of-range or "negative" unsigned shift clamps to 32 and yields the zero
+// low half).
+__device__ __forceinline__ void onehot8_full(uint32_t w, uint32_t* r) {
+#pragma unroll
+  for (int s = 0; s < kKC; ++s) {
+    const uint32_t c8 = s == 0 ? (w << 3) & 0x78u : (w >> (4 * s - 3)) & 0x78u;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) r[4 * s + i] = __funnelshift_lc(0u, 1u, c8 - 32u * i);
+  }
+}
 
 // One-hot words of 8 subspaces: word 4s + i has byte (code & 3) = 1 when
 // (code >> 2) == i, for the code of subspace s (its 16-byte K row); subspaces
@@ -229,7 +251,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
   const int nkc = (a.Kp + KC - 1) / KC;  // chunks per block
   const int nwords = (a.Kp + kKC - 1) / kKC;
 
-  if (warp == 16) {
+  if (warp == kMmaWarp) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(tmem_slot)),
                  "r"(kTmemCols));
@@ -256,6 +278,8 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
   // range spans few groups.  Per group segment: load the group's tables into
   // shared memory, then stream its blocks through the pipeline.  Pipeline
   // counters run across segments so the barrier parities stay in step.
+  long long tw0 = 0, tw1 = 0, tw2 = 0;  // exp&16: cycles waiting (per warp role)
+  const long long tstart = clock64();
   int64_t blk_it = 0;
   int slot = 0;          // A ring position (producers and issuer walk it in step)
   uint32_t round = 0;    // completed passes over the ring
@@ -298,23 +322,23 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     }
     __syncthreads();
 
-    if (warp < 8) {
+    if (warp < kProdWarps) {
       // ---- producers: one-hot A chunks into the TMEM ring ----
-      // Two warps per TMEM lane quadrant take alternate K chunks, so one
-      // warp's tcgen05.st / barrier latency overlaps the other's generation.
+      // kNPar warps per TMEM lane quadrant take K chunks round-robin, so one
+      // warp's tcgen05.st / barrier latency overlaps the others' generation.
       const int quad = warp & 3, par = warp >> 2;
       const uint32_t lane_base = (uint32_t)(quad * 32) << 16;
       // this warp's code words of a block (words of its chunks; others 0),
       // loaded one block ahead so the load latency hides behind the MMAs
-      constexpr int NCH = (MAXC + NW - 1) / NW;    // max chunks per block
-      constexpr int OW = ((NCH + 1) / 2) * NW;     // words of this warp's chunks
-      uint32_t nxt[OW];                            // own chunk oc = c/2: words oc*NW + h
+      constexpr int NCH = (MAXC + NW - 1) / NW;              // max chunks per block
+      constexpr int OW = ((NCH + kNPar - 1) / kNPar) * NW;   // words of this warp's chunks
+      uint32_t nxt[OW];  // own chunk oc = c/kNPar: words oc*NW + h
       auto load_block = [&](int64_t bi) {
         const int64_t p = (b0 + bi) * kPM + quad * 32 + lane;
         const bool live = bi < nblk && p < a.n;
 #pragma unroll
         for (int i = 0; i < OW; ++i) {
-          const int w = (2 * (i / NW) + par) * NW + (i % NW);
+          const int w = (kNPar * (i / NW) + par) * NW + (i % NW);
           nxt[i] = (live && w < nwords) ? __ldg(a.hcodes + (int64_t)w * a.stride + p) : 0u;
         }
       };
@@ -329,15 +353,21 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
 #pragma unroll
         for (int c = 0; c < NCH; ++c) {
           if (c >= nkc) break;
-          if ((c & 1) == par) {
+          if ((c % kNPar) == par) {
             if (round > 0) {
+              const long long t0 = clock64();
               mbar_wait(&aempty[slot], (round - 1) & 1u);
+              tw0 += clock64() - t0;
               asm volatile("tcgen05.fence::after_thread_sync;");
             }
 #pragma unroll
             for (int h = 0; h < NW; ++h) {  // 32 columns (8 subspaces) per store
               uint32_t r[32];
-              onehot8(cur[(c >> 1) * NW + h], live ? min(kKC, a.K - (c * NW + h) * kKC) : 0, r);
+              if (live && (c * NW + h + 1) * kKC <= a.K) {
+                onehot8_full(cur[(c / kNPar) * NW + h], r);
+              } else {
+                onehot8(cur[(c / kNPar) * NW + h], live ? min(kKC, a.K - (c * NW + h) * kKC) : 0, r);
+              }
               if (!(a.exp & 2)) TMEM_ST32(tmem_a + lane_base + (uint32_t)(slot * SC + 32 * h), r);
             }
             if (!(a.exp & 2)) asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
@@ -350,31 +380,33 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
           }
         }
       }
-    } else if (warp < 16) {
+    } else if (warp < kMmaWarp) {
       // ---- epilogue: accumulator -> u16 totals [query][point] ----
-      // Two warps per TMEM lane quadrant take alternate 32-column tiles.
+      // kEpiPar warps per TMEM lane quadrant take alternate 32-column tiles.
       // Per 32x32 tile (32 points of this warp's lanes x 32 queries): the
       // tile is transposed through shared memory (conflict-free u16 stores,
       // one query row per 64 B) and one lane hands it to the TMA engine as a
       // 2-D tensor store; two staging buffers per warp.
-      const int quad = warp & 3, half = (warp >> 2) & 1;
+      const int quad = warp & 3, half = (warp - kEpiWarp0) >> 2;
       const uint32_t lane_base = (uint32_t)(quad * 32) << 16;
-      uint16_t* stg = sStage + (warp - 8) * 2 * 1024;
+      uint16_t* stg = sStage + (warp - kEpiWarp0) * 2 * 1024;
       for (int64_t bi = 0; bi < nblk; ++bi) {
         const int64_t bt = blk_it + bi;
         const int buf = (int)(bt & 1);
+        const long long t0 = clock64();
         mbar_wait(&dfull[buf], (uint32_t)((bt >> 1) & 1));
+        tw0 += clock64() - t0;
         asm volatile("tcgen05.fence::after_thread_sync;");
         const int64_t pbase = (b0 + bi) * kPM + quad * 32;
         if (half * 32 >= NQ) {  // no tile of this block for this warp
           asm volatile("tcgen05.fence::before_thread_sync;");
           mbar_arrive(&dempty[buf]);
         }
-        for (int c = half * 32; c < NQ; c += 64) {
+        for (int c = half * 32; c < NQ; c += 32 * kEpiPar) {
           uint32_t r[32];
           TMEM_LD32(tmem + lane_base + (uint32_t)(buf * NQ + c), r);
           asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-          if (c + 64 >= NQ) {  // this warp's part of the accumulator read: release
+          if (c + 32 * kEpiPar >= NQ) {  // this warp's part of the accumulator read: release
             asm volatile("tcgen05.fence::before_thread_sync;");
             mbar_arrive(&dempty[buf]);
           }
@@ -443,12 +475,16 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
         const int64_t bt = blk_it + bi;
         const int buf = (int)(bt & 1);
         if (bt >= 2) {
+          const long long t0 = clock64();
           mbar_wait(&dempty[buf], (uint32_t)(((bt >> 1) - 1) & 1));
+          tw1 += clock64() - t0;
           asm volatile("tcgen05.fence::after_thread_sync;");
         }
         const uint32_t d = tmem + (uint32_t)(buf * NQ);
         for (int c = 0; c < nkc; ++c) {
+          const long long t0 = clock64();
           mbar_wait(&afull[slot], round & 1u);
+          tw0 += clock64() - t0;
           asm volatile("tcgen05.fence::after_thread_sync;");
           const int npair = min(KC, a.Kp - c * KC) / 2;  // Kp even
           const uint32_t ta = tmem_a + (uint32_t)(slot * SC);
@@ -456,10 +492,12 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
           // descriptor's (address >> 4) field
           const uint64_t bd = bdesc0 + (uint64_t)(c * KC * NQ);
           if (elect_one()) {
+            if (!(a.exp & 8)) {
             mma_ts(d, ta, bd, idesc, c > 0 ? 1u : 0u);
 #pragma unroll
             for (int m = 1; m < KC / 2; ++m)
               if (npair > m) mma_ts(d, ta + 8 * m, bd + (uint64_t)(2 * m * NQ), idesc, 1u);
+            }
             mma_commit(&aempty[slot]);
           }
           __syncwarp();
@@ -480,10 +518,13 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
         if (q0 + i < a.nq) a.cnt[(q0 + i) * a.nseg + seg_id] = sCnt[i];
     }
   }
-  if (!FILTER && warp >= 8 && warp < 16 && lane == 0)
+  if (!FILTER && warp >= kEpiWarp0 && warp < kMmaWarp && lane == 0)
     asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  if ((a.exp & 16) && lane == 0 && (blockIdx.x == 0 || blockIdx.x == 77))
+    printf("TCPROF cta=%d warp=%d total=%lld wait0=%lld wait1=%lld items=%lld\n", (int)blockIdx.x, warp,
+           clock64() - tstart, tw0, tw1, (long long)(it1 - it0));
   __syncthreads();
-  if (warp == 16) {
+  if (warp == kMmaWarp) {
     asm volatile("tcgen05.fence::after_thread_sync;");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
                  "r"(kTmemCols));
