@@ -202,6 +202,9 @@ int run_search(DeviceIndex& ix, const hs_query_batch& qb, int64_t nnz, int max_q
   const int64_t cpts = stage1_chunk_points();
   const int64_t m_s = std::min<int64_t>(
       ix.n, ceil_div(std::max<int64_t>(ev_s ? m_min : m_auto, 4 * sz.k1), cpts) * cpts);
+  // threshold from the exact sample top-k1 (full stage-1 kernels) instead of
+  // the sample's totals (dev / A-B knob)
+  const bool exact_sample = getenv_flag("HSB200_EXACT_SAMPLE");
   const bool use_fuse = use_tc && ix.K <= 256 && sz.k1 <= 4096 && ix.n >= 8 * m_s &&
                         (!sparse_part || (use_buckets && ix.pcodes != nullptr)) &&
                         !getenv_flag("HSB200_NO_FUSE");
@@ -284,6 +287,7 @@ int run_search(DeviceIndex& ix, const hs_query_batch& qb, int64_t nnz, int max_q
       // fused path
       uint16_t* tot_s;
       Cand* cand_s;
+      double* T;
       uint32_t* tlim;
       uint2* list;
       uint32_t* lcnt;
@@ -317,7 +321,8 @@ int run_search(DeviceIndex& ix, const hs_query_batch& qb, int64_t nnz, int max_q
     if (use_tc && !use_fuse) p.tot16 = a.template take<uint16_t>(QB * tc_ld);
     if (use_fuse) {
       p.tot_s = a.template take<uint16_t>(QB * ld_s);
-      p.cand_s = a.template take<Cand>(QB * sz.k1 + 1);
+      p.cand_s = exact_sample ? a.template take<Cand>(QB * sz.k1 + 1) : nullptr;
+      p.T = a.template take<double>(QB);
       p.tlim = a.template take<uint32_t>(QB);
       p.list = a.template take<uint2>(QB * nseg * Cf);
       p.lcnt = a.template take<uint32_t>(QB * nseg);
@@ -391,8 +396,10 @@ int run_search(DeviceIndex& ix, const hs_query_batch& qb, int64_t nnz, int max_q
     }
     const bool tc_chunk = use_tc && nqc >= kTcMinQueries;
     if (tc_chunk && use_fuse) {
-      // 1. exact top-k1 of the first m_s points -> threshold
+      // 1. u16 totals of the first m_s points -> threshold
       HS_CHECK(launch_lut16_tc(ix, luts, nqc, P.tot_s, ld_s, st, m_s));
+      ix.launches += 1;
+      if (exact_sample) {
       Stage1Plan ps = plan_stage1(ix, nqc, sz.k1, max_qnnz, S1_SELECT, m_s);
       ps.sparse = nnz > 0;
       HS_CHECK(launch_stage1(ix, qc, ps, lbeg, lend, qv, lidx, luts, btot, scl, off, s1out,
@@ -400,8 +407,13 @@ int run_search(DeviceIndex& ix, const hs_query_batch& qb, int64_t nnz, int max_q
                              ld_s));
       HS_CHECK(launch_select_topk(s1out, nqc, (int64_t)ps.ntiles * ps.out_per_tile, sz.k1,
                                   P.cand_s, st));
-      launch_tlim(P.cand_s, nqc, (int)sz.k1, btot, scl, off, P.tlim, st);
-      ix.launches += 4;
+      launch_tlim(P.cand_s, nqc, (int)sz.k1, btot, scl, off, P.tlim, P.T, st);
+      ix.launches += 3;
+      } else {
+        launch_sample_tlim(P.tot_s, ld_s, m_s, nqc, (int)sz.k1, nnz > 0 ? qc.sp_indptr : nullptr, qv,
+                           ix.post_wmin, ix.post_wmax, btot, scl, off, P.tlim, P.T, st);
+        ix.launches += 1;
+      }
       if (tm) tm->mark("sample");
       // 2. filtered tensor-core pass over every point
       HS_CHECK(launch_lut16_filter(ix, luts, nqc, P.tlim, P.list, P.lcnt, Cf, st));
@@ -413,7 +425,7 @@ int run_search(DeviceIndex& ix, const hs_query_batch& qb, int64_t nnz, int max_q
       lut16_filter_layout(ix, nqc, &nseg_c, &frac_c);
       HS_CHECK(launch_fuse_cands(ix, nqc, luts, btot, scl, off, P.list, P.lcnt, Cf, (int)nseg_c,
                                  sparse_part ? &sb : nullptr, P.bitmap, P.fout, Mf, P.fcnt,
-                                 P.fallback, P.cand_s, (int)sz.k1, st));
+                                 P.fallback, P.T, st));
       if (tm) tm->mark("fuse");
       HS_CHECK(launch_select_topk(P.fout, nqc, Mf, sz.k1, cand1, st, P.fcnt));
       ix.launches += 2;
@@ -623,6 +635,15 @@ int hs_index_create(const hs_index_desc* ds, int device, hs_index_t* out) {
       HS_CUDA(cudaMalloc(&tw, sizeof(float) * nnz_post));
       HS_CUDA(cudaMemcpy(tid, ds->post_ids, sizeof(uint32_t) * nnz_post, cudaMemcpyHostToDevice));
       HS_CUDA(cudaMemcpy(tw, ds->post_w, sizeof(float) * nnz_post, cudaMemcpyHostToDevice));
+      if (ix->d_dense > 0) {  // weight range: the filtered stage 1's sparse lower bound
+        float lo = ds->post_w[0], hi = ds->post_w[0];
+        for (int64_t i = 1; i < nnz_post; ++i) {
+          lo = std::min(lo, ds->post_w[i]);
+          hi = std::max(hi, ds->post_w[i]);
+        }
+        ix->post_wmin = lo;
+        ix->post_wmax = hi;
+      }
       // one pad posting: the stream copies 16-byte pairs and may read past the end
       HS_CHECK(dalloc(*ix, &ix->post, nnz_post + 1));
       HS_CUDA(cudaMemset(ix->post + nnz_post, 0xFF, sizeof(uint2)));

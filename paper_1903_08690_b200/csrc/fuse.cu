@@ -5,11 +5,15 @@
 // over all points (pipeline.py:192-203 then select_topk, pipeline.py:165-189).
 // Materialising every u16 total costs 2 bytes per (point, query) written and
 // read back; instead:
-//   1. sample: the exact top-k1 of the first `m` points (same kernels as the
-//      full stage 1) gives T[q] = its k1-th best score.  Any subset's k1-th
-//      best is <= the full k1-th best, so every true top-k1 point scores >= T.
-//   2. k_tlim: tlim[q] = the smallest u16 total whose dense-only score reaches
-//      T (the f64 ops are monotone in the total);
+//   1. sample: the u16 totals of the first `m` points give t_k, their k1-th
+//      largest total, and k_sample_tlim turns it into T[q], a lower bound on
+//      the k1-th best stage-1 score (k1 real points score at least
+//      dense(t_k) + a lower bound of the sparse part; see there).  Every true
+//      top-k1 point scores >= T.  (HSB200_EXACT_SAMPLE=1: T = the exact
+//      k1-th best of the sample, through the full stage-1 kernels — tighter,
+//      slower.)
+//   2. tlim[q] = the smallest u16 total whose dense-only score reaches T (the
+//      f64 ops are monotone in the total);
 //   3. the tensor-core pass in filter mode emits only (point, total) with
 //      total >= tlim[q] — every point without a sparse part that can still
 //      reach the top-k1;
@@ -32,20 +36,115 @@ __device__ __forceinline__ double dense_score(double btot, double scl, double of
   return __dadd_rn(__dadd_rn(btot, __dmul_rn(scl, (double)t)), off);
 }
 
-__global__ void k_tlim(const Cand* __restrict__ cand_s, int64_t nq, int k,
-                       const double* __restrict__ btot, const double* __restrict__ scl,
-                       const double* __restrict__ off, uint32_t* __restrict__ tlim) {
-  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (q >= nq) return;
-  const double T = cand_s[q * k + (k - 1)].s;  // -inf when the sample had < k points
-  const double b = btot[q], s = scl[q], o = off ? off[q] : 0.0;
+// smallest u16 total whose dense-only score reaches T (65536: none)
+__device__ uint32_t tlim_of(double T, double b, double s, double o) {
   int lo = 0, hi = 65536;
   while (lo < hi) {
     const int mid = (lo + hi) >> 1;
     if (dense_score(b, s, o, (uint32_t)mid) >= T) hi = mid;
     else lo = mid + 1;
   }
-  tlim[q] = (uint32_t)lo;
+  return (uint32_t)lo;
+}
+
+__global__ void k_tlim(const Cand* __restrict__ cand_s, int64_t nq, int k,
+                       const double* __restrict__ btot, const double* __restrict__ scl,
+                       const double* __restrict__ off, uint32_t* __restrict__ tlim,
+                       double* __restrict__ Tout) {
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= nq) return;
+  const double T = cand_s[q * k + (k - 1)].s;  // -inf when the sample had < k points
+  tlim[q] = tlim_of(T, btot[q], scl[q], off ? off[q] : 0.0);
+  Tout[q] = T;
+}
+
+// Threshold from the sample's u16 totals alone (no sample stage 1): t_k = the
+// k-th largest total among the first m points (two 8-bit radix passes with
+// per-warp shared-memory histograms).  Those k points are real points whose
+// stage-1 score is acc + dense >= dense(t_k) + lb, where lb <= every point's
+// sparse accumulator: sum over the query's dims of min(0, q*wmin, q*wmax)
+// (each posting product lies between q*wmin and q*wmax of the index's
+// weights; a point gets at most one product per dim).  So
+// T = dense(t_k) + lb is <= the k-th best stage-1 score over all points.  With
+// lb == 0 (non-negative products: acc >= +0 exactly, and fl(acc + d) >= d)
+// T = dense(t_k) exactly; otherwise it is lowered by a relative guard that
+// covers the f64 rounding of the sums.
+constexpr int kTlThreads = 256;
+__global__ void __launch_bounds__(kTlThreads) k_sample_tlim(
+    const uint16_t* __restrict__ tot_s, int64_t ld, int64_t m, int k,
+    const int64_t* __restrict__ qptr, const double* __restrict__ qv, double wmin, double wmax,
+    const double* __restrict__ btot, const double* __restrict__ scl,
+    const double* __restrict__ off, uint32_t* __restrict__ tlim, double* __restrict__ Tout) {
+  __shared__ uint32_t hist[kTlThreads / 32][256];
+  __shared__ uint32_t s_sum[256];
+  __shared__ double s_lb[kTlThreads / 32];
+  __shared__ int s_sel;
+  __shared__ uint32_t s_rem;
+  const int64_t q = blockIdx.x;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint16_t* t = tot_s + q * ld;
+  // sparse lower bound (query dims, any order: every term is <= 0)
+  double lb = 0.0;
+  if (qptr) {
+    for (int64_t j = qptr[q] + tid; j < qptr[q + 1]; j += kTlThreads) {
+      const double x = qv[j];
+      lb += fmin(0.0, fmin(x * wmin, x * wmax));
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) lb += __shfl_xor_sync(0xffffffffu, lb, o);
+  if (lane == 0) s_lb[warp] = lb;
+  uint32_t prefix = 0, rem = (uint32_t)k;
+  bool none = m < k;  // fewer sample points than k: every total passes
+  for (int pass = 0; pass < 2 && !none; ++pass) {
+    for (int i = tid; i < (kTlThreads / 32) * 256; i += kTlThreads) (&hist[0][0])[i] = 0u;
+    __syncthreads();
+    for (int64_t p = (int64_t)tid * 8; p < m; p += (int64_t)kTlThreads * 8) {
+      const uint4 v4 = *reinterpret_cast<const uint4*>(t + p);
+      const uint32_t w[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+      for (int h = 0; h < 8; ++h) {
+        if (p + h >= m) break;
+        const uint32_t v = (w[h >> 1] >> (16 * (h & 1))) & 0xFFFFu;
+        if (pass == 0) atomicAdd(&hist[warp][v >> 8], 1u);
+        else if ((v >> 8) == prefix) atomicAdd(&hist[warp][v & 0xFFu], 1u);
+      }
+    }
+    __syncthreads();
+    {
+      uint32_t c = 0;
+#pragma unroll
+      for (int w = 0; w < kTlThreads / 32; ++w) c += hist[w][tid];
+      s_sum[tid] = c;
+    }
+    __syncthreads();
+    if (tid == 0) {  // highest bin where the running count from the top reaches rem
+      uint32_t run = 0;
+      int b = 255;
+      for (; b > 0; --b) {
+        if (run + s_sum[b] >= rem) break;
+        run += s_sum[b];
+      }
+      s_sel = b;
+      s_rem = rem - run;
+    }
+    __syncthreads();
+    prefix = pass == 0 ? (uint32_t)s_sel : (prefix << 8) | (uint32_t)s_sel;
+    rem = s_rem;
+    __syncthreads();
+  }
+  if (tid == 0) {
+    double l = 0.0;
+    for (int w = 0; w < kTlThreads / 32; ++w) l += s_lb[w];
+    const double b = btot[q], s = scl[q], o = off ? off[q] : 0.0;
+    double T = -INFINITY;
+    if (!none) {
+      const double dk = dense_score(b, s, o, prefix);
+      T = l == 0.0 ? dk : (dk + l * (1.0 + 1e-6)) - 1e-9 * fabs(dk);
+    }
+    tlim[q] = tlim_of(T, b, s, o);
+    Tout[q] = T;
+  }
 }
 
 struct FuseArgs {
@@ -75,8 +174,7 @@ struct FuseArgs {
   int64_t M;
   uint32_t* out_cnt;            // [nq]
   int* fallback;                // [nq]
-  const Cand* cand_s;           // [nq][k1] sample top-k1: [k1-1] is the threshold
-  int k1;
+  const double* T;              // [nq] no top-k1 point scores below
 };
 
 template <bool SP>
@@ -114,7 +212,7 @@ __global__ void __launch_bounds__(kFuseThreads) k_fuse_cands(FuseArgs a) {
     s_cnt = 0;
   }
   const double b = a.btot[q], s = a.scl[q], o = a.off ? a.off[q] : 0.0;
-  const double T = a.cand_s[q * a.k1 + (a.k1 - 1)].s;  // no top-k1 point scores below
+  const double T = a.T[q];  // no top-k1 point scores below
   Cand* out = a.out + q * a.M;
   uint32_t* bm = SP ? a.bitmap + q * a.words : nullptr;
   const uint32_t* qb = SP ? a.boff + q * (int64_t)(a.nchunks + 1) : nullptr;
@@ -212,20 +310,28 @@ void launch_to_pcodes(const uint8_t* packed, int64_t n, int npairs, uint8_t* pc,
 }
 
 void launch_tlim(const Cand* cand_s, int64_t nq, int k, const double* btot, const double* scl,
-                 const double* off, uint32_t* tlim, cudaStream_t st) {
+                 const double* off, uint32_t* tlim, double* T, cudaStream_t st) {
   if (nq <= 0) return;
-  k_tlim<<<(unsigned)ceil_div(nq, 128), 128, 0, st>>>(cand_s, nq, k, btot, scl, off, tlim);
+  k_tlim<<<(unsigned)ceil_div(nq, 128), 128, 0, st>>>(cand_s, nq, k, btot, scl, off, tlim, T);
+}
+
+void launch_sample_tlim(const uint16_t* tot_s, int64_t ld, int64_t m, int64_t nq, int k,
+                        const int64_t* qptr, const double* qv, double wmin, double wmax,
+                        const double* btot, const double* scl, const double* off,
+                        uint32_t* tlim, double* T, cudaStream_t st) {
+  if (nq <= 0) return;
+  k_sample_tlim<<<(unsigned)nq, kTlThreads, 0, st>>>(tot_s, ld, m, k, qptr, qv, wmin, wmax, btot,
+                                                     scl, off, tlim, T);
 }
 
 int launch_fuse_cands(const DeviceIndex& ix, int64_t nq, const uint8_t* luts, const double* btot,
                       const double* scl, const double* off, const uint2* list,
                       const uint32_t* cnt, int64_t cap, int nseg, const SparseBuckets* sb,
                       uint32_t* bitmap, Cand* out, int64_t M, uint32_t* out_cnt, int* fallback,
-                      const Cand* cand_s, int k1, cudaStream_t st) {
+                      const double* T, cudaStream_t st) {
   if (nq <= 0) return HS_OK;
   FuseArgs a;
-  a.cand_s = cand_s;
-  a.k1 = k1;
+  a.T = T;
   a.n = ix.n;
   a.Kp = ix.Kp;
   a.npairs = ix.npairs;

@@ -23,6 +23,7 @@ struct DeviceIndex {
   uint32_t* post_dims = nullptr;  // [n_active]
   uint32_t* post_ptr = nullptr;   // [n_active+1] (nnz_post < 2^32)
   uint2* post = nullptr;          // [nnz_post] {id, __float_as_uint(w)}
+  double post_wmin = 0.0, post_wmax = 0.0;  // range of the posting weights
   // chunk skip tables of long lists: skip_row[list] = row index or -1;
   // row r holds, for every 4096-slot chunk c, the list-relative position of
   // the first posting with id >= 4096*c (nchunks+1 entries)
@@ -175,12 +176,16 @@ int launch_lut16_filter(const DeviceIndex& ix, const uint8_t* luts, int64_t nq,
 int64_t pcodes_row(int npairs);
 void launch_to_pcodes(const uint8_t* packed, int64_t n, int npairs, uint8_t* pc, cudaStream_t st);
 void launch_tlim(const Cand* cand_s, int64_t nq, int k, const double* btot, const double* scl,
-                 const double* off, uint32_t* tlim, cudaStream_t st);
+                 const double* off, uint32_t* tlim, double* T, cudaStream_t st);
+void launch_sample_tlim(const uint16_t* tot_s, int64_t ld, int64_t m, int64_t nq, int k,
+                        const int64_t* qptr, const double* qv, double wmin, double wmax,
+                        const double* btot, const double* scl, const double* off,
+                        uint32_t* tlim, double* T, cudaStream_t st);
 int launch_fuse_cands(const DeviceIndex& ix, int64_t nq, const uint8_t* luts, const double* btot,
                       const double* scl, const double* off, const uint2* list,
                       const uint32_t* cnt, int64_t cap, int nseg, const SparseBuckets* sb,
                       uint32_t* bitmap, Cand* out, int64_t M, uint32_t* out_cnt, int* fallback,
-                      const Cand* cand_s, int k1, cudaStream_t st);
+                      const double* T, cudaStream_t st);
 
 // select.cu
 // best k of each query's row in[q][0..m) (or [0..counts[q]) when counts is
