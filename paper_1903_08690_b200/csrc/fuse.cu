@@ -24,6 +24,8 @@
 //   5. the variable-length selection keeps the exact top-k1.
 // A query whose candidate list overflowed, or whose postings were not
 // bucketed, is flagged and rerun through the unfiltered stage 1.
+#include <cstdlib>
+
 #include "kernels.cuh"
 
 namespace hs {
@@ -150,7 +152,7 @@ __global__ void __launch_bounds__(kTlThreads) k_sample_tlim(
 struct FuseArgs {
   int64_t n;
   int Kp, npairs;
-  int64_t prow;                 // bytes per pcodes row (multiple of 4)
+  int64_t prow;                 // bytes per pcodes row (multiple of 16)
   const uint8_t* pcodes;        // [n][prow]
   const uint8_t* luts;          // [nq][Kp][16]
   const double* btot;
@@ -175,6 +177,7 @@ struct FuseArgs {
   uint32_t* out_cnt;            // [nq]
   int* fallback;                // [nq]
   const double* T;              // [nq] no top-k1 point scores below
+  int exp;                      // dev timing knob (HSB200_FUSE_EXP): 1 skip touched, 2 skip dense
 };
 
 template <bool SP>
@@ -225,53 +228,67 @@ __global__ void __launch_bounds__(kFuseThreads) k_fuse_cands(FuseArgs a) {
   }
   __syncthreads();
 
-  if (SP && E > 0) {
-    // touched points: the first entry of a point inside its chunk's bucket
-    // (entries ascend in dim there) sums the point's products in order
-    for (uint32_t e = tid; e < E; e += blockDim.x) {
-      int lo = 0, hi = a.nchunks;  // largest c with qb[c] <= e
-      while (hi - lo > 1) {
-        const int mid = (lo + hi) >> 1;
-        if (qb[mid] <= e) lo = mid;
-        else hi = mid;
-      }
-      const uint32_t s0 = qb[lo], s1 = qb[lo + 1];
-      const uint32_t sl = qs[e];
-      bool first = true;
-      for (uint32_t j = s0; j < e && first; ++j) first = qs[j] != sl;
-      if (!first) continue;
-      double acc = 0.0;
-      acc += qv[e];
-      for (uint32_t j = e + 1; j < s1; ++j)
-        if (qs[j] == sl) acc += qv[j];
-      atomicOr(bm + (sl >> 5), 1u << (sl & 31));
-      // the point's LUT16 total from its codes (exact integer sum)
-      const uint32_t* row = reinterpret_cast<const uint32_t*>(a.pcodes + (int64_t)sl * a.prow);
-      uint32_t t = 0;
-      for (int w = 0; w * 4 < a.npairs; ++w) {
-        const uint32_t v = __ldg(row + w);
+  if (SP && E > 0 && !(a.exp & 1)) {
+    // touched points: buckets hold one entry per point (k_bucket_aggregate:
+    // its products summed in the reference's ascending dim order), then
+    // empty entries
+    // four entries per thread per round: their code-row loads overlap
+    constexpr int U = 4;
+    for (uint32_t eb = 0; eb < E; eb += U * blockDim.x) {
+      uint32_t sl[U], t[U];
+      double acc[U];
+      const uint32_t* row[U];
 #pragma unroll
-        for (int bb = 0; bb < 4; ++bb) {
-          const int pair = w * 4 + bb;
-          if (pair < a.npairs) {
-            const uint32_t byte = (v >> (8 * bb)) & 0xFFu;
-            t += lut[(2 * pair) * 16 + (byte & 15u)];
-            t += lut[(2 * pair + 1) * 16 + (byte >> 4)];  // padding row of odd K is zero
+      for (int u = 0; u < U; ++u) {
+        const uint32_t e = eb + u * blockDim.x + tid;
+        sl[u] = e < E ? qs[e] : 0xFFFFFFFFu;
+        acc[u] = e < E ? qv[e] : 0.0;
+        t[u] = 0;
+        row[u] = reinterpret_cast<const uint32_t*>(
+            a.pcodes + (int64_t)(sl[u] == 0xFFFFFFFFu ? 0u : sl[u]) * a.prow);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (sl[u] != 0xFFFFFFFFu) atomicOr(bm + (sl[u] >> 5), 1u << (sl[u] & 31));
+      // the points' LUT16 totals from their codes (exact integer sums); rows
+      // are read 16 bytes (32 subspaces) at a time
+      for (int w = 0; w * 16 < a.npairs; ++w) {
+        uint4 v4[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) v4[u] = __ldg(reinterpret_cast<const uint4*>(row[u]) + w);
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+#pragma unroll
+          for (int bb = 0; bb < 4; ++bb) {
+            const int pair = w * 16 + h * 4 + bb;
+            if (pair < a.npairs) {
+#pragma unroll
+              for (int u = 0; u < U; ++u) {
+                const uint32_t word = h == 0 ? v4[u].x : h == 1 ? v4[u].y : h == 2 ? v4[u].z : v4[u].w;
+                const uint32_t byte = (word >> (8 * bb)) & 0xFFu;
+                t[u] += lut[(2 * pair) * 16 + (byte & 15u)];
+                t[u] += lut[(2 * pair + 1) * 16 + (byte >> 4)];  // padding row of odd K is zero
+              }
+            }
           }
         }
       }
-      Cand c;
-      c.s = __dadd_rn(acc, dense_score(b, s, o, t));
-      if (!(c.s >= T)) continue;  // below the sample threshold (still marked touched)
-      c.tie = __ldg(a.order + sl);
-      c.slot = sl;
-      out[atomicAdd(&s_cnt, 1u)] = c;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (sl[u] == 0xFFFFFFFFu) continue;
+        Cand c;
+        c.s = __dadd_rn(acc[u], dense_score(b, s, o, t[u]));
+        if (!(c.s >= T)) continue;  // below the sample threshold (still marked touched)
+        c.tie = __ldg(a.order + sl[u]);
+        c.slot = sl[u];
+        out[atomicAdd(&s_cnt, 1u)] = c;
+      }
     }
   }
   __syncthreads();
   // dense candidates without a sparse part
   const uint2* lst = a.list + q * a.nseg * a.cap;
-  for (uint32_t i = tid; i < nd; i += blockDim.x) {
+  for (uint32_t i = tid; i < ((a.exp & 2) ? 0u : nd); i += blockDim.x) {
     int lo = 0, hi = a.nseg;  // segment of flat index i: largest c with s_pre[c] <= i
     while (hi - lo > 1) {
       const int mid = (lo + hi) >> 1;
@@ -288,7 +305,10 @@ __global__ void __launch_bounds__(kFuseThreads) k_fuse_cands(FuseArgs a) {
   }
   __syncthreads();
   if (SP && E > 0)
-    for (uint32_t e = tid; e < E; e += blockDim.x) bm[qs[e] >> 5] = 0u;
+    for (uint32_t e = tid; e < E; e += blockDim.x) {
+      const uint32_t sl = qs[e];
+      if (sl != 0xFFFFFFFFu) bm[sl >> 5] = 0u;
+    }
   if (tid == 0) a.out_cnt[q] = s_cnt;
 }
 
@@ -302,7 +322,8 @@ __global__ void k_to_pcodes(const uint8_t* __restrict__ packed, int64_t n, int n
 
 }  // namespace
 
-int64_t pcodes_row(int npairs) { return ((int64_t)npairs + 3) / 4 * 4; }
+// rows padded to 16 bytes: one 16-byte load per 32 subspaces
+int64_t pcodes_row(int npairs) { return ((int64_t)npairs + 15) / 16 * 16; }
 
 void launch_to_pcodes(const uint8_t* packed, int64_t n, int npairs, uint8_t* pc, cudaStream_t st) {
   if (n <= 0) return;
@@ -332,6 +353,7 @@ int launch_fuse_cands(const DeviceIndex& ix, int64_t nq, const uint8_t* luts, co
   if (nq <= 0) return HS_OK;
   FuseArgs a;
   a.T = T;
+  a.exp = std::getenv("HSB200_FUSE_EXP") ? std::atoi(std::getenv("HSB200_FUSE_EXP")) : 0;
   a.n = ix.n;
   a.Kp = ix.Kp;
   a.npairs = ix.npairs;

@@ -81,6 +81,73 @@ __device__ double warp_row_dot(const int64_t* __restrict__ indptr,
   return sum;
 }
 
+// Query-dim hash table in shared memory (open addressing, linear probing):
+// hkey[h] = dim (0xFFFFFFFF empty), hval[h] = index into qval.  Size: a power
+// of two >= 2 * nnz, so probes stay short.
+__device__ __forceinline__ uint32_t dim_hash(uint32_t d, uint32_t mask) {
+  return (d * 0x9E3779B1u) >> 7 & mask;
+}
+
+__device__ __forceinline__ void hash_build(uint32_t* hkey, int* hval, int hsize,
+                                           const uint32_t* __restrict__ dims, int n) {
+  for (int i = threadIdx.x; i < hsize; i += blockDim.x) hkey[i] = 0xFFFFFFFFu;
+  __syncthreads();
+  const uint32_t mask = (uint32_t)hsize - 1u;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const uint32_t d = dims[i];
+    uint32_t h = dim_hash(d, mask);
+    for (;;) {
+      const uint32_t prev = atomicCAS(&hkey[h], 0xFFFFFFFFu, d);
+      if (prev == 0xFFFFFFFFu || prev == d) break;  // dims of a query are distinct
+      h = (h + 1u) & mask;
+    }
+    hval[h] = i;
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ int hash_find(const uint32_t* hkey, const int* hval, uint32_t mask,
+                                         uint32_t d) {
+  uint32_t h = dim_hash(d, mask);
+  for (;;) {
+    const uint32_t k = hkey[h];
+    if (k == d) return hval[h];
+    if (k == 0xFFFFFFFFu) return -1;
+    h = (h + 1u) & mask;
+  }
+}
+
+// warp_row_dot with the query dims looked up in the hash table
+__device__ double warp_row_dot_h(const int64_t* __restrict__ indptr,
+                                 const uint32_t* __restrict__ indices,
+                                 const float* __restrict__ data, int64_t row,
+                                 const uint32_t* hkey, const int* hval, uint32_t mask,
+                                 const double* __restrict__ qval) {
+  const int lane = threadIdx.x & 31;
+  const int64_t b = indptr[row], e = indptr[row + 1];
+  double sum = 0.0;
+  for (int64_t base = b; base < e; base += 32) {
+    const int64_t i = base + lane;
+    double prod = 0.0;
+    bool hit = false;
+    if (i < e) {
+      const int j = hash_find(hkey, hval, mask, __ldg(indices + i));
+      if (j >= 0) {
+        prod = __dmul_rn((double)__ldg(data + i), qval[j]);
+        hit = true;
+      }
+    }
+    unsigned ball = __ballot_sync(0xffffffffu, hit);
+    while (ball) {  // matches in column order, sequential from +0.0
+      const int src = __ffs(ball) - 1;
+      const double v = __shfl_sync(0xffffffffu, prod, src);
+      sum = __dadd_rn(sum, v);
+      ball &= ball - 1;
+    }
+  }
+  return sum;
+}
+
 __global__ void __launch_bounds__(kRrThreads) k_stage2(
     const Cand* __restrict__ cand1, int k1, int k2, int64_t d, const double* __restrict__ qw_all,
     const float* __restrict__ lo, const float* __restrict__ step,
@@ -125,7 +192,7 @@ __global__ void k_copy_prefix(const Cand* __restrict__ in, int k1, int k2, int64
 
 struct Stage3Args {
   const Cand* cand2;
-  int k2, kh, exact, P, max_qnnz;
+  int k2, kh, exact, P, max_qnnz, hsize;
   const int64_t* qptr;
   const uint32_t* qdims;
   const float* qvals;
@@ -154,6 +221,8 @@ __global__ void __launch_bounds__(kRrThreads) k_stage3(Stage3Args a) {
   double* qd = reinterpret_cast<double*>(buf + a.P);
   double* qval = qd + a.d;
   uint32_t* qdims = reinterpret_cast<uint32_t*>(qval + a.max_qnnz);
+  uint32_t* hkey = qdims + a.max_qnnz;
+  int* hval = reinterpret_cast<int*>(hkey + a.hsize);
   const int64_t q = blockIdx.x;
   const int64_t qb = a.qptr[q];
   const int nqz = (int)(a.qptr[q + 1] - qb);
@@ -166,41 +235,53 @@ __global__ void __launch_bounds__(kRrThreads) k_stage3(Stage3Args a) {
   if (a.exact)
     for (int64_t i = threadIdx.x; i < a.d; i += blockDim.x) qd[i] = a.qd_all[q * a.d + i];
   __syncthreads();
+  hash_build(hkey, hval, a.hsize, qdims, nqz);
+  const uint32_t hmask = (uint32_t)a.hsize - 1u;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nwarps = blockDim.x >> 5;
-  for (int c = warp; c < a.k2; c += nwarps) {
-    Cand e = a.cand2[q * a.k2 + c];
-    if (e.slot == 0xFFFFFFFFu) {
-      if (lane == 0) buf[c] = e;
-      continue;
-    }
-    double fin;
+  const int g = lane >> 2, lane4 = lane & 3;
+  const unsigned gmask = 0xFu << (lane & ~3);
+  // a warp takes 8 candidates at a time: the 8 quarter-warp groups evaluate
+  // their dense dots concurrently (the dgemv recipe needs 4 FMA chains), then
+  // the warp walks the 8 sparse rows one by one
+  for (int c0 = warp * 8; c0 < a.k2; c0 += nwarps * 8) {
+    const int c = c0 + g;
+    Cand e = c < a.k2 ? a.cand2[q * a.k2 + c] : worst_cand();
+    const bool live = c < a.k2 && e.slot != 0xFFFFFFFFu;
     if (a.exact) {
-      const int64_t id = e.tie;  // original id (within this index)
-      const float* row = a.ds_dense + id * a.d;
       double dense = 0.0;
-      if (a.d > 0) {
-        // 8 groups of 4 lanes each compute the same dot; group 0's result is used
-        auto elem = [&](int i) -> double { return (double)row[i]; };
-        dense = group4_dot_recipe(elem, qd, (int)a.d, lane & 3, 0xFu << (lane & ~3));
-        dense = __shfl_sync(0xffffffffu, dense, 0);
+      if (a.d > 0) {  // every group runs the recipe (converged shuffles); dead ones on row 0
+        const float* row = a.ds_dense + (live ? (int64_t)e.tie : 0) * a.d;
+        auto elem = [&](int i) -> double { return (double)__ldg(row + i); };
+        dense = group4_dot_recipe(elem, qd, (int)a.d, lane4, gmask);
       }
-      fin = dense;
-      if (nqz > 0) {
-        const double sp = warp_row_dot(a.ds_indptr, a.ds_indices, a.ds_data, id, qdims, qval, nqz);
-        fin = __dadd_rn(dense, sp);
+      if (live) e.s = dense;
+    }
+    if (c < a.k2 && lane4 == 0) buf[c] = e;
+    __syncwarp();
+    const int nc = min(8, a.k2 - c0);
+    for (int j = 0; j < nc; ++j) {
+      Cand ej = buf[c0 + j];
+      if (ej.slot == 0xFFFFFFFFu) continue;  // uniform across the warp
+      double fin;
+      if (a.exact) {
+        fin = ej.s;  // dense part
+        if (nqz > 0) {
+          const double sp = warp_row_dot_h(a.ds_indptr, a.ds_indices, a.ds_data, (int64_t)ej.tie,
+                                           hkey, hval, hmask, qval);
+          fin = __dadd_rn(fin, sp);
+        }
+      } else {
+        double rd = 0.0;
+        if (nqz > 0 && a.res_nnz > 0)
+          rd = warp_row_dot_h(a.res_indptr, a.res_indices, a.res_data, ej.slot, hkey, hval, hmask,
+                              qval);
+        fin = __dadd_rn(ej.s, __dmul_rn(rd, a.sparse_weight));
       }
-    } else {
-      double rd = 0.0;
-      if (nqz > 0 && a.res_nnz > 0)
-        rd = warp_row_dot(a.res_indptr, a.res_indices, a.res_data, e.slot, qdims, qval, nqz);
-      fin = __dadd_rn(e.s, __dmul_rn(rd, a.sparse_weight));
+      if (lane == 0) buf[c0 + j].s = fin;
     }
-    if (lane == 0) {
-      e.s = fin;
-      buf[c] = e;
-    }
+    __syncwarp();
   }
   for (int i = a.k2 + threadIdx.x; i < a.P; i += blockDim.x) buf[i] = worst_cand();
   __syncthreads();
@@ -295,6 +376,8 @@ void launch_stage3(const DeviceIndex& ix, const QueryView& q, const Cand* cand2,
   a.exact = exact;
   a.P = next_pow2(k2);
   a.max_qnnz = max_qnnz < 1 ? 1 : max_qnnz;
+  a.hsize = 64;
+  while (a.hsize < 2 * a.max_qnnz) a.hsize *= 2;
   a.qptr = q.sp_indptr;
   a.qdims = q.sp_dims;
   a.qvals = q.sp_vals;
@@ -313,8 +396,12 @@ void launch_stage3(const DeviceIndex& ix, const QueryView& q, const Cand* cand2,
   a.res_data = ix.res_data;
   a.out_ids = out_ids;
   a.out_scores = out_scores;
-  const size_t smem = sizeof(Cand) * a.P + sizeof(double) * (ix.d_dense + a.max_qnnz) +
-                      sizeof(uint32_t) * a.max_qnnz;
+  auto smem_of = [&](int hs) {
+    return sizeof(Cand) * a.P + sizeof(double) * (ix.d_dense + a.max_qnnz) +
+           sizeof(uint32_t) * a.max_qnnz + (sizeof(uint32_t) + sizeof(int)) * hs;
+  };
+  while (smem_of(a.hsize) > 227 * 1024 && a.hsize / 2 > a.max_qnnz) a.hsize /= 2;  // fuller table
+  const size_t smem = smem_of(a.hsize);
   cudaFuncSetAttribute(k_stage3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k_stage3<<<(unsigned)nq, kRrThreads, smem, st>>>(a);
 }

@@ -47,6 +47,7 @@ constexpr int kSmallPostings = 512;        // below this a chunk's postings skip
 constexpr int kRingBytes = 24 * 1024;  // posting ring (bulk-copy staging), default size
 constexpr int kPieceMax = 1024;        // postings per staged piece
 constexpr int kPieceBars = 32;         // mbarrier pairs = pieces in flight
+constexpr uint32_t kNoSlot = 0xFFFFFFFFu;  // empty bucket entry (after k_bucket_aggregate)
 
 struct Stage1Args {
   int64_t n;
@@ -723,31 +724,17 @@ __global__ void __launch_bounds__(WS ? kThreads + 32 : kThreads, 3) k_stage1(Sta
       const int64_t cg = cb / kChunk;
       const uint32_t e0 = __ldg(qboff + cg), e1 = __ldg(qboff + cg + 1);
       if (e1 > e0) {
-        // Entries are in ascending dim order within the chunk.  The first
-        // entry of each point sums all of that point's entries in that order
-        // (the reference's per-point summation order) and stores the total;
-        // every other point of the chunk keeps the zero.
+        // Entries are aggregated per point (k_bucket_aggregate: one sum per
+        // touched point, in the reference's per-point order), then kNoSlot
+        // (only in buckets that had repeated points).
         const uint32_t L = e1 - e0;
         for (int i = tid; i < kChunk; i += kThreads) s.acc[i] = 0.0;
-        const bool staged = L <= (uint32_t)kThreads;
-        if (staged && tid < (int)L) {
-          s.bslot[tid] = __ldg(qslots + e0 + tid);
-          s.bval[tid] = __ldg(qvals + e0 + tid);
-        }
         csync<WS>();
         for (uint32_t i = tid; i < L; i += kThreads) {
-          const uint32_t sl = staged ? s.bslot[i] : __ldg(qslots + e0 + i);
-          bool first = true;
-          for (uint32_t j = 0; j < i && first; ++j)
-            first = (staged ? s.bslot[j] : __ldg(qslots + e0 + j)) != sl;
-          if (!first) continue;
-          double sum = 0.0;
-          sum += staged ? s.bval[i] : __ldg(qvals + e0 + i);
-          for (uint32_t j = i + 1; j < L; ++j)
-            if ((staged ? s.bslot[j] : __ldg(qslots + e0 + j)) == sl)
-              sum += staged ? s.bval[j] : __ldg(qvals + e0 + j);
+          const uint32_t sl = __ldg(qslots + e0 + i);
+          if (sl == kNoSlot) break;  // the sums come first, then only kNoSlot
           HS_DCHECK(sl - (uint32_t)cb < (uint32_t)kChunk);
-          s.acc[acc_ix(sl - (uint32_t)cb)] = sum;
+          s.acc[acc_ix(sl - (uint32_t)cb)] = __ldg(qvals + e0 + i);
         }
         csync<WS>();
         nact = 1;
@@ -1256,6 +1243,108 @@ __global__ void __launch_bounds__(kBucketThreads) k_sparse_bucket(
   }
 }
 
+// Per-point aggregation of the buckets: one warp per (query, chunk) bucket.
+// A slot bitmap finds the buckets with repeated points (rare with pruned
+// lists; those without are left as they are).  A bucket with repeats is
+// stably sorted by slot in shared memory, each point's run summed in bucket
+// order — ascending dim, the reference's per-point order (sparse.py:277-282)
+// — from +0.0, and rewritten: the sums compacted to its front (ascending
+// slot), then kNoSlot entries.  Consumers read one entry per touched point.
+// Buckets hold <= 1024 entries (k_sparse_bucket streams queries with fuller
+// chunks).
+constexpr int kAggWarps = 4;
+constexpr int kAggMax = 1024;
+
+__global__ void __launch_bounds__(kAggWarps * 32) k_bucket_aggregate(
+    const int* __restrict__ mode, const uint32_t* __restrict__ boff, int nchunks, int64_t capq,
+    uint32_t* __restrict__ slots, double* __restrict__ vals) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int64_t q = blockIdx.x;
+  if (mode[q] != 1) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* val = reinterpret_cast<double*>(smem_raw) + warp * kAggMax;
+  uint32_t* slt = reinterpret_cast<uint32_t*>(smem_raw + sizeof(double) * kAggWarps * kAggMax) +
+                  warp * kAggMax;
+  uint32_t* seen = reinterpret_cast<uint32_t*>(smem_raw + (sizeof(double) + sizeof(uint32_t)) *
+                                                              kAggWarps * kAggMax) +
+                   warp * (kChunk / 32);  // bitmap of the chunk's 4096 slots
+  for (int i = lane; i < kChunk / 32; i += 32) seen[i] = 0u;
+  __syncwarp();
+  const uint32_t* qb = boff + q * (int64_t)(nchunks + 1);
+  uint32_t* qs = slots + q * capq;
+  double* qv = vals + q * capq;
+  for (int c = blockIdx.y * kAggWarps + warp; c < nchunks; c += gridDim.y * kAggWarps) {
+    const uint32_t b0 = qb[c];
+    const int L = (int)(qb[c + 1] - b0);
+    if (L <= 1) continue;
+    const uint32_t cbase = (uint32_t)c << 12;
+    // pass 1: any repeated point?  (bitmap of the slots seen, cleared after)
+    bool rep = false;
+    for (int i = lane; i < L; i += 32) {
+      const uint32_t ls = __ldg(qs + b0 + i) - cbase;
+      const uint32_t bit = 1u << (ls & 31);
+      rep |= (atomicOr(&seen[ls >> 5], bit) & bit) != 0u;
+    }
+    __syncwarp();
+    for (int i = lane; i < L; i += 32) seen[(__ldg(qs + b0 + i) - cbase) >> 5] = 0u;
+    __syncwarp();
+    if (!__any_sync(0xffffffffu, rep)) continue;
+    // pass 2 (buckets with repeats): stable sort by slot — key = local slot
+    // << 10 | entry index — so each point's entries form a run in bucket
+    // (= ascending dim) order; run heads sum their runs from +0.0
+    int P = 32;
+    while (P < L) P <<= 1;
+    for (int i = lane; i < P; i += 32) {
+      if (i < L) {
+        slt[i] = ((qs[b0 + i] - cbase) << 10) | (uint32_t)i;
+        val[i] = qv[b0 + i];
+      } else {
+        slt[i] = 0xFFFFFFFFu;
+      }
+    }
+    __syncwarp();
+    for (int kk = 2; kk <= P; kk <<= 1)
+      for (int j = kk >> 1; j > 0; j >>= 1) {
+        for (int i = lane; i < P; i += 32) {
+          const int ixj = i ^ j;
+          if (ixj > i) {
+            const uint32_t x = slt[i], y = slt[ixj];
+            if ((x > y) == ((i & kk) == 0)) {
+              slt[i] = y;
+              slt[ixj] = x;
+            }
+          }
+        }
+        __syncwarp();
+      }
+    uint32_t out = 0;
+    for (int r0 = 0; r0 < L; r0 += 32) {
+      const int r = r0 + lane;
+      bool head = false;
+      uint32_t ls = 0;
+      double sum = 0.0;
+      if (r < L) {
+        const uint32_t k = slt[r];
+        ls = k >> 10;
+        head = r == 0 || (slt[r - 1] >> 10) != ls;
+        if (head) {
+          sum += val[k & 1023u];
+          for (int t = r + 1; t < L && (slt[t] >> 10) == ls; ++t) sum += val[slt[t] & 1023u];
+        }
+      }
+      const unsigned hb = __ballot_sync(0xffffffffu, head);
+      if (head) {
+        const uint32_t pos = out + __popc(hb & ((1u << lane) - 1u));
+        qs[b0 + pos] = cbase + ls;
+        qv[b0 + pos] = sum;
+      }
+      out += __popc(hb);
+    }
+    for (uint32_t i = out + lane; i < (uint32_t)L; i += 32) qs[b0 + i] = kNoSlot;
+    __syncwarp();
+  }
+}
+
 // skip table of one long list: row[c] = #postings with id < 4096*c
 __global__ void k_skip_rows(const uint2* __restrict__ post, const uint32_t* __restrict__ ptr,
                             const int32_t* __restrict__ long_lists, int nchunks,
@@ -1338,6 +1427,15 @@ void launch_sparse_bucket(const DeviceIndex& ix, const QueryView& q, const uint3
   k_sparse_bucket<<<(unsigned)q.nq, kBucketThreads, smem, st>>>(
       q.sp_indptr, lbeg, lend, qv, ix.post, sb.nchunks, sb.capq, sb.mode, sb.boff, sb.slots,
       sb.vals);
+  const size_t asmem = ((sizeof(uint32_t) + sizeof(double)) * kAggMax + kChunk / 8) * kAggWarps;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_bucket_aggregate, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)asmem);
+    attr = true;
+  }
+  const int ys = (int)std::min<int64_t>(ceil_div(sb.nchunks, kAggWarps), 8);
+  k_bucket_aggregate<<<dim3((unsigned)q.nq, (unsigned)ys), kAggWarps * 32, asmem, st>>>(
+      sb.mode, sb.boff, sb.nchunks, sb.capq, sb.slots, sb.vals);
 }
 
 int64_t vertical_stride(int64_t n) {
