@@ -18,7 +18,12 @@ REPO = os.path.dirname(HERE)
 OBJ = os.path.join(REPO, "build", "obj_debug" if os.environ.get("HSB200_DEBUG", "") == "1"
                    else "obj")
 DEBUG = os.environ.get("HSB200_DEBUG", "") == "1"
-LIB_CUDA = os.path.join(HERE, "libhsb200_debug.so" if DEBUG else "libhsb200.so")
+# HSB200_LIB_TAG: dev A/B builds (libhsb200_<tag>.so, objects in build/obj_<tag>)
+TAG = os.environ.get("HSB200_LIB_TAG", "")
+if TAG:
+    OBJ = os.path.join(REPO, "build", "obj_" + TAG)
+LIB_CUDA = os.path.join(HERE, "libhsb200_debug.so" if DEBUG else
+                        ("libhsb200_%s.so" % TAG if TAG else "libhsb200.so"))
 LIB_HOST = os.path.join(HERE, "libhsbuild.so")
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -29,6 +34,7 @@ NVFLAGS = ["-O3", "-lineinfo", "-std=c++17", "--fmad=false", "-Xcompiler", "-fPI
            "-Xcompiler", "-O3", "-I", os.path.join(REPO, "include")]
 if DEBUG:
     NVFLAGS += ["-DHS_DEBUG"]
+NVFLAGS += os.environ.get("HSB200_EXTRA_NVFLAGS", "").split()
 
 
 def _sources(ext):

@@ -43,6 +43,9 @@ constexpr int kPPT = 16;                   // points per thread per chunk
 constexpr int kChunk = kThreads * kPPT;    // 4096 points
 constexpr int kOfferPer = 4;                       // offers per thread per insertion round
 constexpr int kOfferRound = kThreads * kOfferPer;  // worst-case offers per insertion round
+#ifndef KB0
+#define KB0 6
+#endif
 constexpr int kSmallPostings = 512;        // below this a chunk's postings skip the barriers
 constexpr int kRingBytes = 24 * 1024;  // posting ring (bulk-copy staging), default size
 constexpr int kPieceMax = 1024;        // postings per staged piece
@@ -182,6 +185,16 @@ static_assert(kChunk == kThreads * kPPT, "chunk = threads x points per thread");
 __device__ __forceinline__ int acc_ix(uint32_t local) {
   const uint32_t j = local & (kPPT - 1), t = local / kPPT;
   return (int)(j * kThreads + (t ^ j));
+}
+// accumulator index of a chunk-local slot (DM == 0: plain, see pt_local)
+template <int DM>
+__device__ __forceinline__ int aix(uint32_t local) {
+  return DM == 0 ? (int)local : acc_ix(local);
+}
+// owner thread of a chunk-local slot
+template <int DM>
+__device__ __forceinline__ uint32_t owner_of(uint32_t local) {
+  return DM == 0 ? (local & (kThreads - 1)) : (local / kPPT);
 }
 
 struct Smem {
@@ -643,6 +656,13 @@ __global__ void __launch_bounds__(WS ? kThreads + 32 : kThreads, 3) k_stage1(Sta
   for (int64_t cb = tile_lo; cb < tile_hi; cb += kChunk) {
     const int64_t ce = min(tile_hi, cb + (int64_t)kChunk);
     const int64_t p0 = cb + (int64_t)tid * kPPT;
+    // points of this thread: 16 consecutive (dense variants: the LUT16 scan's
+    // layout) or, sparse-only, strided by the block (then the accumulator
+    // is indexed by the plain chunk-local slot: conflict-free both for the
+    // posting stream's consecutive slots and for the owners' reads)
+    auto pt_local = [&](int j) -> uint32_t {
+      return DM == 0 ? (uint32_t)(j * kThreads + tid) : (uint32_t)(tid * kPPT + j);
+    };
     HS_DCHECK(cb >= tile_lo && ce <= a.n);
 
     // ---- dense: LUT16 scan of this thread's 16 points ----
@@ -734,7 +754,7 @@ __global__ void __launch_bounds__(WS ? kThreads + 32 : kThreads, 3) k_stage1(Sta
           const uint32_t sl = __ldg(qslots + e0 + i);
           if (sl == kNoSlot) break;  // the sums come first, then only kNoSlot
           HS_DCHECK(sl - (uint32_t)cb < (uint32_t)kChunk);
-          s.acc[acc_ix(sl - (uint32_t)cb)] = __ldg(qvals + e0 + i);
+          s.acc[aix<DM>(sl - (uint32_t)cb)] = __ldg(qvals + e0 + i);
         }
         csync<WS>();
         nact = 1;
@@ -776,8 +796,8 @@ __global__ void __launch_bounds__(WS ? kThreads + 32 : kThreads, 3) k_stage1(Sta
           const uint32_t g = pc.y + 2 * j;
           // halves outside [g0, ge) go to a scratch slot; f64(q)*f64(w) is
           // exact, so the fma rounds like the reference's separate add
-          double* a0 = g >= pc.z ? &s.acc[acc_ix(v.x - (uint32_t)cb)] : s.scratch;
-          double* a1 = g + 1 < pc.w ? &s.acc[acc_ix(v.z - (uint32_t)cb)] : s.scratch + 1;
+          double* a0 = g >= pc.z ? &s.acc[aix<DM>(v.x - (uint32_t)cb)] : s.scratch;
+          double* a1 = g + 1 < pc.w ? &s.acc[aix<DM>(v.z - (uint32_t)cb)] : s.scratch + 1;
           HS_DCHECK(g < pc.z || (v.x >= cb && v.x < ce));
           HS_DCHECK(g + 1 >= pc.w || (v.z >= cb && v.z < ce));
           *a0 = fma(qv, (double)__uint_as_float(v.y), *a0);
@@ -858,7 +878,7 @@ __global__ void __launch_bounds__(WS ? kThreads + 32 : kThreads, 3) k_stage1(Sta
         // loads) and adds only those landing on its own 16 points — per-point
         // order stays ascending in dim with no block barriers
   #pragma unroll
-        for (int j = 0; j < kPPT; ++j) s.acc[acc_ix(tid * kPPT + j)] = 0.0;
+        for (int j = 0; j < kPPT; ++j) s.acc[aix<DM>(pt_local(j))] = 0.0;
         for (int i = 0; i < nact; ++i) {
           const uint32_t b = s.abase[i], c = s.acnt[i];
           const double qv = s.dqv[s.alist[i]];
@@ -870,8 +890,8 @@ __global__ void __launch_bounds__(WS ? kThreads + 32 : kThreads, 3) k_stage1(Sta
 #pragma unroll
             for (int r = 0; r < 8; ++r) {
               const uint32_t local = pw[r].x - (uint32_t)cb;
-              if (pw[r].x != 0xFFFFFFFFu && (local >> 4) == (uint32_t)tid)
-                s.acc[acc_ix(local)] += qv * (double)__uint_as_float(pw[r].y);
+              if (pw[r].x != 0xFFFFFFFFu && owner_of<DM>(local) == (uint32_t)tid)
+                s.acc[aix<DM>(local)] += qv * (double)__uint_as_float(pw[r].y);
             }
           }
         }
@@ -909,22 +929,35 @@ __global__ void __launch_bounds__(WS ? kThreads + 32 : kThreads, 3) k_stage1(Sta
             if (cur[r].x == 0xFFFFFFFFu) continue;
             HS_DCHECK(cur[r].x >= cb && cur[r].x < ce);
             // f64(q) * f64(w) is exact, so contraction cannot change the sum
-            s.acc[acc_ix(cur[r].x - (uint32_t)cb)] += qv * (double)__uint_as_float(cur[r].y);
+            s.acc[aix<DM>(cur[r].x - (uint32_t)cb)] += qv * (double)__uint_as_float(cur[r].y);
           }
-          // long slices: the rest in batches of 8 loads in flight per thread
-          constexpr int kB = 8;
-          for (uint32_t j0 = kPre * kThreads; j0 < c; j0 += kB * kThreads) {
+          // long slices: the rest in batches of kB loads per thread, the next
+          // batch in flight while this one adds
+          constexpr int kB = DM == 0 ? KB0 : 4;  // (register budget of the dense variants)
+          if (c > (uint32_t)(kPre * kThreads)) {
             uint2 v[kB];
 #pragma unroll
             for (int r = 0; r < kB; ++r) {
-              const uint32_t j = j0 + tid + r * kThreads;
+              const uint32_t j = kPre * kThreads + tid + r * kThreads;
               v[r] = j < c ? __ldg(&a.post[b + j]) : make_uint2(0xFFFFFFFFu, 0u);
             }
+            for (uint32_t j0 = kPre * kThreads; j0 < c; j0 += kB * kThreads) {
+              uint2 w[kB];
 #pragma unroll
-            for (int r = 0; r < kB; ++r) {
-              if (v[r].x == 0xFFFFFFFFu) continue;
-              HS_DCHECK(v[r].x >= cb && v[r].x < ce);
-              s.acc[acc_ix(v[r].x - (uint32_t)cb)] += qv * (double)__uint_as_float(v[r].y);
+              for (int r = 0; r < kB; ++r) w[r] = v[r];
+              if (j0 + kB * kThreads < c) {
+#pragma unroll
+                for (int r = 0; r < kB; ++r) {
+                  const uint32_t j = j0 + kB * kThreads + tid + r * kThreads;
+                  v[r] = j < c ? __ldg(&a.post[b + j]) : make_uint2(0xFFFFFFFFu, 0u);
+                }
+              }
+#pragma unroll
+              for (int r = 0; r < kB; ++r) {
+                if (w[r].x == 0xFFFFFFFFu) continue;
+                HS_DCHECK(w[r].x >= cb && w[r].x < ce);
+                s.acc[aix<DM>(w[r].x - (uint32_t)cb)] += qv * (double)__uint_as_float(w[r].y);
+              }
             }
           }
           csync<WS>();
@@ -934,7 +967,7 @@ __global__ void __launch_bounds__(WS ? kThreads + 32 : kThreads, 3) k_stage1(Sta
 
     // ---- scores (recomputed where needed instead of held in 16 f64 registers) ----
     auto acc_of = [&](int j) -> double {
-      return (SP && nact > 0) ? s.acc[acc_ix(tid * kPPT + j)] : 0.0;
+      return (SP && nact > 0) ? s.acc[aix<DM>(pt_local(j))] : 0.0;
     };
     auto score_with = [&](int j, double acc) -> double {
       if (a.raw_dense) return __dadd_rn(btot, __dmul_rn(scl, (double)tot[j]));
@@ -949,9 +982,10 @@ __global__ void __launch_bounds__(WS ? kThreads + 32 : kThreads, 3) k_stage1(Sta
     if (a.mode == S1_DUMP) {
 #pragma unroll
       for (int j = 0; j < kPPT; ++j) {
-        if (p0 + j >= ce) continue;
-        a.dump[q * a.n + p0 + j] = score(j);
-        if (a.dump_tot) a.dump_tot[q * a.n + p0 + j] = tot[j];
+        const int64_t pt = cb + pt_local(j);
+        if (pt >= ce) continue;
+        a.dump[q * a.n + pt] = score(j);
+        if (a.dump_tot) a.dump_tot[q * a.n + pt] = tot[j];
       }
       csync<WS>();
       continue;
@@ -960,7 +994,7 @@ __global__ void __launch_bounds__(WS ? kThreads + 32 : kThreads, 3) k_stage1(Sta
       Cand* o = a.out + (q * a.ntiles + tile) * a.out_per_tile;
 #pragma unroll
       for (int j = 0; j < kPPT; ++j) {
-        const int64_t pt = p0 + j;
+        const int64_t pt = cb + pt_local(j);
         if (pt < ce) {
           Cand c;
           c.s = score(j);
@@ -989,7 +1023,7 @@ __global__ void __launch_bounds__(WS ? kThreads + 32 : kThreads, 3) k_stage1(Sta
       const Cand th = *s.th;
 #pragma unroll
       for (int j = 0; j < kPPT; ++j) {
-        const int64_t pt = p0 + j;
+        const int64_t pt = cb + pt_local(j);
         if (pt >= ce) continue;
         const double aj = acc_of(j);
         // integer pre-filter: no sparse part and a LUT total below tlim
@@ -1017,7 +1051,7 @@ __global__ void __launch_bounds__(WS ? kThreads + 32 : kThreads, 3) k_stage1(Sta
           if (!(mask >> j & 1)) continue;
           Cand c;
           c.s = score(j);
-          c.slot = (uint32_t)(p0 + j);
+          c.slot = (uint32_t)(cb + pt_local(j));
           c.tie = kTieUnset;
           s.buf[pos++] = c;
         }
@@ -1041,7 +1075,7 @@ __global__ void __launch_bounds__(WS ? kThreads + 32 : kThreads, 3) k_stage1(Sta
             const int jj = kOfferPer * r + j;
             const double sj = score(jj);
             bool pass = sj > th.s;
-            if (!pass && sj == th.s) pass = a.order[p0 + jj] < th.tie;
+            if (!pass && sj == th.s) pass = a.order[cb + pt_local(jj)] < th.tie;
             if (pass) m2 |= 1u << j;
           }
           m = m2;
@@ -1055,7 +1089,7 @@ __global__ void __launch_bounds__(WS ? kThreads + 32 : kThreads, 3) k_stage1(Sta
             const int jj = kOfferPer * r + j;
             Cand c;
             c.s = score(jj);
-            c.slot = (uint32_t)(p0 + jj);
+            c.slot = (uint32_t)(cb + pt_local(jj));
             c.tie = kTieUnset;
             s.buf[pos++] = c;
           }
