@@ -117,23 +117,37 @@ __device__ __forceinline__ int hash_find(const uint32_t* hkey, const int* hval, 
   }
 }
 
-// warp_row_dot with the query dims looked up in the hash table
-__device__ double warp_row_dot_h(const int64_t* __restrict__ indptr,
-                                 const uint32_t* __restrict__ indices,
-                                 const float* __restrict__ data, int64_t row,
-                                 const uint32_t* hkey, const int* hval, uint32_t mask,
-                                 const double* __restrict__ qval) {
+// warp_row_dot with the query dims looked up in the hash table; the row
+// bounds [b, e) are given.  Column indices and values of a 32-entry piece are
+// loaded together (one memory round trip per piece), the next piece's loads
+// issued before this one's lookups.
+__device__ double warp_row_dot_h(int64_t b, int64_t e, const uint32_t* __restrict__ indices,
+                                 const float* __restrict__ data, const uint32_t* hkey,
+                                 const int* hval, uint32_t mask, const double* __restrict__ qval) {
   const int lane = threadIdx.x & 31;
-  const int64_t b = indptr[row], e = indptr[row + 1];
   double sum = 0.0;
+  int64_t i = b + lane;
+  uint32_t ci = 0xFFFFFFFFu;
+  float cv = 0.f;
+  if (i < e) {
+    ci = __ldg(indices + i);
+    cv = __ldg(data + i);
+  }
   for (int64_t base = b; base < e; base += 32) {
-    const int64_t i = base + lane;
+    const uint32_t col = ci;
+    const float val = cv;
+    const bool live = base + lane < e;
+    i = base + 32 + lane;
+    if (i < e) {  // next piece in flight
+      ci = __ldg(indices + i);
+      cv = __ldg(data + i);
+    }
     double prod = 0.0;
     bool hit = false;
-    if (i < e) {
-      const int j = hash_find(hkey, hval, mask, __ldg(indices + i));
+    if (live) {
+      const int j = hash_find(hkey, hval, mask, col);
       if (j >= 0) {
-        prod = __dmul_rn((double)__ldg(data + i), qval[j]);
+        prod = __dmul_rn((double)val, qval[j]);
         hit = true;
       }
     }
@@ -261,22 +275,32 @@ __global__ void __launch_bounds__(kRrThreads) k_stage3(Stage3Args a) {
     if (c < a.k2 && lane4 == 0) buf[c] = e;
     __syncwarp();
     const int nc = min(8, a.k2 - c0);
+    // sparse row bounds of the 8 candidates, loaded in parallel (lanes 0-7)
+    const bool use_sp = nqz > 0 && (a.exact || a.res_nnz > 0);
+    const int64_t* rp = a.exact ? a.ds_indptr : a.res_indptr;
+    int64_t rb = 0, re = 0;
+    if (use_sp && lane < nc) {
+      const Cand el = buf[c0 + lane];
+      if (el.slot != 0xFFFFFFFFu) {
+        const int64_t row = a.exact ? (int64_t)el.tie : (int64_t)el.slot;
+        rb = __ldg(rp + row);
+        re = __ldg(rp + row + 1);
+      }
+    }
     for (int j = 0; j < nc; ++j) {
       Cand ej = buf[c0 + j];
+      const int64_t b0 = __shfl_sync(0xffffffffu, rb, j), e0 = __shfl_sync(0xffffffffu, re, j);
       if (ej.slot == 0xFFFFFFFFu) continue;  // uniform across the warp
       double fin;
       if (a.exact) {
         fin = ej.s;  // dense part
-        if (nqz > 0) {
-          const double sp = warp_row_dot_h(a.ds_indptr, a.ds_indices, a.ds_data, (int64_t)ej.tie,
-                                           hkey, hval, hmask, qval);
+        if (use_sp) {
+          const double sp = warp_row_dot_h(b0, e0, a.ds_indices, a.ds_data, hkey, hval, hmask, qval);
           fin = __dadd_rn(fin, sp);
         }
       } else {
         double rd = 0.0;
-        if (nqz > 0 && a.res_nnz > 0)
-          rd = warp_row_dot_h(a.res_indptr, a.res_indices, a.res_data, ej.slot, hkey, hval, hmask,
-                              qval);
+        if (use_sp) rd = warp_row_dot_h(b0, e0, a.res_indices, a.res_data, hkey, hval, hmask, qval);
         fin = __dadd_rn(ej.s, __dmul_rn(rd, a.sparse_weight));
       }
       if (lane == 0) buf[c0 + j].s = fin;
