@@ -176,3 +176,41 @@ def test_threshold_filtered_stage1_matches_unfiltered_and_oracle(name, n, nq, sa
         ids, sc, _ = O.search_topk(idx, *O.query_parts(qs, i), s["h"], **kw)
         assert fused[i].ids.tolist() == ids.tolist()
         np.testing.assert_allclose(fused[i].scores, sc, rtol=1e-9)
+
+
+@pytest.mark.parametrize("name,n,nq,top_t,negate", [
+    ("cfg2", 60_000, 160, 128, True),    # negative query values: sparse lower bound lb < 0
+    ("cfg1", 40_000, 150, None, False),  # unpruned lists: points repeat inside chunk buckets
+    ("cfg1", 40_000, 150, None, True),
+])
+def test_filtered_stage1_negative_values_and_repeats(name, n, nq, top_t, negate, monkeypatch):
+    """The totals-only sample threshold must stay a lower bound when products
+    are negative (lb < 0), and the per-point bucket aggregation must sum
+    repeated points in the reference's dim order; both checked against the
+    unfiltered scan, the exact-sample threshold and the oracle."""
+    ds, qs, cfg, idx = _scaled(name, n, nq, top_t=top_t)
+    if negate:
+        sp = qs.sparse.copy()
+        sp.data[::3] *= -1.0
+        qs = hs.HybridDataset(sp, qs.dense)
+    s = cfg.search
+    kw = dict(overfetch=s["overfetch"], retain=s["retain"],
+              exact_final_rerank=s["exact_final_rerank"])
+    monkeypatch.setenv("HSB200_FUSE_SAMPLE", "4096")
+    dev = hs.device_index(idx)
+    dev.set_timing(True)
+    fused = hs.search_batch(idx, qs, s["h"], **kw)
+    assert "fuse" in dev.kernel_times()
+    monkeypatch.setenv("HSB200_EXACT_SAMPLE", "1")
+    exact = hs.search_batch(idx, qs, s["h"], **kw)
+    monkeypatch.delenv("HSB200_EXACT_SAMPLE")
+    monkeypatch.setenv("HSB200_NO_FUSE", "1")
+    ref = hs.search_batch(idx, qs, s["h"], **kw)
+    for a, b, c in zip(fused, exact, ref):
+        assert a.ids.tolist() == c.ids.tolist()
+        assert b.ids.tolist() == c.ids.tolist()
+        assert a.scores.tolist() == c.scores.tolist()
+    for i in range(0, qs.n, max(1, qs.n // 5)):
+        ids, sc, _ = O.search_topk(idx, *O.query_parts(qs, i), s["h"], **kw)
+        assert fused[i].ids.tolist() == ids.tolist()
+        np.testing.assert_allclose(fused[i].scores, sc, rtol=1e-9)
