@@ -104,13 +104,16 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
 }
 
+// The suspend-time hint lets a waiting warp sleep until the phase completes
+// instead of re-polling: without it the waiting epilogue / MMA / producer
+// warps' retry loops took ~30% of the issue slots the producers need.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
       "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
-      "r"(parity)
+      "r"(parity), "r"(0x989680u)
       : "memory");
 }
 
@@ -187,7 +190,7 @@ struct TcArgs {
   int64_t cap;
   int nseg;                // segment stride (>= grid size)
   int exp;                 // dev profiling knobs (HSB200_TC_EXP: 1 epilogue drain only, 2 no TMEM
-                           // stores, 8 no MMAs, 16 per-warp wait cycles), results invalid when set
+                           // stores, 8 no MMAs, 16 unused; build with -DHS_TCPROF for per-warp wait cycles), results invalid when set
   uint32_t tmax;           // 255*K + 1: no total reaches it
   int64_t ngroups;
   int64_t nblocks;         // point blocks of 128
@@ -278,8 +281,15 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
   // range spans few groups.  Per group segment: load the group's tables into
   // shared memory, then stream its blocks through the pipeline.  Pipeline
   // counters run across segments so the barrier parities stay in step.
-  long long tw0 = 0, tw1 = 0, tw2 = 0;  // exp&16: cycles waiting (per warp role)
+#ifdef HS_TCPROF  // per-role wait cycles, printed for two CTAs (dev builds only)
+  long long tw0 = 0, tw1 = 0;
   const long long tstart = clock64();
+#define TC_T0() const long long t0 = clock64()
+#define TC_ACC(v) v += clock64() - t0
+#else
+#define TC_T0() (void)0
+#define TC_ACC(v) (void)0
+#endif
   int64_t blk_it = 0;
   int slot = 0;          // A ring position (producers and issuer walk it in step)
   uint32_t round = 0;    // completed passes over the ring
@@ -339,7 +349,10 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
 #pragma unroll
         for (int i = 0; i < OW; ++i) {
           const int w = (kNPar * (i / NW) + par) * NW + (i % NW);
-          nxt[i] = (live && w < nwords) ? __ldg(a.hcodes + (int64_t)w * a.stride + p) : 0u;
+          if (a.exp & 32)
+            nxt[i] = (uint32_t)(p * 2654435761u + w);
+          else
+            nxt[i] = (live && w < nwords) ? __ldg(a.hcodes + (int64_t)w * a.stride + p) : 0u;
         }
       };
       load_block(0);
@@ -355,9 +368,9 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
           if (c >= nkc) break;
           if ((c % kNPar) == par) {
             if (round > 0) {
-              const long long t0 = clock64();
+              TC_T0();
               mbar_wait(&aempty[slot], (round - 1) & 1u);
-              tw0 += clock64() - t0;
+              TC_ACC(tw0);
               asm volatile("tcgen05.fence::after_thread_sync;");
             }
 #pragma unroll
@@ -393,9 +406,9 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
       for (int64_t bi = 0; bi < nblk; ++bi) {
         const int64_t bt = blk_it + bi;
         const int buf = (int)(bt & 1);
-        const long long t0 = clock64();
+        TC_T0();
         mbar_wait(&dfull[buf], (uint32_t)((bt >> 1) & 1));
-        tw0 += clock64() - t0;
+        TC_ACC(tw0);
         asm volatile("tcgen05.fence::after_thread_sync;");
         const int64_t pbase = (b0 + bi) * kPM + quad * 32;
         if (half * 32 >= NQ) {  // no tile of this block for this warp
@@ -475,16 +488,16 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
         const int64_t bt = blk_it + bi;
         const int buf = (int)(bt & 1);
         if (bt >= 2) {
-          const long long t0 = clock64();
+          TC_T0();
           mbar_wait(&dempty[buf], (uint32_t)(((bt >> 1) - 1) & 1));
-          tw1 += clock64() - t0;
+          TC_ACC(tw1);
           asm volatile("tcgen05.fence::after_thread_sync;");
         }
         const uint32_t d = tmem + (uint32_t)(buf * NQ);
         for (int c = 0; c < nkc; ++c) {
-          const long long t0 = clock64();
+          TC_T0();
           mbar_wait(&afull[slot], round & 1u);
-          tw0 += clock64() - t0;
+          TC_ACC(tw0);
           asm volatile("tcgen05.fence::after_thread_sync;");
           const int npair = min(KC, a.Kp - c * KC) / 2;  // Kp even
           const uint32_t ta = tmem_a + (uint32_t)(slot * SC);
@@ -520,9 +533,11 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
   }
   if (!FILTER && warp >= kEpiWarp0 && warp < kMmaWarp && lane == 0)
     asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-  if ((a.exp & 16) && lane == 0 && (blockIdx.x == 0 || blockIdx.x == 77))
+#ifdef HS_TCPROF
+  if (lane == 0 && (blockIdx.x == 0 || blockIdx.x == 77))
     printf("TCPROF cta=%d warp=%d total=%lld wait0=%lld wait1=%lld items=%lld\n", (int)blockIdx.x, warp,
            clock64() - tstart, tw0, tw1, (long long)(it1 - it0));
+#endif
   __syncthreads();
   if (warp == kMmaWarp) {
     asm volatile("tcgen05.fence::after_thread_sync;");
@@ -626,8 +641,10 @@ int launch_tc(const DeviceIndex& ix, const uint8_t* luts, int64_t nq, int64_t n_
   a.Kp = ix.Kp;
   a.nq_grp = NQ;
   const int nw = (int)ceil_div(a.Kp, kKC);
-  const int KCsel = (nw > 8 && nw <= 16) ? 16 : 8;  // wide slots for the K<=128, N<=128 case
-  a.slots = std::min(8, (kTmemCols - 2 * NQ) / (4 * KCsel));
+  static const int kc_env = std::getenv("HSB200_TC_KC") ? std::atoi(std::getenv("HSB200_TC_KC")) : 0;
+  static const int slot_cap = std::getenv("HSB200_TC_SLOTS") ? std::atoi(std::getenv("HSB200_TC_SLOTS")) : 8;
+  const int KCsel = kc_env == 8 ? 8 : (nw > 8 && nw <= 16) ? 16 : 8;  // wide slots for K<=128
+  a.slots = std::min(slot_cap, (kTmemCols - 2 * NQ) / (4 * KCsel));
   a.hcodes = ix.hcodes;
   a.luts = luts;
   a.tot = tot;
@@ -649,9 +666,13 @@ int launch_tc(const DeviceIndex& ix, const uint8_t* luts, int64_t nq, int64_t n_
       (size_t)a.Kp * NQ * 16 + kStageBytes + (2 * a.slots + 4) * sizeof(uint64_t) + 16;
   void (*kern)(TcArgs, const CUtensorMap);
   if (filter)
-    kern = nw <= 8 ? k_lut16_tc<8, true, 8> : nw <= 16 ? k_lut16_tc<16, true, 16> : k_lut16_tc<33, true, 8>;
+    kern = nw <= 8 ? k_lut16_tc<8, true, 8>
+           : nw <= 16 ? (KCsel == 16 ? k_lut16_tc<16, true, 16> : k_lut16_tc<16, true, 8>)
+                      : k_lut16_tc<33, true, 8>;
   else
-    kern = nw <= 8 ? k_lut16_tc<8, false, 8> : nw <= 16 ? k_lut16_tc<16, false, 16> : k_lut16_tc<33, false, 8>;
+    kern = nw <= 8 ? k_lut16_tc<8, false, 8>
+           : nw <= 16 ? (KCsel == 16 ? k_lut16_tc<16, false, 16> : k_lut16_tc<16, false, 8>)
+                      : k_lut16_tc<33, false, 8>;
   HS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   CUtensorMap tmap;
   std::memset(&tmap, 0, sizeof(tmap));
