@@ -311,12 +311,46 @@ def search_batch(index, queries, h: int | None = None, threads: int = 1, device:
     scores = np.empty((q.nq, kh), dtype=np.float64)
     secs = np.zeros(3, dtype=np.float64)
     b = q.batch()
-    nat.check(nat.lib().hs_search_batch(dev.handle, ctypes.byref(b), ctypes.byref(p),
-                                        nat.ptr(ids), nat.ptr(scores), nat.ptr(secs)))
+    call = lambda: nat.lib().hs_search_batch(dev.handle, ctypes.byref(b), ctypes.byref(p),  # noqa: E731
+                                             nat.ptr(ids), nat.ptr(scores), nat.ptr(secs))
+    if q.nq < 64:
+        nat.check(call())
+        per_q = (secs / q.nq).tolist()
+        return [SearchResult(i_row, s_row, StageStats([k1, k2, kh], per_q.copy()))
+                for i_row, s_row in zip(list(ids), list(scores))]
+    # Large batches: the C call (which releases the GIL) runs on a worker
+    # thread while this thread builds the result objects around row views of
+    # the output arrays; the rows are filled when the call returns.
+    started = threading.Event()
+
+    def run():
+        started.set()  # the ctypes call below releases the GIL
+        nat.check(call())  # (hs_last_error is thread-local: check on this thread)
+
+    fut = _worker().submit(run)
+    started.wait()  # blocks (GIL released) until the worker is about to call in
+    stats = [StageStats([k1, k2, kh], [0.0, 0.0, 0.0]) for _ in range(q.nq)]
+    res = [SearchResult(i_row, s_row, st) for i_row, s_row, st in zip(list(ids), list(scores), stats)]
+    fut.result()
     per_q = (secs / q.nq).tolist()
-    # one row view per query (list() of a 2-D array is the cheapest way to get them)
-    return [SearchResult(i_row, s_row, StageStats([k1, k2, kh], per_q.copy()))
-            for i_row, s_row in zip(list(ids), list(scores))]
+    for st in stats:
+        st.seconds[:] = per_q
+    return res
+
+
+_WORKER = None
+_WORKER_LOCK = threading.Lock()
+
+
+def _worker():
+    global _WORKER
+    if _WORKER is None:
+        with _WORKER_LOCK:
+            if _WORKER is None:
+                import concurrent.futures as cf
+
+                _WORKER = cf.ThreadPoolExecutor(max_workers=4, thread_name_prefix="hsb200")
+    return _WORKER
 
 
 def search_topk(index, query, h: int | None = None, *, overfetch=None, retain=None,
