@@ -66,6 +66,9 @@ void free_device_arrays(DeviceIndex* ix) {
     if (p) cudaFree(p);
   if (ix->io_host) cudaFreeHost(ix->io_host);
   if (ix->stream) cudaStreamDestroy(ix->stream);
+  if (ix->aux) cudaStreamDestroy(ix->aux);
+  if (ix->ev_fork) cudaEventDestroy(ix->ev_fork);
+  if (ix->ev_join) cudaEventDestroy(ix->ev_join);
 }
 
 int ensure_scratch(DeviceIndex& ix, size_t bytes) {
@@ -189,6 +192,10 @@ int run_search(DeviceIndex& ix, const hs_query_batch& qb, int64_t nnz, int max_q
                       !getenv_flag("HSB200_NO_TC");
   const bool use_buckets = nnz > 0 && ix.nnz_post > 0 && !getenv_flag("HSB200_NO_BUCKETS");
   const bool sparse_part = nnz > 0 && ix.nnz_post > 0;
+  // bucketing overlapped with the dense chain on the aux stream (not while
+  // timing: the per-kernel breakdown needs the serial order)
+  const bool overlap = use_buckets && ix.aux != nullptr && !(tm && tm->on) &&
+                       !getenv_flag("HSB200_NO_OVERLAP");
   // sample size of the threshold pass and capacity of the filtered lists
   // (HSB200_FUSE_SAMPLE / HSB200_FUSE_CAP: test knobs that shrink the sample
   // and the list capacity so small indices exercise the filter and fallback)
@@ -388,18 +395,35 @@ int run_search(DeviceIndex& ix, const hs_query_batch& qb, int64_t nnz, int max_q
       ix.launches += 1;
       if (tm) tm->mark("lut_build");
     }
+    bool sb_pending = false;  // bucketing in flight on the aux stream
     if (use_buckets) {
-      launch_sparse_bucket(ix, qc, lbeg, lend, qv, sb, st);
+      if (overlap) {  // fork: aux waits for everything issued so far on st
+        HS_CUDA(cudaEventRecord(ix.ev_fork, st));
+        HS_CUDA(cudaStreamWaitEvent(ix.aux, ix.ev_fork, 0));
+        launch_sparse_bucket(ix, qc, lbeg, lend, qv, sb, ix.aux);
+        HS_CUDA(cudaEventRecord(ix.ev_join, ix.aux));
+        sb_pending = true;
+      } else {
+        launch_sparse_bucket(ix, qc, lbeg, lend, qv, sb, st);
+      }
       HS_CUDA(cudaGetLastError());
       ix.launches += 1;
       if (tm) tm->mark("sparse_bucket");
     }
+    auto join_sb = [&]() -> int {  // before the first consumer of the buckets
+      if (sb_pending) {
+        HS_CUDA(cudaStreamWaitEvent(st, ix.ev_join, 0));
+        sb_pending = false;
+      }
+      return HS_OK;
+    };
     const bool tc_chunk = use_tc && nqc >= kTcMinQueries;
     if (tc_chunk && use_fuse) {
       // 1. u16 totals of the first m_s points -> threshold
       HS_CHECK(launch_lut16_tc(ix, luts, nqc, P.tot_s, ld_s, st, m_s));
       ix.launches += 1;
       if (exact_sample) {
+      HS_CHECK(join_sb());
       Stage1Plan ps = plan_stage1(ix, nqc, sz.k1, max_qnnz, S1_SELECT, m_s);
       ps.sparse = nnz > 0;
       HS_CHECK(launch_stage1(ix, qc, ps, lbeg, lend, qv, lidx, luts, btot, scl, off, s1out,
@@ -423,6 +447,7 @@ int run_search(DeviceIndex& ix, const hs_query_batch& qb, int64_t nnz, int max_q
       int64_t nseg_c = 0;
       double frac_c = 1.0;
       lut16_filter_layout(ix, nqc, &nseg_c, &frac_c);
+      HS_CHECK(join_sb());
       HS_CHECK(launch_fuse_cands(ix, nqc, luts, btot, scl, off, P.list, P.lcnt, Cf, (int)nseg_c,
                                  sparse_part ? &sb : nullptr, P.bitmap, P.fout, Mf, P.fcnt,
                                  P.fallback, P.T, st));
@@ -446,6 +471,7 @@ int run_search(DeviceIndex& ix, const hs_query_batch& qb, int64_t nnz, int max_q
         if (tm) tm->mark("lut16_tc");
       }
       ix.launches += 2;  // stage1, merge
+      HS_CHECK(join_sb());
       HS_CHECK(launch_stage1(ix, qc, pc, lbeg, lend, qv, lidx, luts, btot, scl, off, s1out,
                              nullptr, st, nullptr, false, use_buckets ? &sb : nullptr,
                              tc_chunk ? tot16 : nullptr, tc_ld));
@@ -454,6 +480,7 @@ int run_search(DeviceIndex& ix, const hs_query_batch& qb, int64_t nnz, int max_q
                                   cand1, st));
       if (tm) tm->mark("merge");
     }
+    HS_CHECK(join_sb());
     ix.launches += 2;  // stage2, stage3
     launch_stage2(ix, cand1, nqc, (int)sz.k1, (int)sz.k2, qw, cand2, st);
     HS_CUDA(cudaGetLastError());
@@ -607,6 +634,9 @@ int hs_index_create(const hs_index_desc* ds, int device, hs_index_t* out) {
   ix->sparse_weight = ds->sparse_weight;
   ix->dense_weight = ds->dense_weight;
   HS_CUDA(cudaStreamCreateWithFlags(&ix->stream, cudaStreamNonBlocking));
+  HS_CUDA(cudaStreamCreateWithFlags(&ix->aux, cudaStreamNonBlocking));
+  HS_CUDA(cudaEventCreateWithFlags(&ix->ev_fork, cudaEventDisableTiming));
+  HS_CUDA(cudaEventCreateWithFlags(&ix->ev_join, cudaEventDisableTiming));
   const int64_t n = ds->n;
   const int T = 256;
 

@@ -63,6 +63,10 @@ struct DeviceIndex {
 
   int64_t bytes = 0;
   cudaStream_t stream = nullptr;
+  // second stream + fork/join events: the sparse bucketing of a query chunk
+  // runs concurrently with its LUT build and sample pass
+  cudaStream_t aux = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   std::mutex mu;
 
   // scratch arena (grown on demand, owned by the handle)
