@@ -43,8 +43,11 @@ constexpr int kPPT = 16;                   // points per thread per chunk
 constexpr int kChunk = kThreads * kPPT;    // 4096 points
 constexpr int kOfferPer = 4;                       // offers per thread per insertion round
 constexpr int kOfferRound = kThreads * kOfferPer;  // worst-case offers per insertion round
+#ifndef MINB0
+#define MINB0 4
+#endif
 #ifndef KB0
-#define KB0 6
+#define KB0 4
 #endif
 constexpr int kSmallPostings = 512;        // below this a chunk's postings skip the barriers
 constexpr int kRingBytes = 24 * 1024;  // posting ring (bulk-copy staging), default size
@@ -517,7 +520,7 @@ __device__ __noinline__ void produce_postings(Smem& s, const Stage1Args& a, int 
 // SP: the query batch has postings to stream (else the sparse phase is elided);
 // WS: warp-specialised posting stream (a 9th, producer warp; see produce_postings).
 template <int DM, bool SP, bool WS>
-__global__ void __launch_bounds__(WS ? kThreads + 32 : kThreads, 3) k_stage1(Stage1Args a) {
+__global__ void __launch_bounds__(WS ? kThreads + 32 : kThreads, DM == 0 ? MINB0 : 3) k_stage1(Stage1Args a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int64_t q = blockIdx.x;
   const int tile = blockIdx.y;
