@@ -740,7 +740,14 @@ int hs_index_create(const hs_index_desc* ds, int device, hs_index_t* out) {
     ix->has_wh = ds->has_whitening;
     if (ds->has_whitening) {
       HS_CHECK(dupload(*ix, &ix->wh_mean, ds->wh_mean, ds->d_dense));
-      HS_CHECK(dupload(*ix, &ix->wh_inv_t, ds->wh_inverse_t, (size_t)ds->d_dense * ds->d_dense));
+      // stored transposed: thread r of the whitening GEMV reads column r, so a
+      // warp's loads of one k are consecutive (the row-major copy made every
+      // load instruction touch 32 rows)
+      const int64_t dd = ds->d_dense;
+      std::vector<double> tr((size_t)dd * dd);
+      for (int64_t r = 0; r < dd; ++r)
+        for (int64_t c = 0; c < dd; ++c) tr[(size_t)c * dd + r] = ds->wh_inverse_t[(size_t)r * dd + c];
+      HS_CHECK(dupload(*ix, &ix->wh_inv_t, tr.data(), (size_t)dd * dd));
     }
   }
   // raw dataset

@@ -51,7 +51,7 @@ struct DeviceIndex {
   float *sq_lo = nullptr, *sq_step = nullptr;
   uint8_t* sq_codes = nullptr;  // [n][d_dense]
   int has_wh = 0;
-  double *wh_mean = nullptr, *wh_inv_t = nullptr;
+  double *wh_mean = nullptr, *wh_inv_t = nullptr;  // wh_inv_t stored transposed ([col][row])
 
   // raw dataset (original order) for exact rerank / ground truth
   int has_ds = 0;

@@ -96,7 +96,8 @@ __global__ void __launch_bounds__(kLutThreads) k_lut_build(
   __syncthreads();
   // qw = qd @ inverse_t.T ; offset = qd @ mean  (pipeline.py:220-223)
   if (has_wh) {
-    for (int64_t r = tid; r < d; r += blockDim.x) qw[r] = dot_recipe(inv_t + r * d, qd, (int)d);
+    // inv_t is stored transposed: element (r, c) at inv_t[c * d + r]
+    for (int64_t r = tid; r < d; r += blockDim.x) qw[r] = dot_recipe(inv_t + r, qd, (int)d, (int)d);
     if (tid == 0) offset[q] = dot_recipe(qd, mean, (int)d);
   } else {
     for (int64_t i = tid; i < d; i += blockDim.x) qw[i] = qd[i];
