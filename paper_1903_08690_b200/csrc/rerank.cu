@@ -169,8 +169,14 @@ __global__ void __launch_bounds__(kRrThreads) k_stage2(
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Cand* buf = reinterpret_cast<Cand*>(smem_raw);
   double* qw = reinterpret_cast<double*>(buf + P);
+  double* slo = qw + d;     // decode affine in f64, shared by the candidates
+  double* sstep = slo + d;
   const int64_t q = blockIdx.x;
-  for (int64_t i = threadIdx.x; i < d; i += blockDim.x) qw[i] = qw_all[q * d + i];
+  for (int64_t i = threadIdx.x; i < d; i += blockDim.x) {
+    qw[i] = qw_all[q * d + i];
+    slo[i] = (double)lo[i];
+    sstep[i] = (double)step[i];
+  }
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const int lane4 = lane & 3;
@@ -184,9 +190,31 @@ __global__ void __launch_bounds__(kRrThreads) k_stage2(
     if (c < k1 && e.slot != 0xFFFFFFFFu) {
       const uint8_t* row = codes + (int64_t)e.slot * d;
       auto elem = [&](int i) -> double {
-        return __dadd_rn((double)lo[i], __dmul_rn((double)step[i], (double)row[i] + 0.5));
+        return __dadd_rn(slo[i], __dmul_rn(sstep[i], (double)row[i] + 0.5));
       };
-      const double dot = group4_dot_recipe(elem, qw, (int)d, lane4, gmask);
+      double dot;
+      if ((d & 15) == 0) {
+        // 16 codes per load (each group's 4 lanes read the same 16 bytes);
+        // lane j's FMA chain still runs over elements j, j+4, ... in order
+        const uint4* r4 = reinterpret_cast<const uint4*>(row);
+        double L = 0.0;
+        for (int i0 = 0; i0 < (int)d; i0 += 16) {
+          const uint4 w = __ldg(r4 + (i0 >> 4));
+          const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const int i = i0 + 4 * t + lane4;
+            const double code = (double)((ws[t] >> (8 * lane4)) & 0xFFu);
+            L = fma(__dadd_rn(slo[i], __dmul_rn(sstep[i], code + 0.5)), qw[i], L);
+          }
+        }
+        const int gb = lane & ~3;
+        const double L0 = __shfl_sync(gmask, L, gb + 0), L1 = __shfl_sync(gmask, L, gb + 1);
+        const double L2 = __shfl_sync(gmask, L, gb + 2), L3 = __shfl_sync(gmask, L, gb + 3);
+        dot = (L0 + L2) + (L1 + L3);
+      } else {
+        dot = group4_dot_recipe(elem, qw, (int)d, lane4, gmask);
+      }
       e.s = __dadd_rn(e.s, dot);  // scores1[cand1] + residual.dot  (pipeline.py:259-260)
     }
     if (c < k1 && lane4 == 0) buf[c] = e;
@@ -383,7 +411,7 @@ void launch_stage2(const DeviceIndex& ix, const Cand* cand1, int64_t nq, int k1,
     return;
   }
   const int P = next_pow2(k1);
-  const size_t smem = sizeof(Cand) * P + sizeof(double) * ix.d_dense;
+  const size_t smem = sizeof(Cand) * P + 3 * sizeof(double) * ix.d_dense;
   cudaFuncSetAttribute(k_stage2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k_stage2<<<(unsigned)nq, kRrThreads, smem, st>>>(cand1, k1, k2, ix.d_dense, qw, ix.sq_lo,
                                                    ix.sq_step, ix.sq_codes, cand2, P);
