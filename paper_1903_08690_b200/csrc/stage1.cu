@@ -1289,7 +1289,7 @@ __global__ void __launch_bounds__(kBucketThreads) k_sparse_bucket(
 // slot), then kNoSlot entries.  Consumers read one entry per touched point.
 // Buckets hold <= 1024 entries (k_sparse_bucket streams queries with fuller
 // chunks).
-constexpr int kAggWarps = 4;
+constexpr int kAggWarps = 8;
 constexpr int kAggMax = 1024;
 
 __global__ void __launch_bounds__(kAggWarps * 32) k_bucket_aggregate(
@@ -1299,14 +1299,15 @@ __global__ void __launch_bounds__(kAggWarps * 32) k_bucket_aggregate(
   const int64_t q = blockIdx.x;
   if (mode[q] != 1) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double* val = reinterpret_cast<double*>(smem_raw) + warp * kAggMax;
-  uint32_t* slt = reinterpret_cast<uint32_t*>(smem_raw + sizeof(double) * kAggWarps * kAggMax) +
-                  warp * kAggMax;
-  uint32_t* seen = reinterpret_cast<uint32_t*>(smem_raw + (sizeof(double) + sizeof(uint32_t)) *
-                                                              kAggWarps * kAggMax) +
-                   warp * (kChunk / 32);  // bitmap of the chunk's 4096 slots
+  // one sort staging area per CTA (buckets with repeats are rare), taken
+  // under a shared-memory lock; a 4096-bit slot bitmap per warp
+  double* val = reinterpret_cast<double*>(smem_raw);
+  uint32_t* slt = reinterpret_cast<uint32_t*>(smem_raw + sizeof(double) * kAggMax);
+  uint32_t* seen = slt + kAggMax + warp * (kChunk / 32);
+  int* lock = reinterpret_cast<int*>(slt + kAggMax + kAggWarps * (kChunk / 32));
+  if (threadIdx.x == 0) *lock = 0;
   for (int i = lane; i < kChunk / 32; i += 32) seen[i] = 0u;
-  __syncwarp();
+  __syncthreads();
   const uint32_t* qb = boff + q * (int64_t)(nchunks + 1);
   uint32_t* qs = slots + q * capq;
   double* qv = vals + q * capq;
@@ -1326,6 +1327,9 @@ __global__ void __launch_bounds__(kAggWarps * 32) k_bucket_aggregate(
     for (int i = lane; i < L; i += 32) seen[(__ldg(qs + b0 + i) - cbase) >> 5] = 0u;
     __syncwarp();
     if (!__any_sync(0xffffffffu, rep)) continue;
+    if (lane == 0)
+      while (atomicCAS(lock, 0, 1) != 0) __nanosleep(64);
+    __syncwarp();
     // pass 2 (buckets with repeats): stable sort by slot — key = local slot
     // << 10 | entry index — so each point's entries form a run in bucket
     // (= ascending dim) order; run heads sum their runs from +0.0
@@ -1379,6 +1383,7 @@ __global__ void __launch_bounds__(kAggWarps * 32) k_bucket_aggregate(
     }
     for (uint32_t i = out + lane; i < (uint32_t)L; i += 32) qs[b0 + i] = kNoSlot;
     __syncwarp();
+    if (lane == 0) atomicExch(lock, 0);
   }
 }
 
@@ -1464,7 +1469,7 @@ void launch_sparse_bucket(const DeviceIndex& ix, const QueryView& q, const uint3
   k_sparse_bucket<<<(unsigned)q.nq, kBucketThreads, smem, st>>>(
       q.sp_indptr, lbeg, lend, qv, ix.post, sb.nchunks, sb.capq, sb.mode, sb.boff, sb.slots,
       sb.vals);
-  const size_t asmem = ((sizeof(uint32_t) + sizeof(double)) * kAggMax + kChunk / 8) * kAggWarps;
+  const size_t asmem = (sizeof(uint32_t) + sizeof(double)) * kAggMax + kChunk / 8 * kAggWarps + 16;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_bucket_aggregate, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)asmem);
