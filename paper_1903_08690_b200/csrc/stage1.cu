@@ -224,7 +224,7 @@ struct Smem {
   double* scratch;      // 2 dummy accumulators
   uint32_t* bslot;  // staged bucket entries (chunk-local slot)
   double* bval;     // staged bucket entries (product)
-  int* ctl;         // [0]=cnt [2]=have_th [4..12]=warp sums
+  int* ctl;         // [0]=cnt [2]=have_th [4..12]=warp sums [16..23]=chunk posting counts
 };
 
 
@@ -656,6 +656,9 @@ __global__ void __launch_bounds__(WS ? kThreads + 32 : kThreads, DM == 0 ? MINB0
     }
   }
   uint32_t consumed = 0;  // pieces consumed (mbarrier slot and phase), uniform
+  // skip-table entries of the next chunk (long lists, nd <= kThreads)
+  uint32_t sk_lo = 0, sk_hi = 0;
+  int64_t skc = -1;
   for (int64_t cb = tile_lo; cb < tile_hi; cb += kChunk) {
     const int64_t ce = min(tile_hi, cb + (int64_t)kChunk);
     const int64_t p0 = cb + (int64_t)tid * kPPT;
@@ -821,8 +824,18 @@ __global__ void __launch_bounds__(WS ? kThreads + 32 : kThreads, DM == 0 ? MINB0
           row = s.dskip[d];
           if (row >= 0) {
             const uint32_t* r = a.skip + (int64_t)row * (a.nchunks_all + 1) + cb / kChunk;
-            sk0 = __ldg(r);
-            sk1 = __ldg(r + 1);
+            if (nd <= kThreads && skc == cb) {  // prefetched during the previous chunk
+              sk0 = sk_lo;
+              sk1 = sk_hi;
+            } else {
+              sk0 = __ldg(r);
+              sk1 = __ldg(r + 1);
+            }
+            if (nd <= kThreads && cb + kChunk < tile_hi) {  // next chunk: row[c+1], row[c+2]
+              sk_lo = sk1;
+              sk_hi = __ldg(r + 2);
+              skc = cb + kChunk;
+            }
           }
         }
         const bool f = d < nd && (row >= 0 ? sk1 > sk0 : s.dnext[d] < (uint32_t)ce) &&
@@ -837,6 +850,7 @@ __global__ void __launch_bounds__(WS ? kThreads + 32 : kThreads, DM == 0 ? MINB0
           before += (i < warp) ? c : 0;
           total += c;
         }
+        uint32_t mycnt = 0;  // postings of this thread's active dim in the chunk
         if (f) {
           const int slot = nact + before + __popc(bal & ((1u << lane) - 1u));
           HS_DCHECK(slot < a.max_qnnz);
@@ -844,6 +858,7 @@ __global__ void __launch_bounds__(WS ? kThreads + 32 : kThreads, DM == 0 ? MINB0
           if (row >= 0) {
             s.abase[slot] = s.dbeg[d] + sk0;
             s.acnt[slot] = sk1 - sk0;
+            mycnt = sk1 - sk0;
           } else {
             const uint32_t cur = s.dcur[d], end = s.dend[d];
             HS_DCHECK(cur < end);
@@ -854,17 +869,21 @@ __global__ void __launch_bounds__(WS ? kThreads + 32 : kThreads, DM == 0 ? MINB0
             const uint32_t nc = cur + cnt;
             s.abase[slot] = cur;
             s.acnt[slot] = cnt;
+            mycnt = cnt;
             s.dcur[d] = nc;
             s.dnext[d] = nc < end ? __ldg(&a.post[nc].x) : 0xFFFFFFFFu;
           }
         }
+        // chunk posting count: per-warp partial sums published before the
+        // barrier that ends this pass (no separate block reduction)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) mycnt += __shfl_xor_sync(0xffffffffu, mycnt, o);
+        if (lane == 0) s.ctl[16 + warp] = (int)mycnt;
         nact += total;
         csync<WS>();
-      }
-      if (nact > 0) {
-        int mine = 0;
-        for (int i = tid; i < nact; i += kThreads) mine += (int)s.acnt[i];
-        npost = block_sum<WS>(mine, s.ctl + 4);
+#pragma unroll
+        for (int i = 0; i < kThreads / 32; ++i) npost += s.ctl[16 + i];
+        if (base + kThreads < nd) csync<WS>();  // ctl[16..] is rewritten by the next pass
       }
   #ifdef HS_DEBUG
       for (int i = tid; i < nact; i += kThreads) {
@@ -1568,7 +1587,7 @@ size_t stage1_smem_bytes(const DeviceIndex& ix, const Stage1Plan& p, bool ws) {
     b += 16 + ring_bytes_env() + (sizeof(uint4) + 3 * sizeof(uint64_t) + sizeof(int)) * kPieceBars +
          2 * sizeof(double);
   b += 8 + (sizeof(double) + sizeof(uint32_t)) * kThreads;  // bucket staging
-  b += sizeof(int) * 16;
+  b += sizeof(int) * 24;
   return b;
 }
 
