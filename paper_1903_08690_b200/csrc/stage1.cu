@@ -670,6 +670,13 @@ __global__ void __launch_bounds__(WS ? kThreads + 32 : kThreads, DM == 0 ? MINB0
       return DM == 0 ? (uint32_t)(j * kThreads + tid) : (uint32_t)(tid * kPPT + j);
     };
     HS_DCHECK(cb >= tile_lo && ce <= a.n);
+    // zero this thread's own accumulator entries (only owners read them, in
+    // the previous chunk's offer phase); the streamed path's adds start after
+    // the active-dim barrier below, so it needs no zeroing pass of its own
+    if (SP && !WS && !bucketed) {
+#pragma unroll
+      for (int j = 0; j < kPPT; ++j) s.acc[aix<DM>(pt_local(j))] = 0.0;
+    }
 
     // ---- dense: LUT16 scan of this thread's 16 points ----
     uint32_t tot[kPPT];
@@ -898,9 +905,8 @@ __global__ void __launch_bounds__(WS ? kThreads + 32 : kThreads, DM == 0 ? MINB0
       if (nact > 0 && npost <= kSmallPostings) {
         // few postings: every thread walks them all in dim order (broadcast
         // loads) and adds only those landing on its own 16 points — per-point
-        // order stays ascending in dim with no block barriers
-  #pragma unroll
-        for (int j = 0; j < kPPT; ++j) s.acc[aix<DM>(pt_local(j))] = 0.0;
+        // order stays ascending in dim with no block barriers (own entries
+        // were zeroed at the top of the chunk)
         for (int i = 0; i < nact; ++i) {
           const uint32_t b = s.abase[i], c = s.acnt[i];
           const double qv = s.dqv[s.alist[i]];
@@ -921,7 +927,6 @@ __global__ void __launch_bounds__(WS ? kThreads + 32 : kThreads, DM == 0 ? MINB0
         // many postings: block-wide per dim, one barrier between dims; the
         // next dim's first kPre*256 postings are loaded while this dim adds
         constexpr int kPre = 4;
-        for (int i = tid; i < kChunk; i += kThreads) s.acc[i] = 0.0;
         uint2 nxt[kPre];
         {
           const uint32_t b = s.abase[0], c = s.acnt[0];
@@ -931,7 +936,6 @@ __global__ void __launch_bounds__(WS ? kThreads + 32 : kThreads, DM == 0 ? MINB0
             nxt[r] = j < c ? __ldg(&a.post[b + j]) : make_uint2(0xFFFFFFFFu, 0u);
           }
         }
-        csync<WS>();
         for (int i = 0; i < nact; ++i) {
           const uint32_t b = s.abase[i], c = s.acnt[i];
           const double qv = s.dqv[s.alist[i]];
