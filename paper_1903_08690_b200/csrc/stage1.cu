@@ -1493,11 +1493,8 @@ void launch_sparse_bucket(const DeviceIndex& ix, const QueryView& q, const uint3
       q.sp_indptr, lbeg, lend, qv, ix.post, sb.nchunks, sb.capq, sb.mode, sb.boff, sb.slots,
       sb.vals);
   const size_t asmem = (sizeof(uint32_t) + sizeof(double)) * kAggMax + kChunk / 8 * kAggWarps + 16;
-  static bool attr = false;
-  if (!attr) {
+  if (asmem > 48 * 1024)
     cudaFuncSetAttribute(k_bucket_aggregate, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)asmem);
-    attr = true;
-  }
   const int ys = (int)std::min<int64_t>(ceil_div(sb.nchunks, kAggWarps), 8);
   k_bucket_aggregate<<<dim3((unsigned)q.nq, (unsigned)ys), kAggWarps * 32, asmem, st>>>(
       sb.mode, sb.boff, sb.nchunks, sb.capq, sb.slots, sb.vals);
