@@ -249,6 +249,8 @@ def main():
     ap.add_argument("--n", type=int, default=None)
     ap.add_argument("--top-t", default=None)
     ap.add_argument("--cpu-sample", type=int, default=None)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0,
+                    help="target CPU work of the cpu_baseline sample")
     ap.add_argument("--truth-queries", type=int, default=None)
     ap.add_argument("--qb1", type=int, default=16,
                     help="single-query launches timed for the Qb=1 scan roofline")
@@ -481,6 +483,10 @@ def main():
         idx.config.retain = s["retain"]
         idx.config.exact_final_rerank = s["exact_final_rerank"]
         qps_cpu, dt = cpu_oracle_qps(idx, qs, sample, threads)
+        if dt < 0.5 * args.cpu_seconds and sample < nq:
+            # the first sample sizes the real one: ~--cpu-seconds of CPU work
+            sample = min(nq, max(sample + 1, int(sample * args.cpu_seconds / max(dt, 1e-3))))
+            qps_cpu, dt = cpu_oracle_qps(idx, qs, sample, threads)
         cpu = {"value": qps_cpu, "unit": "queries/s", "cores": threads, "kind": "port",
                "sample": f"first {sample} of {nq} {args.workload} queries, oracle "
                          f"search_batch(threads={threads}), {dt:.1f} s"}

@@ -42,6 +42,17 @@ from .builder import (  # noqa: F401
     whiten_apply,
     whiten_fit,
 )
+from .formats import (  # noqa: F401
+    load_dataset,
+    load_dense_index,
+    load_device_index,
+    load_index,
+    load_inverted_index,
+    save_dataset,
+    save_dense_index,
+    save_index,
+    save_inverted_index,
+)
 from .search import (  # noqa: F401
     DeviceIndex,
     adc_table,

@@ -82,10 +82,10 @@ def build_cuda(verbose=False, force=False):
 
 
 def build_host(force=False):
-    src = os.path.join(CSRC, "hostbuild.cpp")
-    if force or _stale(LIB_HOST, [src]):
+    srcs = [os.path.join(CSRC, "hostbuild.cpp"), os.path.join(CSRC, "formats.cpp")]
+    if force or _stale(LIB_HOST, srcs + [os.path.join(os.path.dirname(HERE), "include", "hsformats.h")]):
         _run(["g++", "-O3", "-march=x86-64-v3", "-ffp-contract=off", "-fopenmp", "-fPIC", "-shared", "-std=c++17",
-              "-o", LIB_HOST, src])
+              "-o", LIB_HOST] + srcs)
     return LIB_HOST
 
 

@@ -8,3 +8,4 @@ from .types import (  # noqa: F401
     LUT16_CENTERS, Codebooks, DenseIndex, PQCodes, QuantizedLUT, ScalarQuantResidual,
     WhiteningTransform,
 )
+from .formats import load_dense_index, save_dense_index  # noqa: F401

@@ -4,3 +4,4 @@ from .search import sparse_scan  # noqa: F401
 from .types import (  # noqa: F401
     DEFAULT_LINE_CAPACITY, Accumulator, InvertedIndex, PruneThresholds, invert_permutation,
 )
+from .formats import load_inverted_index, save_inverted_index  # noqa: F401
