@@ -136,7 +136,7 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def build_workload(args, rank, world):
+def build_workload(args, rank, world, device=None):
     """Seeded cfg data (this rank's id-range shard) + queries + index."""
     from paper_1903_08690_b200 import build_index, sharded, synth
 
@@ -154,7 +154,7 @@ def build_workload(args, rank, world):
     icfg = cfg.index_config(**kw)
     t0 = time.time()
     exact = cfg.search["exact_final_rerank"]
-    idx = build_index(ds, icfg, keep_dataset=exact)
+    idx = build_index(ds, icfg, keep_dataset=exact, device=device)
     if cfg.search["overfetch"] == 1.0 and idx.dense_index is not None:
         # "no rerank" configs: the stage-1 composition (cfg 3)
         idx.dense_index.residual = None
@@ -287,7 +287,8 @@ def main():
     import paper_1903_08690_b200 as hs
     from paper_1903_08690_b200 import _native as nat
 
-    cfg, ds_full, ds, qs, idx, icfg, id_lo, t_gen, t_build = build_workload(args, rank, world)
+    cfg, ds_full, ds, qs, idx, icfg, id_lo, t_gen, t_build = build_workload(args, rank, world,
+                                                                            device=local)
     s = cfg.search
     h = s["h"]
     dev_index = (hs.device_index(idx, local) if world == 1

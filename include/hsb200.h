@@ -24,6 +24,8 @@
  *   hs_select_topk       <- select_topk                            pipeline.py:165-189
  *   hs_exact_topk        <- brute_force_topk (_exact_scores)       harness.py:25-35, pipeline.py:313-322
  *   hs_shard_merge_dev   <- (new) top-h merge of per-shard results; no reference counterpart
+ *   hs_dense_encode      <- build_index's dense part: pq_encode(...)[order] + pack_codes +
+ *                           sq_encode(residual)   pipeline.py:142-157, dense.py:138-170, 381-390
  */
 #ifndef HSB200_H
 #define HSB200_H
@@ -177,6 +179,18 @@ int hs_index_launches(hs_index_t index, int64_t* launches);
  * (used by bench.py for the roofline). names joined by ';'. */
 int hs_last_kernel_times(hs_index_t index, double* ms, int32_t max_entries,
                          int32_t* n_entries, char* names, int32_t names_cap);
+
+/* ---- index build (dense slice) ---- */
+/* Host pointers.  vec [n][d] f64 in original id order (whitened when the
+ * config whitens), order [n] layout slot -> id, K subspaces of width 1 or 2,
+ * centers = concatenation over k of 16 x subdims[k] f32.  Outputs in layout
+ * order: packed [(K+1)/2][n] pair-major 4-bit codes; optional (NULL = skip)
+ * sq_lo/sq_step [d] and sq_codes [n][d].  Bit-identical to the host build.
+ * seconds (optional) receives the device time of the two kernels. */
+int hs_dense_encode(const double* vec, int64_t n, int64_t d, const int64_t* order,
+                    int32_t K, const int64_t* subdims, const float* centers, int32_t l,
+                    uint8_t* packed, float* sq_lo, float* sq_step, uint8_t* sq_codes,
+                    int device, double* seconds);
 
 #ifdef __cplusplus
 }

@@ -84,6 +84,7 @@ def lib():
         L.hs_set_timing.argtypes = [P, ctypes.c_int]
         L.hs_index_launches.argtypes = [P, ctypes.POINTER(i64)]
         L.hs_last_kernel_times.argtypes = [P, P, i32, ctypes.POINTER(i32), ctypes.c_char_p, i32]
+        L.hs_dense_encode.argtypes = [P, i64, i64, P, i32, P, P, i32, P, P, P, P, ctypes.c_int, P]
         _LIB = L
     return _LIB
 

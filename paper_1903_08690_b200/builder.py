@@ -390,12 +390,47 @@ def sq_residual(vec, order, codes, cb: Codebooks) -> ScalarQuantResidual:
     return ScalarQuantResidual(lo=lo, step=step, codes=q)
 
 
+def dense_encode_gpu(vec, order, cb: Codebooks, device: int = 0, with_sq: bool = True,
+                     timing: dict | None = None):
+    """PQ codes (packed, layout order) + SQ residual on the GPU (`hs_dense_encode`).
+
+    Same products, bit for bit, as `PQCodes.from_codes(pq_encode(vec, cb)[order])`
+    and `sq_residual(vec, order, codes, cb)` (pipeline.py:152-157).
+    """
+    from . import _native as nat
+
+    L = nat.require_gpu()
+    x = np.ascontiguousarray(vec, dtype=np.float64)
+    n, d = x.shape
+    K = cb.n_subspaces
+    order = np.ascontiguousarray(order, dtype=np.int64)
+    sub = np.ascontiguousarray(cb.subdims, dtype=np.int64)
+    cen = np.ascontiguousarray(np.concatenate([c.reshape(-1) for c in cb.centers]),
+                               dtype=np.float32)
+    packed = np.empty(((K + 1) // 2, n), dtype=np.uint8)
+    lo = np.empty(d, np.float32) if with_sq else None
+    step = np.empty(d, np.float32) if with_sq else None
+    q = np.empty((n, d), np.uint8) if with_sq else None
+    sec = ctypes.c_double(0.0)
+    nat.check(L.hs_dense_encode(_ptr(x), n, d, _ptr(order), K, _ptr(sub), _ptr(cen),
+                                cb.n_centers, _ptr(packed), nat.ptr(lo), nat.ptr(step),
+                                nat.ptr(q), int(device), ctypes.byref(sec)))
+    if timing is not None:
+        timing["dense_encode_s"] = sec.value
+    codes = PQCodes(n=n, n_subspaces=K, n_centers=cb.n_centers, packed=packed)
+    return codes, (ScalarQuantResidual(lo=lo, step=step, codes=q) if with_sq else None)
+
+
 # ----------------------------------------------------------------------------
 # build_index
 # ----------------------------------------------------------------------------
 def build_index(dataset: HybridDataset, config: HybridIndexConfig | None = None,
-                keep_dataset: bool = True, order_fn=None) -> HybridIndex:
-    """Full hybrid index; deterministic for a fixed config seed (pipeline.py:119-162)."""
+                keep_dataset: bool = True, order_fn=None, device: int | None = None) -> HybridIndex:
+    """Full hybrid index; deterministic for a fixed config seed (pipeline.py:119-162).
+
+    `device` (not in the reference): run the dense encode (PQ codes + SQ
+    residual) on that GPU through `hs_dense_encode`; products are identical.
+    """
     config = config or HybridIndexConfig()
     data_part, residual_part, _ = prune_split(dataset.sparse, config.prune_thresholds(),
                                               with_discarded=False)
@@ -415,9 +450,14 @@ def build_index(dataset: HybridDataset, config: HybridIndexConfig | None = None,
         K = config.pq_subspaces or max(1, math.ceil(dataset.d_dense / 2))
         cb = train_codebooks(vec, K, n_centers=config.pq_centers, n_iters=config.kmeans_iters,
                              seed=config.seed, sample=config.train_sample)
-        codes = pq_encode(vec, cb)[order]
-        dense_index = DenseIndex(codebooks=cb, codes=PQCodes.from_codes(codes, config.pq_centers),
-                                 residual=sq_residual(vec, order, codes, cb), whitening=wt)
+        if device is not None and config.pq_centers == 16 and int(np.max(cb.subdims)) <= 2:
+            pq, sq = dense_encode_gpu(vec, order, cb, device)
+            dense_index = DenseIndex(codebooks=cb, codes=pq, residual=sq, whitening=wt)
+        else:
+            codes = pq_encode(vec, cb)[order]
+            dense_index = DenseIndex(codebooks=cb,
+                                     codes=PQCodes.from_codes(codes, config.pq_centers),
+                                     residual=sq_residual(vec, order, codes, cb), whitening=wt)
     return HybridIndex(config=config, n=dataset.n, d_sparse=dataset.d_sparse,
                        d_dense=dataset.d_dense, order=order, sparse_index=sidx,
                        sparse_residual=res, dense_index=dense_index,
