@@ -8,16 +8,17 @@
 // hsb_sq_residual, which the golden build fixtures pin to the reference).
 //
 // Two HBM-bound kernels:
-//   k_pq_encode_pack  grid (slot chunks, subspace pairs): one thread per
-//                     (layout slot, pair) reads the pair's <= 4 f64 values of
-//                     row order[i] (one 32-byte sector), picks the nearest of
-//                     the 16 centers per subspace in f64 (first minimum wins),
-//                     writes the packed byte (coalesced along slots) and folds
-//                     the residuals into per-dimension min/max (block
-//                     reduction, then one ordered-key atomic per dim).
-//   k_sq_encode       one thread per (slot, dim), dims fastest: recomputes the
-//                     residual from the packed nibble and writes the u8 code.
-// Bytes per point: d*8 (vectors, read twice) + ceil(K/2) + d (codes out).
+//   k_pq_encode_pack  persistent CTAs over tiles of 32 layout slots; a warp
+//                     encodes a whole row order[i] (lane = subspace pair,
+//                     contiguous loads), picks the nearest of the 16 centers
+//                     per subspace in f64 (first minimum wins), stores the
+//                     tile pair-major through a shared-memory transpose plus a
+//                     point-major copy for the SQ pass, and keeps per-dim
+//                     residual min/max in registers (ordered-key atomics once
+//                     per CTA).
+//   k_sq_encode       CTA per row, threads over dims: recomputes the residual
+//                     from the point-major code and writes the u8 code.
+// Bytes per point: 2*d*8 (vectors, read twice) + 3*ceil(K/2) + d.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -54,127 +55,225 @@ struct SubTab {  // per-subspace geometry (device arrays)
   const double* csq;        // [K][16] |c|^2 in the host recipe
 };
 
+constexpr int kTile = 32;  // layout slots per tile
+
+// nearest of 16 centers for one subspace (hostbuild.cpp hsb_pq_encode recipe)
+__device__ __forceinline__ int nearest(double x0, double x1, int w, const float2* c,
+                                       const double* csq, int cs) {
+  int best = 0;
+  double bd = 0.0;
+  if (w == 2) {
+    const double sq = __dadd_rn(__dadd_rn(0.0, __dmul_rn(x0, x0)), __dmul_rn(x1, x1));
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const float2 cc = c[j * cs];
+      const double dot = __fma_rn(x1, (double)cc.y, __dmul_rn(x0, (double)cc.x));
+      const double d2 = __dadd_rn(__dsub_rn(sq, __dmul_rn(2.0, dot)), csq[j * cs]);
+      if (j == 0 || d2 < bd) {
+        bd = d2;
+        best = j;
+      }
+    }
+  } else {
+    const double sq = __dadd_rn(0.0, __dmul_rn(x0, x0));
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const double dot = __dmul_rn(x0, (double)c[j * cs].x);
+      const double d2 = __dadd_rn(__dsub_rn(sq, __dmul_rn(2.0, dot)), csq[j * cs]);
+      if (j == 0 || d2 < bd) {
+        bd = d2;
+        best = j;
+      }
+    }
+  }
+  return best;
+}
+
+// Persistent: a CTA walks tiles of kTile layout slots; each warp encodes whole
+// rows (lane = subspace pair, so a warp's loads of one row are contiguous),
+// the tile's codes are transposed in shared memory and stored pair-major
+// (32 consecutive bytes per pair), and a point-major copy [n][npairs] feeds
+// the SQ pass.  Residual min/max per dim stay in registers across tiles
+// (lane-owned pairs), then shared-memory and global ordered-key atomics once
+// per CTA.  M = ceil(npairs / 32).
+template <int M>
 __global__ void __launch_bounds__(kEncThreads)
 k_pq_encode_pack(const double* __restrict__ vec, int64_t n, int64_t d,
                  const int64_t* __restrict__ order, int32_t K, SubTab t,
                  const float* __restrict__ centers, uint8_t* __restrict__ packed,
-                 unsigned long long* __restrict__ lo_key, unsigned long long* __restrict__ hi_key) {
-  const int p = blockIdx.y;
-  const int64_t i = (int64_t)blockIdx.x * kEncThreads + threadIdx.x;
-  __shared__ float s_c[2][16][2];
-  __shared__ double s_csq[2][16];
-  __shared__ double s_red[2][4][kEncThreads / 32];  // [min|max][dim][warp]
-  int ks[2] = {2 * p, 2 * p + 1};
-  const int nk = (2 * p + 1 < K) ? 2 : 1;
-  for (int e = threadIdx.x; e < nk * 16; e += blockDim.x) {
-    const int s = e >> 4, c = e & 15, k = ks[s], w = t.width[k];
-    s_c[s][c][0] = centers[t.cen_off[k] + c * w];
-    s_c[s][c][1] = w == 2 ? centers[t.cen_off[k] + c * w + 1] : 0.f;
-    s_csq[s][c] = t.csq[k * 16 + c];
+                 uint8_t* __restrict__ codes_pm, unsigned long long* __restrict__ lo_key,
+                 unsigned long long* __restrict__ hi_key) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int npairs = (K + 1) / 2;
+  const int npad = 2 * ((K + 1) / 2);
+  float2* s_c = reinterpret_cast<float2*>(smem);                         // [16][2][npairs]
+  double* s_csq = reinterpret_cast<double*>(s_c + (size_t)npad * 16);    // [16][2][npairs]
+  unsigned long long* s_lo = reinterpret_cast<unsigned long long*>(s_csq + (size_t)npad * 16);  // [d]
+  unsigned long long* s_hi = s_lo + d;                                   // [d]
+  uint8_t* s_tile = reinterpret_cast<uint8_t*>(s_hi + d);                // [npairs][kTile]
+  // centers and |c|^2 at [c][k & 1][k >> 1]: the lanes of a warp (consecutive
+  // pairs) read consecutive entries, no bank conflicts
+  const int cstride = 2 * npairs;
+  for (int e = threadIdx.x; e < K * 16; e += blockDim.x) {
+    const int k = e >> 4, c = e & 15, w = t.width[k];
+    const float* src = centers + t.cen_off[k] + c * w;
+    const int at = c * cstride + (k & 1) * npairs + (k >> 1);
+    s_c[at] = make_float2(src[0], w == 2 ? src[1] : 0.f);
+    s_csq[at] = t.csq[e];
+  }
+  for (int j = threadIdx.x; j < d; j += blockDim.x) {
+    s_lo[j] = ~0ull;
+    s_hi[j] = 0ull;
   }
   __syncthreads();
-  const bool live = i < n;
-  double rmin[4], rmax[4];
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    rmin[q] = INFINITY;
-    rmax[q] = -INFINITY;
-  }
-  uint8_t byte = 0;
-  if (live) {
-    const double* row = vec + order[i] * d;
-#pragma unroll
-    for (int s = 0; s < 2; ++s) {
-      if (s < nk) {
-        const int k = ks[s], w = t.width[k];
-        const double x0 = row[t.dim_off[k]];
-        const double x1 = w == 2 ? row[t.dim_off[k] + 1] : 0.0;
-        int best = 0;
-        double bd = 0.0;
-        if (w == 2) {
-          const double sq = __dadd_rn(__dadd_rn(0.0, __dmul_rn(x0, x0)), __dmul_rn(x1, x1));
-#pragma unroll
-          for (int c = 0; c < 16; ++c) {
-            const double dot = __fma_rn(x1, (double)s_c[s][c][1], __dmul_rn(x0, (double)s_c[s][c][0]));
-            const double d2 = __dadd_rn(__dsub_rn(sq, __dmul_rn(2.0, dot)), s_csq[s][c]);
-            if (c == 0 || d2 < bd) {
-              bd = d2;
-              best = c;
-            }
-          }
-        } else {
-          const double sq = __dadd_rn(0.0, __dmul_rn(x0, x0));
-#pragma unroll
-          for (int c = 0; c < 16; ++c) {
-            const double dot = __dmul_rn(x0, (double)s_c[s][c][0]);
-            const double d2 = __dadd_rn(__dsub_rn(sq, __dmul_rn(2.0, dot)), s_csq[s][c]);
-            if (c == 0 || d2 < bd) {
-              bd = d2;
-              best = c;
-            }
-          }
-        }
-        byte |= (uint8_t)(best << (4 * s));
-        const double r0 = __dsub_rn(x0, (double)s_c[s][best][0]);
-        rmin[2 * s] = rmax[2 * s] = r0;
-        if (w == 2) {
-          const double r1 = __dsub_rn(x1, (double)s_c[s][best][1]);
-          rmin[2 * s + 1] = rmax[2 * s + 1] = r1;
-        }
-      }
-    }
-    packed[(int64_t)p * n + i] = byte;
-  }
-  // block min/max per dim of this pair (<= 4 dims)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double rmin[M][4], rmax[M][4];
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    double a = rmin[q], b = rmax[q];
+  for (int m = 0; m < M; ++m)
 #pragma unroll
-    for (int o = 16; o; o >>= 1) {
-      a = fmin(a, __shfl_xor_sync(0xffffffffu, a, o));
-      b = fmax(b, __shfl_xor_sync(0xffffffffu, b, o));
+    for (int q = 0; q < 4; ++q) {
+      rmin[m][q] = INFINITY;
+      rmax[m][q] = -INFINITY;
     }
-    if (lane == 0) {
-      s_red[0][q][warp] = a;
-      s_red[1][q][warp] = b;
+  const int64_t ntiles = (n + kTile - 1) / kTile;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t base = tile * kTile;
+    // S slots of this warp in flight: all their loads issue before the math
+    constexpr int S = M >= 4 ? 1 : 4 / M;
+    constexpr int kWarps = kEncThreads / 32;
+    for (int s0 = warp; s0 < kTile; s0 += kWarps * S) {
+      double xv[S][M][4];
+#pragma unroll
+      for (int u = 0; u < S; ++u) {
+        const int64_t i = base + s0 + u * kWarps;
+        const bool ok = s0 + u * kWarps < kTile && i < n;
+        const double* row = vec + (ok ? order[i] : 0) * d;
+#pragma unroll
+        for (int m = 0; m < M; ++m) {
+          const int p = lane + 32 * m;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int k = 2 * p + h;
+            const bool live = ok && p < npairs && k < K;
+            const int w = live ? t.width[k] : 1, off = live ? t.dim_off[k] : 0;
+            xv[u][m][2 * h] = live ? row[off] : 0.0;
+            xv[u][m][2 * h + 1] = live && w == 2 ? row[off + 1] : 0.0;
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < S; ++u) {
+        const int s = s0 + u * kWarps;
+        const int64_t i = base + s;
+        if (s >= kTile || i >= n) break;
+#pragma unroll
+        for (int m = 0; m < M; ++m) {
+          const int p = lane + 32 * m;
+          if (p < npairs) {
+            uint8_t byte = 0;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int k = 2 * p + h;
+              if (k < K) {
+                const int w = t.width[k];
+                const double x0 = xv[u][m][2 * h], x1 = xv[u][m][2 * h + 1];
+                const int at = h * npairs + p;
+                const int c = nearest(x0, x1, w, s_c + at, s_csq + at, cstride);
+                byte |= (uint8_t)(c << (4 * h));
+                const float2 cc = s_c[c * cstride + at];
+                const double r0 = __dsub_rn(x0, (double)cc.x);
+                rmin[m][2 * h] = fmin(rmin[m][2 * h], r0);
+                rmax[m][2 * h] = fmax(rmax[m][2 * h], r0);
+                if (w == 2) {
+                  const double r1 = __dsub_rn(x1, (double)cc.y);
+                  rmin[m][2 * h + 1] = fmin(rmin[m][2 * h + 1], r1);
+                  rmax[m][2 * h + 1] = fmax(rmax[m][2 * h + 1], r1);
+                }
+              }
+            }
+            s_tile[p * kTile + s] = byte;
+            codes_pm[i * npairs + p] = byte;
+          }
+        }
+      }
+    }
+    __syncthreads();
+    const int live = (int)((n - base) < kTile ? (n - base) : kTile);
+    for (int e = threadIdx.x; e < npairs * kTile; e += blockDim.x) {
+      const int p = e / kTile, s = e % kTile;
+      if (s < live) packed[(int64_t)p * n + base + s] = s_tile[e];
+    }
+    __syncthreads();
+  }
+  // fold the lane-owned dims into shared memory, then once per CTA to global
+#pragma unroll
+  for (int m = 0; m < M; ++m) {
+    const int p = lane + 32 * m;
+    if (p >= npairs) continue;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int k = 2 * p + (q >> 1), tt = q & 1;
+      if (k >= K || tt >= t.width[k] || !(rmin[m][q] <= rmax[m][q])) continue;
+      const int dim = t.dim_off[k] + tt;
+      atomicMin(s_lo + dim, dkey(rmin[m][q]));
+      atomicMax(s_hi + dim, dkey(rmax[m][q]));
     }
   }
   __syncthreads();
-  if (threadIdx.x < 8) {
-    const int q = threadIdx.x & 3, mx = threadIdx.x >> 2;
-    const int s = q >> 1, tt = q & 1;
-    if (s < nk && tt < t.width[ks[s]]) {
-      double v = s_red[mx][q][0];
-      for (int w = 1; w < kEncThreads / 32; ++w)
-        v = mx ? fmax(v, s_red[mx][q][w]) : fmin(v, s_red[mx][q][w]);
-      if (isfinite(v)) {
-        const int dim = t.dim_off[ks[s]] + tt;
-        if (mx) atomicMax(hi_key + dim, dkey(v));
-        else atomicMin(lo_key + dim, dkey(v));
-      }
-    }
+  for (int j = threadIdx.x; j < d; j += blockDim.x) {
+    if (s_lo[j] != ~0ull) atomicMin(lo_key + j, s_lo[j]);
+    if (s_hi[j] != 0ull) atomicMax(hi_key + j, s_hi[j]);
   }
 }
 
-__global__ void k_sq_encode(const double* __restrict__ vec, int64_t n, int64_t d,
-                            const int64_t* __restrict__ order, const int32_t* __restrict__ dim_k,
-                            const int32_t* __restrict__ dim_t, const int32_t* __restrict__ width,
-                            const int32_t* __restrict__ cen_off, const float* __restrict__ centers,
-                            const uint8_t* __restrict__ packed, const double* __restrict__ lo,
-                            const double* __restrict__ safe, uint8_t* __restrict__ sq) {
-  const int64_t total = n * d;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = e / d;
-    const int j = (int)(e - i * d);
-    const int k = dim_k[j];
-    const int code = (packed[(int64_t)(k >> 1) * n + i] >> (4 * (k & 1))) & 15;
-    const double r = __dsub_rn(vec[order[i] * d + j],
-                               (double)centers[cen_off[k] + code * width[k] + dim_t[j]]);
-    double q = floor(__ddiv_rn(__dsub_rn(r, lo[j]), safe[j]));
-    q = q < 0.0 ? 0.0 : (q > 255.0 ? 255.0 : q);
-    sq[e] = (uint8_t)q;
+// One CTA row at a time (grid-stride over layout slots), threads over dims:
+// the row of vec and the slot's point-major codes are contiguous loads, the
+// u8 output row a contiguous store.
+__global__ void __launch_bounds__(256)
+k_sq_encode(const double* __restrict__ vec, int64_t n, int64_t d,
+            const int64_t* __restrict__ order, const int32_t* __restrict__ dim_k,
+            const int32_t* __restrict__ dim_t, const int32_t* __restrict__ width,
+            const int32_t* __restrict__ cen_off, const float* __restrict__ centers,
+            const uint8_t* __restrict__ codes_pm, int npairs, const double* __restrict__ lo,
+            const double* __restrict__ safe, uint8_t* __restrict__ sq) {
+  constexpr int R = 4;  // rows in flight per CTA
+  for (int64_t i0 = (int64_t)blockIdx.x * R; i0 < n; i0 += (int64_t)gridDim.x * R) {
+    const double* rows[R];
+    const uint8_t* crs[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int64_t i = i0 + r < n ? i0 + r : n - 1;
+      rows[r] = vec + order[i] * d;
+      crs[r] = codes_pm + i * npairs;
+    }
+    for (int j = threadIdx.x; j < d; j += blockDim.x) {
+      const int k = dim_k[j];
+      const double l0 = lo[j], sf = safe[j], iv = 1.0 / sf;
+      const float* cb = centers + cen_off[k] + dim_t[j];
+      const int w = width[k];
+      double x[R];
+      int code[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        x[r] = rows[r][j];
+        code[r] = (crs[r][k >> 1] >> (4 * (k & 1))) & 15;
+      }
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        if (i0 + r >= n) break;
+        const double res = __dsub_rn(x[r], (double)cb[code[r] * w]);
+        // floor(RN(a / sf)) through the reciprocal when a*inv is not within
+        // 1e-6 of an integer (|a*inv - RN(a/sf)| is a few ulp of a value
+        // <= 256, far below that); the IEEE division otherwise
+        const double a = __dsub_rn(res, l0);
+        const double tq = a * iv;
+        double q = floor(tq);
+        const double fr = tq - q;
+        if (!(fr > 1e-6 && fr < 1.0 - 1e-6)) q = floor(__ddiv_rn(a, sf));
+        q = q < 0.0 ? 0.0 : (q > 255.0 ? 255.0 : q);
+        sq[(i0 + r) * d + j] = (uint8_t)q;
+      }
+    }
   }
 }
 
@@ -242,7 +341,7 @@ extern "C" int hs_dense_encode(const double* vec, int64_t n, int64_t d, const in
   int64_t* dord;
   int32_t *ddo, *dw, *dco, *ddk, *ddt;
   float* dcen;
-  uint8_t *dpk, *dsq = nullptr;
+  uint8_t *dpk, *dpm, *dsq = nullptr;
   unsigned long long* dkeys;
   HS_CUDA(b.upload(&dvec, vec, (size_t)(n * d)));
   HS_CUDA(b.upload(&dord, order, (size_t)n));
@@ -254,6 +353,7 @@ extern "C" int hs_dense_encode(const double* vec, int64_t n, int64_t d, const in
   HS_CUDA(b.upload(&dcsq, csq.data(), csq.size()));
   HS_CUDA(b.upload(&dcen, centers, (size_t)co));
   HS_CUDA(b.alloc(&dpk, (size_t)(npairs * n)));
+  HS_CUDA(b.alloc(&dpm, (size_t)(npairs * n)));
   HS_CUDA(b.alloc(&dkeys, (size_t)(2 * d)));
   HS_CUDA(b.alloc(&dlo, (size_t)d));
   HS_CUDA(b.alloc(&dsafe, (size_t)d));
@@ -266,9 +366,23 @@ extern "C" int hs_dense_encode(const double* vec, int64_t n, int64_t d, const in
   HS_CUDA(cudaEventRecord(e0));
   if (n > 0) {
     SubTab t{ddo, dw, dco, dcsq};
-    dim3 grid((unsigned)((n + kEncThreads - 1) / kEncThreads), (unsigned)npairs);
-    k_pq_encode_pack<<<grid, kEncThreads>>>(dvec, n, d, dord, K, t, dcen, dpk, dkeys, dkeys + d);
-    HS_CUDA(cudaGetLastError());
+    const size_t smem = (size_t)(2 * npairs) * 16 * (sizeof(float2) + sizeof(double)) +
+                        2 * sizeof(unsigned long long) * (size_t)d + (size_t)npairs * kTile;
+    const int64_t ntiles = (n + kTile - 1) / kTile;
+    const unsigned grid = (unsigned)(ntiles < kNumSMs * 4 ? ntiles : kNumSMs * 4);
+    const int M = (npairs + 31) / 32;
+    auto go = [&](auto kern) -> cudaError_t {
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      kern<<<grid, kEncThreads, smem>>>(dvec, n, d, dord, K, t, dcen, dpk, dpm, dkeys, dkeys + d);
+      return cudaGetLastError();
+    };
+    if (smem > 200 * 1024) HS_FAIL(HS_EUNSUPPORTED, "hs_dense_encode: too many subspaces");
+    if (M <= 1) HS_CUDA(go(k_pq_encode_pack<1>));
+    else if (M <= 2) HS_CUDA(go(k_pq_encode_pack<2>));
+    else if (M <= 4) HS_CUDA(go(k_pq_encode_pack<4>));
+    else if (M <= 8) HS_CUDA(go(k_pq_encode_pack<8>));
+    else HS_FAIL(HS_EUNSUPPORTED, "hs_dense_encode: more than 512 subspaces");
   }
   std::vector<double> lo(d), step(d), safe(d);
   if (sq_codes || sq_lo || sq_step) {
@@ -288,11 +402,11 @@ extern "C" int hs_dense_encode(const double* vec, int64_t n, int64_t d, const in
   if (sq_codes && n > 0) {
     HS_CUDA(cudaMemcpy(dlo, lo.data(), sizeof(double) * d, cudaMemcpyHostToDevice));
     HS_CUDA(cudaMemcpy(dsafe, safe.data(), sizeof(double) * d, cudaMemcpyHostToDevice));
-    const int64_t total = n * d;
-    const int threads = 256;
-    const int64_t want = (total + threads - 1) / threads;
-    const unsigned blocks = (unsigned)(want < kNumSMs * 32 ? want : kNumSMs * 32);
-    k_sq_encode<<<blocks, threads>>>(dvec, n, d, dord, ddk, ddt, dw, dco, dcen, dpk, dlo, dsafe, dsq);
+    const int threads = d >= 256 ? 256 : (int)((d + 31) / 32 * 32);
+    const int64_t rows4 = (n + 3) / 4;
+    const unsigned blocks = (unsigned)(rows4 < kNumSMs * 16 ? rows4 : kNumSMs * 16);
+    k_sq_encode<<<blocks, threads>>>(dvec, n, d, dord, ddk, ddt, dw, dco, dcen, dpm, npairs, dlo,
+                                     dsafe, dsq);
     HS_CUDA(cudaGetLastError());
   }
   HS_CUDA(cudaEventRecord(e1));
