@@ -622,6 +622,16 @@ int hs_index_create(const hs_index_desc* ds, int device, hs_index_t* out) {
     HS_FAIL(HS_EINVAL, "d_sparse must be < 2^32");
   const int64_t nnz_post = ds->n_active ? ds->post_ptr[ds->n_active] : 0;
   if (nnz_post >= (int64_t)0xFFFFFFFFLL) HS_FAIL(HS_EINVAL, "more than 2^32 postings");
+  // indices the kernels dereference: reject a corrupt (e.g. hand-edited file)
+  // index here rather than read out of bounds on the device
+  for (int64_t i = 0; i < ds->n; ++i)
+    if (ds->order[i] < 0 || ds->order[i] >= ds->n) HS_FAIL(HS_EINVAL, "layout order out of range");
+  for (int64_t a = 0; a < ds->n_active; ++a) {
+    if ((int64_t)ds->post_dims[a] >= ds->d_sparse) HS_FAIL(HS_EINVAL, "posting dimension out of range");
+    if (ds->post_ptr[a + 1] < ds->post_ptr[a]) HS_FAIL(HS_EINVAL, "posting offsets not ascending");
+  }
+  for (int64_t e = 0; e < nnz_post; ++e)
+    if ((int64_t)ds->post_ids[e] >= ds->n) HS_FAIL(HS_EINVAL, "posting id out of range");
   HS_CUDA(cudaSetDevice(device));
   std::unique_ptr<hs_index, void (*)(hs_index*)> ix(new hs_index(), [](hs_index* p) {
     hs::free_index(p);

@@ -58,18 +58,20 @@ struct SubTab {  // per-subspace geometry (device arrays)
 constexpr int kTile = 32;  // layout slots per tile
 
 // nearest of 16 centers for one subspace (hostbuild.cpp hsb_pq_encode recipe)
-__device__ __forceinline__ int nearest(double x0, double x1, int w, const double2* c,
-                                       const double* csq, int cs) {
+__device__ __forceinline__ int nearest(double x0, double x1, int w, const float2* c, int cs) {
   int best = 0;
   double bd = 0.0;
   if (w == 2) {
     const double sq = __dadd_rn(__dadd_rn(0.0, __dmul_rn(x0, x0)), __dmul_rn(x1, x1));
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
-      const double2 cc = c[j * cs];
-      const double dot = __fma_rn(x1, cc.y, __dmul_rn(x0, cc.x));
+      const float2 cf = c[j * cs];
+      const double c0 = cf.x, c1 = cf.y;
+      const double dot = __fma_rn(x1, c1, __dmul_rn(x0, c0));
+      // |c|^2 as hsb_pq_encode: (0 + c0*c0) + c1*c1 (0 + v is exact)
+      const double csq = __dadd_rn(__dmul_rn(c0, c0), __dmul_rn(c1, c1));
       // 2*dot is exact, so fma(-2, dot, sq) == RN(sq - 2*dot)
-      const double d2 = __dadd_rn(__fma_rn(-2.0, dot, sq), csq[j * cs]);
+      const double d2 = __dadd_rn(__fma_rn(-2.0, dot, sq), csq);
       if (j == 0 || d2 < bd) {
         bd = d2;
         best = j;
@@ -79,8 +81,9 @@ __device__ __forceinline__ int nearest(double x0, double x1, int w, const double
     const double sq = __dadd_rn(0.0, __dmul_rn(x0, x0));
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
-      const double dot = __dmul_rn(x0, c[j * cs].x);
-      const double d2 = __dadd_rn(__fma_rn(-2.0, dot, sq), csq[j * cs]);
+      const double c0 = c[j * cs].x;
+      const double dot = __dmul_rn(x0, c0);
+      const double d2 = __dadd_rn(__fma_rn(-2.0, dot, sq), __dmul_rn(c0, c0));
       if (j == 0 || d2 < bd) {
         bd = d2;
         best = j;
@@ -107,9 +110,8 @@ k_pq_encode_pack(const double* __restrict__ vec, int64_t n, int64_t d,
   extern __shared__ __align__(16) unsigned char smem[];
   const int npairs = (K + 1) / 2;
   const int npad = 2 * ((K + 1) / 2);
-  double2* s_c = reinterpret_cast<double2*>(smem);                       // [16][2][npairs]
-  double* s_csq = reinterpret_cast<double*>(s_c + (size_t)npad * 16);    // [16][2][npairs]
-  unsigned long long* s_lo = reinterpret_cast<unsigned long long*>(s_csq + (size_t)npad * 16);  // [d]
+  float2* s_c = reinterpret_cast<float2*>(smem);                         // [16][2][npairs]
+  unsigned long long* s_lo = reinterpret_cast<unsigned long long*>(s_c + (size_t)npad * 16);  // [d]
   unsigned long long* s_hi = s_lo + d;                                   // [d]
   uint8_t* s_tile = reinterpret_cast<uint8_t*>(s_hi + d);                // [npairs][kTile]
   // centers and |c|^2 at [c][k & 1][k >> 1]: the lanes of a warp (consecutive
@@ -119,8 +121,7 @@ k_pq_encode_pack(const double* __restrict__ vec, int64_t n, int64_t d,
     const int k = e >> 4, c = e & 15, w = t.width[k];
     const float* src = centers + t.cen_off[k] + c * w;
     const int at = c * cstride + (k & 1) * npairs + (k >> 1);
-    s_c[at] = make_double2((double)src[0], w == 2 ? (double)src[1] : 0.0);
-    s_csq[at] = t.csq[e];
+    s_c[at] = make_float2(src[0], w == 2 ? src[1] : 0.f);
   }
   for (int j = threadIdx.x; j < d; j += blockDim.x) {
     s_lo[j] = ~0ull;
@@ -179,14 +180,14 @@ k_pq_encode_pack(const double* __restrict__ vec, int64_t n, int64_t d,
                 const int w = t.width[k];
                 const double x0 = xv[u][m][2 * h], x1 = xv[u][m][2 * h + 1];
                 const int at = h * npairs + p;
-                const int c = nearest(x0, x1, w, s_c + at, s_csq + at, cstride);
+                const int c = nearest(x0, x1, w, s_c + at, cstride);
                 byte |= (uint8_t)(c << (4 * h));
-                const double2 cc = s_c[c * cstride + at];
-                const double r0 = __dsub_rn(x0, cc.x);
+                const float2 cc = s_c[c * cstride + at];
+                const double r0 = __dsub_rn(x0, (double)cc.x);
                 rmin[m][2 * h] = fmin(rmin[m][2 * h], r0);
                 rmax[m][2 * h] = fmax(rmax[m][2 * h], r0);
                 if (w == 2) {
-                  const double r1 = __dsub_rn(x1, cc.y);
+                  const double r1 = __dsub_rn(x1, (double)cc.y);
                   rmin[m][2 * h + 1] = fmin(rmin[m][2 * h + 1], r1);
                   rmax[m][2 * h + 1] = fmax(rmax[m][2 * h + 1], r1);
                 }
@@ -367,7 +368,7 @@ extern "C" int hs_dense_encode(const double* vec, int64_t n, int64_t d, const in
   HS_CUDA(cudaEventRecord(e0));
   if (n > 0) {
     SubTab t{ddo, dw, dco, dcsq};
-    const size_t smem = (size_t)(2 * npairs) * 16 * (sizeof(double2) + sizeof(double)) +
+    const size_t smem = (size_t)(2 * npairs) * 16 * sizeof(float2) +
                         2 * sizeof(unsigned long long) * (size_t)d + (size_t)npairs * kTile;
     const int64_t ntiles = (n + kTile - 1) / kTile;
     const unsigned grid = (unsigned)(ntiles < kNumSMs * 4 ? ntiles : kNumSMs * 4);

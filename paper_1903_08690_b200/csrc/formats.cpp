@@ -24,6 +24,7 @@
 
 #include <cerrno>
 #include <cstdio>
+#include <cstdint>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -56,6 +57,13 @@ struct Cursor {
     return v;
   }
 };
+
+// Checked byte count a*b (SIZE_MAX on overflow, which no cursor can satisfy,
+// so a hostile length reads as a truncated file instead of wrapping).
+inline size_t nb(size_t a, size_t b) {
+  size_t r;
+  return __builtin_mul_overflow(a, b, &r) ? SIZE_MAX : r;
+}
 
 template <class T>
 T ld(const uint8_t* p) {
@@ -124,8 +132,8 @@ SparseView parse_hsix(Cursor c) {
   v.d = int64_t(ld<uint64_t>(h + 12));
   if (version != 1) fail(HS_FMT_EBADVERSION, "unsupported sparse index version " + std::to_string(version));
   if (v.n < 0 || v.d < 0) fail(HS_FMT_ETRUNCATED, "truncated file while reading permutation");
-  v.order = c.take(size_t(v.n) * 4, "permutation");
-  v.counts = c.take(size_t(v.d) * 4, "posting counts");
+  v.order = c.take(nb(size_t(v.n), 4), "permutation");
+  v.counts = c.take(nb(size_t(v.d), 4), "posting counts");
   v.recs = c.base + c.pos;
   size_t off = 0;
   for (int64_t j = 0; j < v.d; ++j) {
@@ -151,26 +159,27 @@ DenseView parse_hdpq(Cursor c) {
   v.l = int32_t(ld<uint32_t>(h + 20));
   if (version != 1) fail(HS_FMT_EBADVERSION, "unsupported dense index version " + std::to_string(version));
   if (v.n < 0 || v.d < 0 || v.K < 0 || v.l < 0) fail(HS_FMT_EINVAL, "dense header out of range");
-  v.subdims = c.take(size_t(v.K) * 4, "subdims");
+  v.subdims = c.take(nb(size_t(v.K), 4), "subdims");
   v.centers = c.base + c.pos;
   for (int32_t k = 0; k < v.K; ++k) {
     int64_t len = int64_t(v.l) * ld<uint32_t>(v.subdims + 4 * k);
-    c.take(size_t(len) * 4, "centers " + std::to_string(k));
+    c.take(nb(size_t(len), 4), "centers " + std::to_string(k));
     v.centers_len += len;
   }
-  v.codes_bytes = v.l == 16 ? int64_t((v.K + 1) / 2) * v.n : v.n * int64_t(v.K);
-  v.codes = c.take(size_t(v.codes_bytes), "codes");
+  const size_t cb = v.l == 16 ? nb(size_t((v.K + 1) / 2), size_t(v.n)) : nb(size_t(v.n), size_t(v.K));
+  v.codes = c.take(cb, "codes");
+  v.codes_bytes = int64_t(cb);
   v.has_sq = *c.take(1, "residual flag") ? 1 : 0;
   if (v.has_sq) {
-    v.sq_lo = c.take(size_t(v.d) * 4, "sq lo");
-    v.sq_step = c.take(size_t(v.d) * 4, "sq step");
-    v.sq_codes = c.take(size_t(v.n) * size_t(v.d), "sq codes");
+    v.sq_lo = c.take(nb(size_t(v.d), 4), "sq lo");
+    v.sq_step = c.take(nb(size_t(v.d), 4), "sq step");
+    v.sq_codes = c.take(nb(size_t(v.n), size_t(v.d)), "sq codes");
   }
   v.has_wh = *c.take(1, "whitening flag") ? 1 : 0;
   if (v.has_wh) {
-    v.wh_mean = c.take(size_t(v.d) * 8, "whitening mean");
-    v.wh_fwd = c.take(size_t(v.d) * size_t(v.d) * 8, "whitening forward");
-    v.wh_inv = c.take(size_t(v.d) * size_t(v.d) * 8, "whitening inverse");
+    v.wh_mean = c.take(nb(size_t(v.d), 8), "whitening mean");
+    v.wh_fwd = c.take(nb(nb(size_t(v.d), size_t(v.d)), 8), "whitening forward");
+    v.wh_inv = c.take(nb(nb(size_t(v.d), size_t(v.d)), 8), "whitening inverse");
   }
   return v;
 }
@@ -182,9 +191,9 @@ CsrView parse_sres(Cursor c) {
   v.rows = int64_t(ld<uint64_t>(h));
   v.nnz = int64_t(ld<uint64_t>(h + 8));
   if (v.rows < 0 || v.nnz < 0) fail(HS_FMT_EINVAL, "residual header out of range");
-  v.indptr = c.take(size_t(v.rows + 1) * 8, "residual indptr");
-  v.indices = c.take(size_t(v.nnz) * 4, "residual indices");
-  v.data = c.take(size_t(v.nnz) * 4, "residual data");
+  v.indptr = c.take(nb(size_t(v.rows) + 1, 8), "residual indptr");
+  v.indices = c.take(nb(size_t(v.nnz), 4), "residual indices");
+  v.data = c.take(nb(size_t(v.nnz), 4), "residual data");
   return v;
 }
 
@@ -215,13 +224,13 @@ void parse_hybx(hs_file* f, Cursor c) {
   f->d_dense = int64_t(ld<uint32_t>(h + 20));
   if (version != 1) fail(HS_FMT_EBADVERSION, "unsupported dataset version " + std::to_string(version));
   if (f->n < 0) fail(HS_FMT_ETRUNCATED, "truncated file while reading dense block");
-  f->ds_dense = c.take(size_t(f->n) * size_t(f->d_dense) * 4, "dense block");
+  f->ds_dense = c.take(nb(nb(size_t(f->n), size_t(f->d_dense)), 4), "dense block");
   f->csr.rows = f->n;
-  f->csr.indptr = c.take(size_t(f->n + 1) * 8, "csr offsets");
+  f->csr.indptr = c.take(nb(size_t(f->n) + 1, 8), "csr offsets");
   f->csr.nnz = int64_t(ld<uint64_t>(f->csr.indptr + 8 * f->n));
   if (f->csr.nnz < 0) fail(HS_FMT_ETRUNCATED, "truncated file while reading csr indices");
-  f->csr.indices = c.take(size_t(f->csr.nnz) * 4, "csr indices");
-  f->csr.data = c.take(size_t(f->csr.nnz) * 4, "csr values");
+  f->csr.indices = c.take(nb(size_t(f->csr.nnz), 4), "csr indices");
+  f->csr.data = c.take(nb(size_t(f->csr.nnz), 4), "csr values");
   f->has_residual = true;
 }
 
@@ -422,8 +431,8 @@ int hs_file_read_csr(hs_file_t f, int64_t* indptr, int32_t* indices, float* data
     return HS_FMT_EINVAL;
   }
   const CsrView& v = f->csr;
-  std::memcpy(indptr, v.indptr, size_t(v.rows + 1) * 8);
-  std::memcpy(data, v.data, size_t(v.nnz) * 4);
+  std::memcpy(indptr, v.indptr, nb(size_t(v.rows) + 1, 8));
+  std::memcpy(data, v.data, nb(size_t(v.nnz), 4));
 #pragma omp parallel for schedule(static) if (v.nnz > (1 << 20))
   for (int64_t i = 0; i < v.nnz; ++i) indices[i] = int32_t(ld<uint32_t>(v.indices + 4 * i));
   return HS_FMT_OK;
@@ -467,7 +476,7 @@ int hs_file_read_dataset_dense(hs_file_t f, float* dense) {
     g_err = "not a dataset file (or null output)";
     return HS_FMT_EINVAL;
   }
-  std::memcpy(dense, f->ds_dense, size_t(f->n) * size_t(f->d_dense) * 4);
+  std::memcpy(dense, f->ds_dense, nb(nb(size_t(f->n), size_t(f->d_dense)), 4));
   return HS_FMT_OK;
 }
 

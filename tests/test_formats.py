@@ -185,3 +185,17 @@ def test_file_to_device_search_matches_reference(tag):
         assert np.stack([r.ids for r in res]).tolist() == z[f"{tag}_s{si}_ids"].tolist(), (tag, si)
         np.testing.assert_allclose(np.stack([r.scores for r in res]), z[f"{tag}_s{si}_scores"],
                                    rtol=1e-12, atol=1e-14)
+
+
+@pytest.mark.gpu
+def test_corrupt_index_rejected_before_upload():
+    """A posting id or layout slot outside [0, n) (a damaged file) is refused
+    by hs_index_create instead of being dereferenced on the device."""
+    idx = hs.load_index(path("default.hidx"))
+    idx.sparse_index.ids[3] = idx.n + 5
+    with pytest.raises(ValueError, match="posting id out of range"):
+        hs.DeviceIndex(idx, device=0)
+    idx = hs.load_index(path("default.hidx"))
+    idx.order[0] = idx.n
+    with pytest.raises(ValueError, match="layout order out of range"):
+        hs.DeviceIndex(idx, device=0)
