@@ -69,12 +69,16 @@ void free_device_arrays(DeviceIndex* ix) {
   if (ix->aux) cudaStreamDestroy(ix->aux);
   if (ix->ev_fork) cudaEventDestroy(ix->ev_fork);
   if (ix->ev_join) cudaEventDestroy(ix->ev_join);
+  if (ix->ev_done) cudaEventDestroy(ix->ev_done);
+  for (cudaEvent_t e : ix->evpool) cudaEventDestroy(e);
+  ix->evpool.clear();
 }
 
 int ensure_scratch(DeviceIndex& ix, size_t bytes) {
   if (bytes <= ix.scratch_bytes) return HS_OK;
   if (ix.scratch) {
     HS_CUDA(cudaStreamSynchronize(ix.stream));
+    if (ix.ev_done) HS_CUDA(cudaEventSynchronize(ix.ev_done));
     cudaFree(ix.scratch);
     ix.scratch = nullptr;
     ix.scratch_bytes = 0;
@@ -118,51 +122,66 @@ int resolve_sizes(const DeviceIndex& ix, const hs_search_params* p, Sizes* s) {
 constexpr int64_t kMaxRerank = 8192;  // k1/k2 held in shared memory for stages 2-3
 constexpr int64_t kTcMinQueries = 64;  // batches at least this large use the tensor cores
 
-// time accumulation helpers
+// time accumulation helpers.  Two modes: FULL records an event after every
+// kernel (the bench's per-kernel breakdown; it serialises the aux-stream
+// overlap), STAGE records only the stage boundaries StageStats needs (three
+// events per chunk, overlap kept).  Events come from a per-index pool.
+enum TimerMode { TM_OFF = 0, TM_STAGE = 1, TM_FULL = 2 };
 struct Timer {
   DeviceIndex* ix;
   cudaStream_t st;
-  std::vector<cudaEvent_t> evs;
+  int mode;
+  size_t used = 0;
   std::vector<std::string> names;
-  bool on;
-  Timer(DeviceIndex* ix_, cudaStream_t st_, bool on_) : ix(ix_), st(st_), on(on_) {}
-  void mark(const char* name) {
-    if (!on) return;
-    cudaEvent_t e;
-    cudaEventCreate(&e);
-    cudaEventRecord(e, st);
-    evs.push_back(e);
+  Timer(DeviceIndex* ix_, cudaStream_t st_, int mode_) : ix(ix_), st(st_), mode(mode_) {}
+  bool full() const { return mode == TM_FULL; }
+  void record(const char* name) {
+    if (used == ix->evpool.size()) {
+      cudaEvent_t e;
+      if (cudaEventCreate(&e) != cudaSuccess) return;
+      ix->evpool.push_back(e);
+    }
+    cudaEventRecord(ix->evpool[used++], st);
     names.push_back(name ? name : "");
+  }
+  // per-kernel mark (FULL only)
+  void mark(const char* name) {
+    if (mode == TM_FULL) record(name);
+  }
+  // stage boundary: "begin", "stage1" (end of stage 1), "stage2", "stage3"
+  void boundary(const char* name) {
+    if (mode == TM_STAGE || (mode == TM_FULL && std::strcmp(name, "stage1") != 0)) record(name);
   }
   // names[i] labels the interval (evs[i-1], evs[i])
   void finish(double* stage_seconds) {
-    if (!on || evs.empty()) return;
-    cudaEventSynchronize(evs.back());
-    ix->tnames.clear();
-    ix->tms.clear();
+    if (mode == TM_OFF || used == 0) return;
+    cudaEventSynchronize(ix->evpool[used - 1]);
+    if (mode == TM_FULL) {
+      ix->tnames.clear();
+      ix->tms.clear();
+    }
     double st3[3] = {0, 0, 0};
-    for (size_t i = 1; i < evs.size(); ++i) {
+    for (size_t i = 1; i < used; ++i) {
       float ms = 0.f;
-      cudaEventElapsedTime(&ms, evs[i - 1], evs[i]);
+      cudaEventElapsedTime(&ms, ix->evpool[i - 1], ix->evpool[i]);
       const std::string& nm = names[i];
-      auto it = std::find(ix->tnames.begin(), ix->tnames.end(), nm);
-      if (it == ix->tnames.end()) {
-        ix->tnames.push_back(nm);
-        ix->tms.push_back(ms);
-      } else {
-        ix->tms[it - ix->tnames.begin()] += ms;
+      if (mode == TM_FULL) {
+        auto it = std::find(ix->tnames.begin(), ix->tnames.end(), nm);
+        if (it == ix->tnames.end()) {
+          ix->tnames.push_back(nm);
+          ix->tms.push_back(ms);
+        } else {
+          ix->tms[it - ix->tnames.begin()] += ms;
+        }
       }
-      if (nm == "map_dims" || nm == "lut_build" || nm == "sparse_bucket" || nm == "lut16_tc" ||
-          nm == "stage1" || nm == "merge" || nm == "sample" || nm == "fuse" || nm == "fuse_select" ||
-          nm == "fallback")
-        st3[0] += ms;
-      else if (nm == "stage2") st3[1] += ms;
+      if (nm == "stage2") st3[1] += ms;
       else if (nm == "stage3") st3[2] += ms;
+      else if (nm != "begin") st3[0] += ms;
     }
     if (stage_seconds)
       for (int i = 0; i < 3; ++i) stage_seconds[i] = st3[i] * 1e-3;
-    for (auto e : evs) cudaEventDestroy(e);
-    evs.clear();
+    used = 0;
+    names.clear();
   }
 };
 
@@ -174,6 +193,9 @@ int run_search(DeviceIndex& ix, const hs_query_batch& qb, int64_t nnz, int max_q
   HS_CHECK(resolve_sizes(ix, params, &sz));
   const int64_t nq = qb.nq;
   if (nq <= 0 || sz.kh <= 0) return HS_OK;
+  // every search carves the same scratch arena: a call on another stream
+  // must not start before the previous call's kernels are done with it
+  if (ix.ev_done) HS_CUDA(cudaStreamWaitEvent(st, ix.ev_done, 0));
   if (ix.d_dense > 0 && ix.K == 0) HS_FAIL(HS_EINVAL, "index has no dense PQ codes");
   if (ix.d_dense > 0 && ix.l != 16) HS_FAIL(HS_EUNSUPPORTED, "lut16_scan requires 16-center codes");
   if (params->exact_final_rerank && !ix.has_ds)
@@ -194,7 +216,7 @@ int run_search(DeviceIndex& ix, const hs_query_batch& qb, int64_t nnz, int max_q
   const bool sparse_part = nnz > 0 && ix.nnz_post > 0;
   // bucketing overlapped with the dense chain on the aux stream (not while
   // timing: the per-kernel breakdown needs the serial order)
-  const bool overlap = use_buckets && ix.aux != nullptr && !(tm && tm->on) &&
+  const bool overlap = use_buckets && ix.aux != nullptr && !(tm && tm->full()) &&
                        !getenv_flag("HSB200_NO_OVERLAP");
   // sample size of the threshold pass and capacity of the filtered lists
   // (HSB200_FUSE_SAMPLE / HSB200_FUSE_CAP: test knobs that shrink the sample
@@ -365,7 +387,7 @@ int run_search(DeviceIndex& ix, const hs_query_batch& qb, int64_t nnz, int max_q
   SparseBuckets sb = P.sb;
   uint16_t* tot16 = P.tot16;
 
-  if (tm) tm->mark("begin");
+  if (tm) tm->boundary("begin");
   QueryView all;
   all.nq = nq;
   all.sp_indptr = qb.sp_indptr;
@@ -481,15 +503,17 @@ int run_search(DeviceIndex& ix, const hs_query_batch& qb, int64_t nnz, int max_q
       if (tm) tm->mark("merge");
     }
     HS_CHECK(join_sb());
+    if (tm) tm->boundary("stage1");
     ix.launches += 2;  // stage2, stage3
     launch_stage2(ix, cand1, nqc, (int)sz.k1, (int)sz.k2, qw, cand2, st);
     HS_CUDA(cudaGetLastError());
-    if (tm) tm->mark("stage2");
+    if (tm) tm->boundary("stage2");
     launch_stage3(ix, qc, cand2, nqc, (int)sz.k2, (int)sz.kh, params->exact_final_rerank ? 1 : 0,
                   max_qnnz, qd, d_ids + q0 * sz.kh, d_scores + q0 * sz.kh, st);
     HS_CUDA(cudaGetLastError());
-    if (tm) tm->mark("stage3");
+    if (tm) tm->boundary("stage3");
   }
+  if (ix.ev_done) HS_CUDA(cudaEventRecord(ix.ev_done, st));
   if (check_lut && d > 0) {
     std::vector<int> hb(QB);
     HS_CUDA(cudaMemcpyAsync(hb.data(), bad, sizeof(int) * QB, cudaMemcpyDeviceToHost, st));
@@ -511,9 +535,11 @@ struct DevQueries {
   char* out_host = nullptr;  // pinned host mirror of it
 };
 
-int grow(void** p, size_t* have, size_t want, bool host, cudaStream_t st) {
+int grow(void** p, size_t* have, size_t want, bool host, cudaStream_t st,
+         cudaEvent_t done = nullptr) {
   if (want <= *have) return HS_OK;
   HS_CUDA(cudaStreamSynchronize(st));
+  if (done) HS_CUDA(cudaEventSynchronize(done));
   if (*p) host ? cudaFreeHost(*p) : cudaFree(*p);
   *p = nullptr;
   *have = 0;
@@ -548,8 +574,8 @@ int upload_queries(DeviceIndex& ix, const hs_query_batch* q, DevQueries* out, bo
   const size_t o_dense = (size_t)lay.take<float>(nq * ix.d_dense + 1);
   const size_t in_bytes = lay.off;
   const size_t o_out = (size_t)lay.take<char>(result_bytes + 1);
-  HS_CHECK(grow(&ix.io_dev, &ix.io_dev_bytes, lay.off, false, ix.stream));
-  HS_CHECK(grow(&ix.io_host, &ix.io_host_bytes, lay.off, true, ix.stream));
+  HS_CHECK(grow(&ix.io_dev, &ix.io_dev_bytes, lay.off, false, ix.stream, ix.ev_done));
+  HS_CHECK(grow(&ix.io_host, &ix.io_host_bytes, lay.off, true, ix.stream, ix.ev_done));
   char* hb = static_cast<char*>(ix.io_host);
   char* db = static_cast<char*>(ix.io_dev);
   int64_t* hp = reinterpret_cast<int64_t*>(hb + o_ptr);
@@ -630,8 +656,29 @@ int hs_index_create(const hs_index_desc* ds, int device, hs_index_t* out) {
     if ((int64_t)ds->post_dims[a] >= ds->d_sparse) HS_FAIL(HS_EINVAL, "posting dimension out of range");
     if (ds->post_ptr[a + 1] < ds->post_ptr[a]) HS_FAIL(HS_EINVAL, "posting offsets not ascending");
   }
+  if (ds->n_active > 0 && ds->post_ptr[0] != 0) HS_FAIL(HS_EINVAL, "posting offsets must start at 0");
   for (int64_t e = 0; e < nnz_post; ++e)
     if ((int64_t)ds->post_ids[e] >= ds->n) HS_FAIL(HS_EINVAL, "posting id out of range");
+  // CSR row pointers the rerank kernels dereference (scipy's csr_matrix only
+  // checks the first and last entry): start at 0, monotone, columns in range
+  auto check_csr = [&](const int64_t* indptr, const uint32_t* indices, const char* what) -> int {
+    if (!indptr || ds->n == 0) return HS_OK;
+    if (indptr[0] != 0) HS_FAIL(HS_EINVAL, std::string(what) + " row pointers must start at 0");
+    for (int64_t i = 0; i < ds->n; ++i)
+      if (indptr[i + 1] < indptr[i]) HS_FAIL(HS_EINVAL, std::string(what) + " row pointers not monotone");
+    const int64_t nnz = indptr[ds->n];
+    if (nnz > 0 && !indices) HS_FAIL(HS_EINVAL, std::string(what) + " column indices missing");
+    for (int64_t e = 0; e < nnz; ++e)
+      if ((int64_t)indices[e] >= ds->d_sparse)
+        HS_FAIL(HS_EINVAL, std::string(what) + " column index out of range");
+    return HS_OK;
+  };
+  HS_CHECK(check_csr(ds->res_indptr, ds->res_indices, "sparse residual"));
+  if (ds->has_dataset) {
+    if (!ds->ds_indptr) HS_FAIL(HS_EINVAL, "dataset row pointers missing");
+    HS_CHECK(check_csr(ds->ds_indptr, ds->ds_indices, "dataset"));
+    if (ds->d_dense > 0 && !ds->ds_dense) HS_FAIL(HS_EINVAL, "dataset dense part missing");
+  }
   HS_CUDA(cudaSetDevice(device));
   std::unique_ptr<hs_index, void (*)(hs_index*)> ix(new hs_index(), [](hs_index* p) {
     hs::free_index(p);
@@ -647,6 +694,7 @@ int hs_index_create(const hs_index_desc* ds, int device, hs_index_t* out) {
   HS_CUDA(cudaStreamCreateWithFlags(&ix->aux, cudaStreamNonBlocking));
   HS_CUDA(cudaEventCreateWithFlags(&ix->ev_fork, cudaEventDisableTiming));
   HS_CUDA(cudaEventCreateWithFlags(&ix->ev_join, cudaEventDisableTiming));
+  HS_CUDA(cudaEventCreateWithFlags(&ix->ev_done, cudaEventDisableTiming));
   const int64_t n = ds->n;
   const int T = 256;
 
@@ -808,7 +856,7 @@ int hs_search_batch(hs_index_t index, const hs_query_batch* queries,
   HS_CHECK(upload_queries(*index, queries, &dq, true, ids_bytes + sizeof(double) * total));
   int64_t* d_ids = reinterpret_cast<int64_t*>(dq.out);
   double* d_sc = reinterpret_cast<double*>(dq.out + ids_bytes);
-  Timer tm(index, index->stream, index->timing);
+  Timer tm(index, index->stream, index->timing ? TM_FULL : TM_STAGE);
   int rc = run_search(*index, dq.b, dq.nnz, dq.max_row, params, d_ids, d_sc, index->stream, &tm,
                       true);
   cudaError_t e = cudaSuccess;
@@ -840,7 +888,7 @@ int hs_search_batch_dev(hs_index_t index, const hs_query_batch* queries,
   if (!index->timing_dev)
     return run_search(*index, *queries, nnz, max_row, params, d_out_ids, d_out_scores, st,
                       nullptr);
-  Timer tm(index, st, true);
+  Timer tm(index, st, TM_FULL);
   const int rc =
       run_search(*index, *queries, nnz, max_row, params, d_out_ids, d_out_scores, st, &tm);
   tm.finish(nullptr);
@@ -850,6 +898,7 @@ int hs_search_batch_dev(hs_index_t index, const hs_query_batch* queries,
 int hs_set_timing(hs_index_t index, int on) {
   if (!index) HS_FAIL(HS_EINVAL, "null index");
   index->timing_dev = on != 0;
+  index->timing = on != 0;
   return HS_OK;
 }
 

@@ -52,7 +52,6 @@ struct SubTab {  // per-subspace geometry (device arrays)
   const int32_t* dim_off;   // [K]
   const int32_t* width;     // [K] 1 or 2
   const int32_t* cen_off;   // [K] float offset of centers[k]
-  const double* csq;        // [K][16] |c|^2 in the host recipe
 };
 
 constexpr int kTile = 32;  // layout slots per tile
@@ -114,8 +113,9 @@ k_pq_encode_pack(const double* __restrict__ vec, int64_t n, int64_t d,
   unsigned long long* s_lo = reinterpret_cast<unsigned long long*>(s_c + (size_t)npad * 16);  // [d]
   unsigned long long* s_hi = s_lo + d;                                   // [d]
   uint8_t* s_tile = reinterpret_cast<uint8_t*>(s_hi + d);                // [npairs][kTile]
-  // centers and |c|^2 at [c][k & 1][k >> 1]: the lanes of a warp (consecutive
-  // pairs) read consecutive entries, no bank conflicts
+  // f32 centers at [c][k & 1][k >> 1] (|c|^2 is recomputed in f64 from them):
+  // the lanes of a warp (consecutive pairs) read consecutive entries, no bank
+  // conflicts
   const int cstride = 2 * npairs;
   for (int e = threadIdx.x; e < K * 16; e += blockDim.x) {
     const int k = e >> 4, c = e & 15, w = t.width[k];
@@ -311,7 +311,6 @@ extern "C" int hs_dense_encode(const double* vec, int64_t n, int64_t d, const in
     HS_FAIL(HS_EINVAL, "hs_dense_encode: bad arguments");
   if (l != 16) HS_FAIL(HS_EUNSUPPORTED, "hs_dense_encode: only 16-center (4-bit) codebooks");
   std::vector<int32_t> dim_off(K), width(K), cen_off(K), dim_k(d), dim_t(d);
-  std::vector<double> csq((size_t)K * 16);
   int64_t o = 0, co = 0;
   for (int32_t k = 0; k < K; ++k) {
     if (subdims[k] < 1 || subdims[k] > 2)
@@ -324,14 +323,6 @@ extern "C" int hs_dense_encode(const double* vec, int64_t n, int64_t d, const in
       dim_k[o + t] = k;
       dim_t[o + t] = (int32_t)t;
     }
-    for (int c = 0; c < 16; ++c) {  // hostbuild.cpp hsb_pq_encode's |c|^2
-      double s = 0.0;
-      for (int64_t t = 0; t < subdims[k]; ++t) {
-        const double v = (double)centers[co + c * subdims[k] + t];
-        s = s + v * v;
-      }
-      csq[(size_t)k * 16 + c] = s;
-    }
     o += subdims[k];
     co += subdims[k] * 16;
   }
@@ -339,7 +330,7 @@ extern "C" int hs_dense_encode(const double* vec, int64_t n, int64_t d, const in
   HS_CUDA(cudaSetDevice(device));
   const int npairs = (K + 1) / 2;
   DBufs b;
-  double *dvec, *dcsq, *dlo, *dsafe;
+  double *dvec, *dlo, *dsafe;
   int64_t* dord;
   int32_t *ddo, *dw, *dco, *ddk, *ddt;
   float* dcen;
@@ -352,7 +343,6 @@ extern "C" int hs_dense_encode(const double* vec, int64_t n, int64_t d, const in
   HS_CUDA(b.upload(&dco, cen_off.data(), K));
   HS_CUDA(b.upload(&ddk, dim_k.data(), (size_t)d));
   HS_CUDA(b.upload(&ddt, dim_t.data(), (size_t)d));
-  HS_CUDA(b.upload(&dcsq, csq.data(), csq.size()));
   HS_CUDA(b.upload(&dcen, centers, (size_t)co));
   HS_CUDA(b.alloc(&dpk, (size_t)(npairs * n)));
   HS_CUDA(b.alloc(&dpm, (size_t)(npairs * n)));
@@ -367,7 +357,7 @@ extern "C" int hs_dense_encode(const double* vec, int64_t n, int64_t d, const in
   HS_CUDA(cudaEventCreate(&e1));
   HS_CUDA(cudaEventRecord(e0));
   if (n > 0) {
-    SubTab t{ddo, dw, dco, dcsq};
+    SubTab t{ddo, dw, dco};
     const size_t smem = (size_t)(2 * npairs) * 16 * sizeof(float2) +
                         2 * sizeof(unsigned long long) * (size_t)d + (size_t)npairs * kTile;
     const int64_t ntiles = (n + kTile - 1) / kTile;

@@ -268,7 +268,15 @@ void parse_hidx(hs_file* f, Cursor c) {
     f->has_dense = true;
   }
   // n / d_sparse / d_dense come from META in the reference; the blobs agree
-  // for files it wrote, and the Python layer reads META for the config.
+  // for files it wrote, and the Python layer cross-checks META against them.
+  // The blobs must agree with each other: every array the device index
+  // uploads is sized by the sparse index's n.
+  if (f->csr.rows != f->sp.n)
+    fail(HS_FMT_EINVAL, "residual rows (" + std::to_string(f->csr.rows) +
+                            ") do not match the sparse index (" + std::to_string(f->sp.n) + ")");
+  if (f->has_dense && f->dn.n != f->sp.n)
+    fail(HS_FMT_EINVAL, "dense index rows (" + std::to_string(f->dn.n) +
+                            ") do not match the sparse index (" + std::to_string(f->sp.n) + ")");
   f->n = f->sp.n;
   f->d_sparse = f->sp.d;
   f->d_dense = f->has_dense ? f->dn.d : 0;

@@ -67,6 +67,9 @@ struct DeviceIndex {
   // runs concurrently with its LUT build and sample pass
   cudaStream_t aux = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  // recorded at the end of every search: the next search (any stream) waits
+  // on it before reusing the scratch arena
+  cudaEvent_t ev_done = nullptr;
   std::mutex mu;
 
   // scratch arena (grown on demand, owned by the handle)
@@ -80,8 +83,9 @@ struct DeviceIndex {
   size_t io_host_bytes = 0;
 
   // per-kernel timing of the last batch (CUDA events; bench roofline)
-  bool timing = true;      // host entry point
+  bool timing = false;      // host entry point: per-kernel events (else stage events only)
   bool timing_dev = false;  // _dev entry point (adds a sync)
+  std::vector<cudaEvent_t> evpool;  // reused timing events
   int64_t launches = 0;
   std::vector<std::string> tnames;
   std::vector<double> tms;

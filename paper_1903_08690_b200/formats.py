@@ -333,6 +333,13 @@ def load_index(path, dataset: HybridDataset | None = None) -> HybridIndex:
         _check(_lib().hs_file_read_meta(f.h, raw))
         meta = json.loads(raw.raw[:fi.meta_len].decode())
         config = HybridIndexConfig(**meta["config"])
+        # META against the blobs: the device upload sizes every array by n
+        if (int(meta["n"]) != int(fi.n) or int(meta["d_sparse"]) != int(fi.d_sparse)
+                or int(meta["d_dense"]) != int(fi.d_dense)):
+            raise FormatError(
+                f"META (n={meta['n']}, d_sparse={meta['d_sparse']}, d_dense={meta['d_dense']}) "
+                f"does not match the index sections (n={fi.n}, d_sparse={fi.d_sparse}, "
+                f"d_dense={fi.d_dense})")
         sparse_index = f.sparse_index()
         residual = f.csr(meta["d_sparse"])
         dense_index = f.dense_index() if fi.has_dense else None

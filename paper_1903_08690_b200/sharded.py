@@ -111,6 +111,7 @@ class ShardedSearcher:
         counts = np.zeros(3, dtype=np.int64)
         nat.check(nat.lib().hs_result_sizes(dev.handle, p, nat.ptr(counts)))
         kh = int(counts[2])
+        self._last_counts = [int(counts[0]), int(counts[1]), kh]
         q = query_arrays(queries, int(idx.d_dense))
         d = torch.device("cuda", self.device or 0)
         t = [torch.as_tensor(q.indptr).to(d), torch.as_tensor(q.dims.view(np.int32)).to(d),
@@ -151,6 +152,15 @@ class ShardedSearcher:
         sc = torch.as_tensor(sc)
         world = self.dist.get_world_size(self.group)
         nq, kh = ids.shape
+        if kh < h:
+            # a shard smaller than h (k2 is capped by the shard's n) returns
+            # fewer columns: pad to h (-1 / -inf, dropped by the merge) so
+            # every rank contributes the same shape to the all-gather
+            pad_i = torch.full((nq, h - kh), -1, dtype=ids.dtype, device=ids.device)
+            pad_s = torch.full((nq, h - kh), -np.inf, dtype=sc.dtype, device=sc.device)
+            ids = torch.cat([ids, pad_i], dim=1)
+            sc = torch.cat([sc, pad_s], dim=1)
+            kh = h
         g_ids = torch.empty((world, nq, kh), dtype=ids.dtype, device=ids.device)
         g_sc = torch.empty((world, nq, kh), dtype=sc.dtype, device=sc.device)
         if ids.is_cuda:  # NCCL: one collective into the stacked buffer
@@ -167,8 +177,11 @@ class ShardedSearcher:
             mi, ms = self._gpu_merge(g_ids, g_sc, h)
             mi, ms = mi.cpu().numpy(), ms.cpu().numpy()
         out = []
+        local = getattr(self, "_last_counts", None)
         for i in range(nq):
             keep = mi[i] >= 0
+            cands = ([local[0], local[1], int(keep.sum())] if local is not None
+                     else [int(keep.sum())] * 3)
             out.append(SearchResult(ids=mi[i][keep], scores=ms[i][keep],
-                                    stages=StageStats(candidates=[], seconds=[])))
+                                    stages=StageStats(candidates=cands, seconds=[0.0, 0.0, 0.0])))
         return out

@@ -199,3 +199,35 @@ def test_corrupt_index_rejected_before_upload():
     idx.order[0] = idx.n
     with pytest.raises(ValueError, match="layout order out of range"):
         hs.DeviceIndex(idx, device=0)
+
+
+def test_meta_must_match_the_sections(tmp_path):
+    """A hand-edited META n (the loop bound of the device upload) that
+    disagrees with the section arrays is rejected at load time."""
+    b = raw("default.hidx")
+    assert b.count(b'"n": 3000') == 1
+    p = tmp_path / "meta.hidx"
+    p.write_bytes(b.replace(b'"n": 3000', b'"n": 9000'))
+    with pytest.raises(hs.FormatError, match="does not match the index sections"):
+        hs.load_index(p)
+
+
+@pytest.mark.gpu
+def test_corrupt_csr_rejected_before_upload():
+    """Residual / dataset CSR row pointers that are not monotone (scipy only
+    checks the first and last entry) are refused by hs_index_create."""
+    import scipy.sparse as sp
+
+    idx = hs.load_index(path("default.hidx"))
+    r = idx.sparse_residual
+    ptr = r.indptr.copy()
+    ptr[2], ptr[3] = ptr[3] + 5, ptr[2]
+    idx.sparse_residual = sp.csr_matrix((r.data, r.indices, ptr), shape=r.shape)
+    with pytest.raises(ValueError, match="sparse residual row pointers not monotone"):
+        hs.DeviceIndex(idx, device=0)
+    idx = hs.load_index(path("default.hidx"))
+    r = idx.sparse_residual
+    idx.sparse_residual = sp.csr_matrix((r.data, r.indices, r.indptr), shape=r.shape)
+    idx.sparse_residual.indices[0] = idx.d_sparse + 1
+    with pytest.raises(ValueError, match="sparse residual column index out of range"):
+        hs.DeviceIndex(idx, device=0)

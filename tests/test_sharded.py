@@ -59,16 +59,26 @@ def _oracle_local(shard, queries, h, overrides):
     return ids, sc
 
 
-def _worker(rank, world, port, out_q):
+def _small_data():
+    """40 points over two ranks with h=30: each 20-point shard returns
+    kh = 20 < h columns (k1 is capped by the shard's n)."""
+    from paper_1903_08690_b200 import synth
+
+    ds, qs, cfg = synth.make_config("cfg1", n=40, n_queries=4)
+    return ds, qs
+
+
+def _worker(rank, world, port, out_q, small=False):
     import torch.distributed as dist
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        ds, qs = _data()
+        ds, qs = _small_data() if small else _data()
+        h = 30 if small else 10
         shard = sharded.build_shard(ds, hs.HybridIndexConfig(**CFG), rank, world)
         s = sharded.ShardedSearcher(shard, local_search=_oracle_local, merge=sharded.merge_host)
-        res = s.search_batch(qs, 10, overfetch=5.0, retain=3.0, exact_final_rerank=True)
+        res = s.search_batch(qs, h, overfetch=5.0, retain=3.0, exact_final_rerank=True)
         out_q.put((rank, [r.ids.tolist() for r in res], [r.scores.tolist() for r in res]))
     finally:
         dist.destroy_process_group()
@@ -137,3 +147,40 @@ def test_two_shards_on_one_gpu_device_merge():
     ei, es = sharded.merge_host(np.stack([x[0] for x in ids_l]), np.stack([x[1] for x in ids_l]), 10)
     assert mi.cpu().numpy().tolist() == ei.tolist()
     np.testing.assert_allclose(ms.cpu().numpy(), es, rtol=1e-12)
+
+
+def test_two_rank_gloo_shards_smaller_than_h():
+    """Ranks whose shard holds fewer than h points pad their local results to
+    h columns before the all-gather (equal shapes on every rank)."""
+    import multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q, True)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = []
+    try:
+        got = [q.get(timeout=240) for _ in procs]
+    finally:
+        for p in procs:
+            p.join(timeout=60)
+            if p.is_alive():
+                p.kill()
+    assert all(p.exitcode == 0 for p in procs)
+    got.sort()
+    assert got[0][1] == got[1][1]
+    ds, qs = _small_data()
+    ids_l, sc_l = [], []
+    for r in range(2):
+        shard = sharded.build_shard(ds, hs.HybridIndexConfig(**CFG), r, 2)
+        i, s = _oracle_local(shard, qs, 30, dict(overfetch=5.0, retain=3.0,
+                                                 exact_final_rerank=True))
+        assert i.shape[1] == 20
+        pad = np.full((qs.n, 10), -1, dtype=np.int64)
+        ids_l.append(np.concatenate([i, pad], axis=1))
+        sc_l.append(np.concatenate([s, np.full((qs.n, 10), -np.inf)], axis=1))
+    mi, ms = sharded.merge_host(np.stack(ids_l), np.stack(sc_l), 30)
+    assert got[0][1] == [row[row >= 0].tolist() for row in mi]
+    assert all(len(row) == 30 for row in got[0][1])  # 2 x 20 candidates cover h
