@@ -26,6 +26,8 @@
  *   hs_shard_merge_dev   <- (new) top-h merge of per-shard results; no reference counterpart
  *   hs_dense_encode      <- build_index's dense part: pq_encode(...)[order] + pack_codes +
  *                           sq_encode(residual)   pipeline.py:142-157, dense.py:138-170, 381-390
+ *   hs_builder_*         <- build_index on the GPU (+ the BASELINE data generator),
+ *                           see the section at the end of this header
  */
 #ifndef HSB200_H
 #define HSB200_H
@@ -191,6 +193,72 @@ int hs_dense_encode(const double* vec, int64_t n, int64_t d, const int64_t* orde
                     int32_t K, const int64_t* subdims, const float* centers, int32_t l,
                     uint8_t* packed, float* sq_lo, float* sq_step, uint8_t* sq_codes,
                     int device, double* seconds);
+
+/* ---- GPU index build and the on-device data generator ----
+ * A builder holds one dataset resident on a GPU — generated there
+ * (hs_builder_generate) or uploaded (hs_builder_upload) — and builds the
+ * index products in place, following build_index (pipeline.py:119-162):
+ *   hs_builder_sparse        <- prune_split + cache_sort + build_inverted
+ *                               (sparse.py:66-163, 219-235): thresholds, data-part
+ *                               flags, layout order, postings — integer products
+ *                               identical to the reference's
+ *   hs_builder_dense_moments <- whiten_fit's mean and covariance (dense.py:333-348;
+ *                               the d x d eigendecomposition stays on the host)
+ *   hs_builder_gather_dense  <- the k-means training sample (dense.py:126-129),
+ *                               whitened (dense.py:351-357)
+ *   hs_builder_dense_encode  <- pq_encode(...)[order] + pack_codes + sq_encode of the
+ *                               residual (pipeline.py:152-157, dense.py:138-170, 381-390)
+ *   hs_builder_finish        -> an hs_index_t (the builder's arrays move into it)
+ * Rows of a generated dataset are keyed by their global id (row0 + i), so the
+ * id-range shards of a multi-GPU job generate exactly the rows of the full set. */
+typedef struct hs_builder* hs_builder_t;
+
+typedef struct {
+  int64_t n;            /* rows generated: global ids [row0, row0 + n) */
+  int64_t d_sparse;
+  int64_t d_dense;
+  double mean_nnz;      /* Poisson mean of the distinct sparse nonzeros per row */
+  double zipf_s;        /* Zipf exponent of the dimension ranks (> 1) */
+  int32_t value_law;    /* 0: |N(0,1)|, 1: lognormal(0,1) */
+  int32_t dense_fp16;   /* store the normalised dense part as fp16 */
+  uint64_t seed;        /* data seed */
+  uint64_t perm_seed;   /* seed of the rank -> dim bijection (shared with queries) */
+  int64_t row0;
+} hs_gen_params;
+
+int hs_builder_generate(const hs_gen_params* p, int device, hs_builder_t* out);
+int hs_builder_upload(int64_t n, int64_t d_sparse, int64_t d_dense, const int64_t* indptr,
+                      const uint32_t* indices, const float* data, const float* dense,
+                      int32_t dense_fp16, int device, hs_builder_t* out);
+void hs_builder_destroy(hs_builder_t b);
+/* info[8] = {n, d_sparse, d_dense, nnz, n_active, nnz_post, n_head, dense_fp16} */
+int hs_builder_info(hs_builder_t b, int64_t* info);
+int hs_builder_phase_times(hs_builder_t b, double* sec, int32_t max_entries,
+                           int32_t* n_entries, char* names, int32_t names_cap);
+int hs_builder_download_rows(hs_builder_t b, int64_t lo, int64_t hi, int64_t* indptr,
+                             uint32_t* indices, float* data, float* dense);
+/* top_t < 0: top_t=None with the constant data_min; residual_min constant */
+int hs_builder_sparse(hs_builder_t b, int64_t top_t, double data_min, double residual_min);
+int hs_builder_download_sparse(hs_builder_t b, int64_t* order, uint32_t* post_dims,
+                               int64_t* post_ptr, uint32_t* post_ids, float* post_w,
+                               uint32_t* dmask, uint32_t* head_dims, float* head_thr);
+/* column means [d] and the biased covariance [d][d] of the dense part (f64) */
+int hs_builder_dense_moments(hs_builder_t b, double* mean, double* cov);
+/* rows [m] (original ids) -> out [m][d] f64, whitened when fwd != NULL:
+ * (x - mean) @ fwd^T (whiten_apply "data", dense.py:354) */
+int hs_builder_gather_dense(hs_builder_t b, const int64_t* rows, int64_t m, const double* mean,
+                            const double* fwd, double* out);
+/* PQ codes + SQ residual in layout order; whitening (mean, fwd, inverse_t)
+ * optional (NULL = off); centers as in hs_dense_encode */
+int hs_builder_dense_encode(hs_builder_t b, int32_t K, const int32_t* subdims,
+                            const float* centers, int32_t l, const double* wh_mean,
+                            const double* wh_fwd, const double* wh_inverse_t);
+int hs_builder_download_dense(hs_builder_t b, uint8_t* packed, float* sq_lo, float* sq_step,
+                              uint8_t* sq_codes);
+/* move the products into a search index; the builder is consumed (destroyed,
+ * also on failure) */
+int hs_builder_finish(hs_builder_t b, double sparse_weight, double dense_weight,
+                      int64_t id_offset, hs_index_t* out);
 
 #ifdef __cplusplus
 }

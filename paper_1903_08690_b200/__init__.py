@@ -59,6 +59,7 @@ from .search import (  # noqa: F401
     brute_force_batch,
     brute_force_topk,
     device_index,
+    exact_topk,
     lut16_scan,
     lut16_scan_reference,
     lut16_totals,
@@ -71,4 +72,6 @@ from .search import (  # noqa: F401
     stage1_scores,
 )
 
-__version__ = "0.1.0"
+from .devbuild import DeviceBuiltIndex, DeviceDataset, GpuBuild  # noqa: F401
+
+__version__ = "0.2.0"

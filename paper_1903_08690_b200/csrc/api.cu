@@ -61,7 +61,7 @@ void free_device_arrays(DeviceIndex* ix) {
                   ix->centers,  ix->vcodes,     ix->sq_lo,    ix->sq_step,    ix->sq_codes,
                   ix->wh_mean,  ix->wh_inv_t,   ix->ds_dense, ix->ds_indptr,  ix->ds_indices,
                   ix->ds_data,  ix->scratch,    ix->skip_row, ix->skip,     ix->io_dev,
-                  ix->hcodes,   ix->pcodes};
+                  ix->hcodes,   ix->pcodes,     ix->ds_dense_h, ix->ds_dmask};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (ix->io_host) cudaFreeHost(ix->io_host);
@@ -626,6 +626,7 @@ int derive_hints(DeviceIndex& ix, const hs_query_batch* q, int64_t* nnz, int* ma
 using namespace hs;
 
 struct hs_index : public hs::DeviceIndex {};
+struct hs_builder : public hs::Builder {};
 
 namespace hs {
 static void free_index(hs_index* ix) {
@@ -1183,6 +1184,110 @@ int hs_shard_merge_dev(const int64_t* d_ids, const double* d_scores, int64_t G, 
   launch_shard_merge(d_ids, d_scores, G, nq, kh, h, d_out_ids, d_out_scores,
                      static_cast<cudaStream_t>(stream));
   HS_CUDA(cudaGetLastError());
+  return HS_OK;
+}
+
+// Move a GPU build's products into a search index (the builder is consumed).
+int hs_builder_finish(hs_builder_t bp, double sparse_weight, double dense_weight,
+                      int64_t id_offset, hs_index_t* out) {
+  std::unique_ptr<hs_builder, void (*)(hs_builder*)> b(bp, [](hs_builder* p) {
+    if (!p) return;
+    hs::builder_free(p);
+    delete p;
+  });
+  if (!b || !out) HS_FAIL(HS_EINVAL, "null argument");
+  *out = nullptr;
+  if (!b->sparse_done) HS_FAIL(HS_EINVAL, "sparse part not built");
+  if (b->d_dense > 0 && !b->dense_done) HS_FAIL(HS_EINVAL, "dense part not built");
+  HS_CUDA(cudaSetDevice(b->device));
+  HS_CUDA(cudaStreamSynchronize(b->st));
+  std::unique_ptr<hs_index, void (*)(hs_index*)> ix(new hs_index(), [](hs_index* p) {
+    hs::free_index(p);
+  });
+  const int64_t n = b->n;
+  ix->device = b->device;
+  ix->n = n;
+  ix->d_sparse = b->d_sparse;
+  ix->d_dense = b->d_dense;
+  ix->id_offset = id_offset;
+  ix->sparse_weight = sparse_weight;
+  ix->dense_weight = dense_weight;
+  HS_CUDA(cudaStreamCreateWithFlags(&ix->stream, cudaStreamNonBlocking));
+  HS_CUDA(cudaStreamCreateWithFlags(&ix->aux, cudaStreamNonBlocking));
+  HS_CUDA(cudaEventCreateWithFlags(&ix->ev_fork, cudaEventDisableTiming));
+  HS_CUDA(cudaEventCreateWithFlags(&ix->ev_join, cudaEventDisableTiming));
+  HS_CUDA(cudaEventCreateWithFlags(&ix->ev_done, cudaEventDisableTiming));
+  auto take = [&](auto*& dst, auto*& src, int64_t bytes) {
+    dst = src;
+    src = nullptr;
+    ix->bytes += bytes;
+  };
+  take(ix->order, b->order, 4 * n);
+  ix->n_active = b->n_active;
+  ix->nnz_post = b->nnz_post;
+  take(ix->post_dims, b->post_dims, 4 * b->n_active);
+  take(ix->post_ptr, b->post_ptr, 4 * (b->n_active + 1));
+  take(ix->post, b->post, 8 * (b->nnz_post + 1));
+  ix->post_wmin = b->wmin;
+  ix->post_wmax = b->wmax;
+  if (ix->nnz_post) HS_CHECK(build_skip_tables_dev(*ix));
+  // residual = the raw rows' non-data entries (no separate CSR)
+  ix->res_raw = 1;
+  ix->res_eps = b->res_eps;
+  ix->res_nnz = b->nnz - b->nnz_post;
+  take(ix->ds_dmask, b->dmask, 4 * ceil_div(b->nnz, 32));
+  if (b->d_dense > 0) {
+    const int K = b->K;
+    ix->K = K;
+    ix->l = b->l;
+    ix->Kp = (K + 1) & ~1;
+    ix->npairs = (K + 1) / 2;
+    std::vector<int32_t> doff(K), coff(K);
+    int64_t dsum = 0, csum = 0;
+    for (int k = 0; k < K; ++k) {
+      doff[k] = (int32_t)dsum;
+      coff[k] = (int32_t)csum;
+      dsum += b->subdims[k];
+      csum += (int64_t)b->subdims[k] * b->l;
+      ix->max_width = std::max(ix->max_width, b->subdims[k]);
+    }
+    HS_CHECK(dupload(*ix, &ix->subdims, b->subdims.data(), K));
+    HS_CHECK(dupload(*ix, &ix->dim_off, doff.data(), K));
+    HS_CHECK(dupload(*ix, &ix->cen_off, coff.data(), K));
+    HS_CHECK(dupload(*ix, &ix->centers, b->centers.data(), csum));
+    ix->vstride = vertical_stride(n);
+    HS_CHECK(dalloc(*ix, &ix->vcodes, (size_t)K * ix->vstride));
+    launch_to_vertical(b->packed, n, K, ix->vstride, ix->vcodes, b->st);
+    HS_CHECK(dalloc(*ix, &ix->hcodes, (size_t)ceil_div(K, 8) * n));
+    launch_to_hcodes(b->packed, n, K, ix->hcodes, b->st);
+    HS_CUDA(cudaGetLastError());
+    HS_CUDA(cudaStreamSynchronize(b->st));
+    take(ix->pcodes, b->pcodes, pcodes_row(ix->npairs) * n);
+    ix->has_sq = 1;
+    HS_CHECK(dupload(*ix, &ix->sq_lo, b->sq_lo.data(), b->d_dense));
+    HS_CHECK(dupload(*ix, &ix->sq_step, b->sq_step.data(), b->d_dense));
+    take(ix->sq_codes, b->sq, n * b->d_dense);
+    ix->has_wh = b->has_wh;
+    if (b->has_wh) {
+      const int64_t dd = b->d_dense;
+      HS_CHECK(dupload(*ix, &ix->wh_mean, b->wh_mean.data(), dd));
+      std::vector<double> tr((size_t)dd * dd);
+      for (int64_t r = 0; r < dd; ++r)
+        for (int64_t c = 0; c < dd; ++c) tr[(size_t)c * dd + r] = b->wh_inv_t[(size_t)r * dd + c];
+      HS_CHECK(dupload(*ix, &ix->wh_inv_t, tr.data(), (size_t)dd * dd));
+    }
+  }
+  ix->has_ds = 1;
+  ix->ds_nnz = b->nnz;
+  take(ix->ds_indptr, b->indptr, 8 * (n + 1));
+  take(ix->ds_indices, b->indices, 4 * b->nnz);
+  take(ix->ds_data, b->data, 4 * b->nnz);
+  if (b->d_dense > 0) {
+    if (b->dense_fp16) take(ix->ds_dense_h, b->dense_h, 2 * n * b->d_dense);
+    else take(ix->ds_dense, b->dense, 4 * n * b->d_dense);
+  }
+  HS_CUDA(cudaDeviceSynchronize());
+  *out = ix.release();
   return HS_OK;
 }
 

@@ -6,6 +6,8 @@
 #include <string>
 #include <vector>
 
+#include <cuda_fp16.h>
+
 #include "common.cuh"
 
 namespace hs {
@@ -56,6 +58,14 @@ struct DeviceIndex {
   // raw dataset (original order) for exact rerank / ground truth
   int has_ds = 0;
   float* ds_dense = nullptr;
+  __half* ds_dense_h = nullptr;  // fp16-stored dense part (cfg 5), instead of ds_dense
+  // GPU-built indices keep no separate residual CSR: the residual of a raw
+  // row is its entries whose data-part flag (bit e of ds_dmask) is clear and
+  // whose magnitude is >= res_eps (prune_split, sparse.py:83-103), read in
+  // the row's column order like the residual CSR (pipeline.py:137-138)
+  int res_raw = 0;
+  uint32_t* ds_dmask = nullptr;  // [ceil(ds_nnz / 32)]
+  double res_eps = 0.0;
   int64_t* ds_indptr = nullptr;
   uint32_t* ds_indices = nullptr;
   float* ds_data = nullptr;
@@ -90,6 +100,60 @@ struct DeviceIndex {
   std::vector<std::string> tnames;
   std::vector<double> tms;
 };
+
+// ---- GPU index build (devbuild.cu sparse part, build.cu dense part) ----
+// A dataset resident on one GPU (generated there or uploaded) and the index
+// products built from it; hs_builder_finish moves them into a DeviceIndex.
+struct Builder {
+  int device = 0;
+  cudaStream_t st = nullptr;
+  int64_t n = 0, d_sparse = 0, d_dense = 0, nnz = 0;
+  int dense_fp16 = 0;
+  // dataset, original row order (CSR columns ascending per row)
+  int64_t* indptr = nullptr;  // [n+1]
+  uint32_t* indices = nullptr;
+  float* data = nullptr;
+  float* dense = nullptr;     // [n][d] f32, or
+  __half* dense_h = nullptr;  // [n][d] fp16
+  // sparse products (hs_builder_sparse)
+  int sparse_done = 0;
+  uint32_t* dmask = nullptr;  // [ceil(nnz/32)] data-part flag per entry
+  double res_eps = 0.0;
+  uint32_t* order = nullptr;  // [n] layout slot -> row
+  int64_t n_active = 0, nnz_post = 0, n_head = 0;
+  uint32_t* post_dims = nullptr;  // [n_active]
+  uint32_t* post_ptr = nullptr;   // [n_active+1]
+  uint2* post = nullptr;          // [nnz_post] {slot, w bits}
+  float wmin = 0.f, wmax = 0.f;
+  uint32_t* head_dims = nullptr;  // [n_head] dims whose count exceeds top_t
+  uint32_t* head_thr = nullptr;   // [n_head] |v| bit pattern of the top_t-th largest
+  // dense products (hs_builder_dense_encode)
+  int dense_done = 0;
+  int K = 0, l = 0;
+  std::vector<int32_t> subdims;
+  std::vector<float> centers;
+  uint8_t* packed = nullptr;  // [npairs][n] pair-major (reference layout)
+  uint8_t* pcodes = nullptr;  // [n][pcodes_row] point-major
+  uint8_t* sq = nullptr;      // [n][d]
+  std::vector<float> sq_lo, sq_step;
+  int has_wh = 0;
+  std::vector<double> wh_mean, wh_inv_t;
+  // phase timings (seconds)
+  std::vector<std::string> tnames;
+  std::vector<double> tsec;
+  void* tmp = nullptr;  // cub temp storage, grown on demand
+  size_t tmp_bytes = 0;
+  int64_t bytes = 0;
+};
+int builder_tmp(Builder& b, size_t bytes);
+void builder_phase(Builder& b, const char* name, double sec);
+void builder_free(Builder* b);
+// f64 rows of the dense part (gathered by `rows`, or order[slot0 + i] when
+// rows == nullptr), optionally whitened: out[i] = (x - mean) @ fwd^T
+int launch_dense_rows(const Builder& b, const uint32_t* rows_u32, const int64_t* rows_i64,
+                      int64_t slot0, int64_t m, const double* mean, const double* fwd,
+                      double* out, cudaStream_t st);
+int build_skip_tables_dev(DeviceIndex& ix);
 
 // ---- per-batch device views of a query chunk ----
 struct QueryView {

@@ -121,9 +121,12 @@ __device__ __forceinline__ int hash_find(const uint32_t* hkey, const int* hval, 
 // bounds [b, e) are given.  Column indices and values of a 32-entry piece are
 // loaded together (one memory round trip per piece), the next piece's loads
 // issued before this one's lookups.
+// With `dmask` set (GPU-built indices: the residual is read from the raw row)
+// only entries whose data-part bit is clear and whose |value| >= eps count.
 __device__ double warp_row_dot_h(int64_t b, int64_t e, const uint32_t* __restrict__ indices,
                                  const float* __restrict__ data, const uint32_t* hkey,
-                                 const int* hval, uint32_t mask, const double* __restrict__ qval) {
+                                 const int* hval, uint32_t mask, const double* __restrict__ qval,
+                                 const uint32_t* __restrict__ dmask = nullptr, double eps = 0.0) {
   const int lane = threadIdx.x & 31;
   double sum = 0.0;
   int64_t i = b + lane;
@@ -144,7 +147,12 @@ __device__ double warp_row_dot_h(int64_t b, int64_t e, const uint32_t* __restric
     }
     double prod = 0.0;
     bool hit = false;
-    if (live) {
+    bool keep = true;
+    if (live && dmask) {
+      const int64_t ei = base + lane;
+      keep = !((__ldg(dmask + (ei >> 5)) >> (ei & 31)) & 1u) && fabs((double)val) >= eps;
+    }
+    if (live && keep) {
       const int j = hash_find(hkey, hval, mask, col);
       if (j >= 0) {
         prod = __dmul_rn((double)val, qval[j]);
@@ -245,10 +253,14 @@ struct Stage3Args {
   int64_t id_offset;
   // exact
   const float* ds_dense;
+  const __half* ds_dense_h;
   const int64_t* ds_indptr;
   const uint32_t* ds_indices;
   const float* ds_data;
-  // residual
+  // residual (res_raw: raw rows by original id, data-part bits in dmask)
+  int res_raw;
+  const uint32_t* dmask;
+  double eps;
   int64_t res_nnz;
   const int64_t* res_indptr;
   const uint32_t* res_indices;
@@ -294,9 +306,16 @@ __global__ void __launch_bounds__(kRrThreads) k_stage3(Stage3Args a) {
     if (a.exact) {
       double dense = 0.0;
       if (a.d > 0) {  // every group runs the recipe (converged shuffles); dead ones on row 0
-        const float* row = a.ds_dense + (live ? (int64_t)e.tie : 0) * a.d;
-        auto elem = [&](int i) -> double { return (double)__ldg(row + i); };
-        dense = group4_dot_recipe(elem, qd, (int)a.d, lane4, gmask);
+        const int64_t r = live ? (int64_t)e.tie : 0;
+        if (a.ds_dense_h) {
+          const __half* row = a.ds_dense_h + r * a.d;
+          auto elem = [&](int i) -> double { return (double)__half2float(row[i]); };
+          dense = group4_dot_recipe(elem, qd, (int)a.d, lane4, gmask);
+        } else {
+          const float* row = a.ds_dense + r * a.d;
+          auto elem = [&](int i) -> double { return (double)__ldg(row + i); };
+          dense = group4_dot_recipe(elem, qd, (int)a.d, lane4, gmask);
+        }
       }
       if (live) e.s = dense;
     }
@@ -305,12 +324,13 @@ __global__ void __launch_bounds__(kRrThreads) k_stage3(Stage3Args a) {
     const int nc = min(8, a.k2 - c0);
     // sparse row bounds of the 8 candidates, loaded in parallel (lanes 0-7)
     const bool use_sp = nqz > 0 && (a.exact || a.res_nnz > 0);
-    const int64_t* rp = a.exact ? a.ds_indptr : a.res_indptr;
+    const bool raw = a.exact || a.res_raw;
+    const int64_t* rp = raw ? a.ds_indptr : a.res_indptr;
     int64_t rb = 0, re = 0;
     if (use_sp && lane < nc) {
       const Cand el = buf[c0 + lane];
       if (el.slot != 0xFFFFFFFFu) {
-        const int64_t row = a.exact ? (int64_t)el.tie : (int64_t)el.slot;
+        const int64_t row = raw ? (int64_t)el.tie : (int64_t)el.slot;
         rb = __ldg(rp + row);
         re = __ldg(rp + row + 1);
       }
@@ -328,7 +348,10 @@ __global__ void __launch_bounds__(kRrThreads) k_stage3(Stage3Args a) {
         }
       } else {
         double rd = 0.0;
-        if (use_sp) rd = warp_row_dot_h(b0, e0, a.res_indices, a.res_data, hkey, hval, hmask, qval);
+        if (use_sp)
+          rd = a.res_raw ? warp_row_dot_h(b0, e0, a.ds_indices, a.ds_data, hkey, hval, hmask, qval,
+                                          a.dmask, a.eps)
+                         : warp_row_dot_h(b0, e0, a.res_indices, a.res_data, hkey, hval, hmask, qval);
         fin = __dadd_rn(ej.s, __dmul_rn(rd, a.sparse_weight));
       }
       if (lane == 0) buf[c0 + j].s = fin;
@@ -348,7 +371,8 @@ __global__ void __launch_bounds__(kRrThreads) k_stage3(Stage3Args a) {
 
 // exact hybrid score of every point (original id order) for a query chunk
 __global__ void __launch_bounds__(kRrThreads) k_exact_scores(
-    int64_t n, int64_t d, const float* __restrict__ dense, const int64_t* __restrict__ indptr,
+    int64_t n, int64_t d, const float* __restrict__ dense, const __half* __restrict__ dense_h,
+    const int64_t* __restrict__ indptr,
     const uint32_t* __restrict__ indices, const float* __restrict__ data,
     const int64_t* __restrict__ qptr, const uint32_t* __restrict__ qdims_g,
     const float* __restrict__ qvals_g, const double* __restrict__ qd_all, double sparse_weight,
@@ -368,7 +392,8 @@ __global__ void __launch_bounds__(kRrThreads) k_exact_scores(
   __syncthreads();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  double s = (d > 0) ? dot_recipe(dense + i * d, qd, (int)d) : 0.0;
+  double s = 0.0;
+  if (d > 0) s = dense_h ? dot_recipe(dense_h + i * d, qd, (int)d) : dot_recipe(dense + i * d, qd, (int)d);
   if (nqz > 0) {
     double sp = 0.0;
     for (int64_t e = indptr[i]; e < indptr[i + 1]; ++e) {
@@ -439,6 +464,10 @@ void launch_stage3(const DeviceIndex& ix, const QueryView& q, const Cand* cand2,
   a.order = ix.order;
   a.id_offset = ix.id_offset;
   a.ds_dense = ix.ds_dense;
+  a.ds_dense_h = ix.ds_dense_h;
+  a.res_raw = ix.res_raw;
+  a.dmask = ix.ds_dmask;
+  a.eps = ix.res_eps;
   a.ds_indptr = ix.ds_indptr;
   a.ds_indices = ix.ds_indices;
   a.ds_data = ix.ds_data;
@@ -471,7 +500,8 @@ void launch_exact_scores(const DeviceIndex& ix, const QueryView& q, int max_qnnz
   const size_t smem = sizeof(double) * (ix.d_dense + mq) + sizeof(uint32_t) * mq;
   cudaFuncSetAttribute(k_exact_scores, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   dim3 grid((unsigned)ceil_div(ix.n, kRrThreads), (unsigned)q.nq);
-  k_exact_scores<<<grid, kRrThreads, smem, st>>>(ix.n, ix.d_dense, ix.ds_dense, ix.ds_indptr,
+  k_exact_scores<<<grid, kRrThreads, smem, st>>>(ix.n, ix.d_dense, ix.ds_dense, ix.ds_dense_h,
+                                                 ix.ds_indptr,
                                                  ix.ds_indices, ix.ds_data, q.sp_indptr,
                                                  q.sp_dims, q.sp_vals, qd, ix.sparse_weight, mq,
                                                  out);

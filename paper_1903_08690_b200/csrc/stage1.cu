@@ -1477,6 +1477,15 @@ int build_skip_tables(DeviceIndex& ix, const int64_t* host_ptr) {
   return HS_OK;
 }
 
+// Same tables from the device-resident post_ptr (GPU-built indices).
+int build_skip_tables_dev(DeviceIndex& ix) {
+  std::vector<uint32_t> p32(ix.n_active + 1);
+  HS_CUDA(cudaMemcpy(p32.data(), ix.post_ptr, sizeof(uint32_t) * (ix.n_active + 1),
+                     cudaMemcpyDeviceToHost));
+  std::vector<int64_t> p64(p32.begin(), p32.end());
+  return build_skip_tables(ix, p64.data());
+}
+
 int64_t bucket_capacity(const DeviceIndex& ix) {
   const int64_t nchunks = ceil_div(ix.n, kChunk);
   return std::min<int64_t>(96 * nchunks, 32768);

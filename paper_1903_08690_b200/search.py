@@ -138,6 +138,18 @@ class DeviceIndex:
         self.has_dataset = ds is not None
         self.sparse_weight, self.dense_weight = float(sw), float(dw)
 
+    @classmethod
+    def from_handle(cls, h, device, n, d_sparse, d_dense, sparse_weight, dense_weight,
+                    has_dataset=True):
+        """Wrap an hs_index_t made elsewhere (hs_builder_finish)."""
+        self = cls.__new__(cls)
+        self._h = h
+        self.device = int(device)
+        self.n, self.d_sparse, self.d_dense = int(n), int(d_sparse), int(d_dense)
+        self.has_dataset = bool(has_dataset)
+        self.sparse_weight, self.dense_weight = float(sparse_weight), float(dense_weight)
+        return self
+
     @property
     def handle(self):
         return self._h
@@ -192,6 +204,8 @@ def _posting_arrays(sidx):
 
 def device_index(index, device: int = 0) -> DeviceIndex:
     """Cached device handle for a (reference-compatible) HybridIndex."""
+    if hasattr(index, "device_handle"):  # built on the GPU (devbuild.DeviceBuiltIndex)
+        return index.device_handle(device)
     cfg = index.config
     key = (int(device), float(cfg.sparse_weight), float(cfg.dense_weight),
            index.dataset is not None, id(index.dataset))
@@ -530,6 +544,22 @@ def brute_force_batch(dataset: HybridDataset, queries, h: int, sparse_weight: fl
     q = query_arrays(queries, int(dataset.d_dense))
     _validate_queries(q, int(dataset.d_sparse), int(dataset.d_dense))
     kh = min(int(h), int(dataset.n))
+    ids = np.empty((q.nq, kh), dtype=np.int64)
+    sc = np.empty((q.nq, kh), dtype=np.float64)
+    b = q.batch()
+    nat.check(nat.lib().hs_exact_topk(dev.handle, ctypes.byref(b), int(h), nat.ptr(ids),
+                                      nat.ptr(sc)))
+    return ids, sc
+
+
+def exact_topk(index, queries, h: int, device: int = 0):
+    """Exact top-h over the index's own raw dataset (brute_force_topk semantics,
+    harness.py:25-35, with the index's weights); works for GPU-built indices,
+    whose dataset lives only on the device."""
+    dev = device_index(index, device)
+    q = query_arrays(queries, int(index.d_dense))
+    _validate_queries(q, int(index.d_sparse), int(index.d_dense))
+    kh = min(int(h), int(index.n))
     ids = np.empty((q.nq, kh), dtype=np.int64)
     sc = np.empty((q.nq, kh), dtype=np.float64)
     b = q.batch()

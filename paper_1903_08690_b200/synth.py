@@ -73,7 +73,23 @@ CONFIGS = {
         index=dict(top_t=None, seed=0),
         search=dict(h=10, overfetch=1.0, retain=1.0, exact_final_rerank=False),
         note="configs[3]: sparse-only posting stream, exact top-10"),
+    # generated and built on the GPU (devbuild.py): 10^8 points do not fit the host
+    "cfg5": BaselineConfig(
+        "cfg5", HybridLaw(100_000_000, 1_000_000_000, 256, 50.0, 1.1, "absnormal",
+                          dense_fp16=True), 10_000, 50.0,
+        index=dict(pq_subspaces=128, pq_centers=16, seed=0),
+        search=dict(h=100, overfetch=10.0, retain=10.0, exact_final_rerank=True),
+        note="configs[4]: large hybrid, top-100 after exact rerank of 1000 candidates "
+             "(per shard)"),
 }
+
+
+def replica_law(law: HybridLaw, n: int) -> HybridLaw:
+    """The same law at n points with the sparse dimensionality scaled by
+    n / law.n (so postings per dim, and the pruning they see, stay alike)."""
+    d = max(1000, int(round(law.d_sparse * n / law.n))) if law.d_sparse else 0
+    return HybridLaw(n, d, law.d_dense, law.mean_nnz, law.zipf_s, law.value_law,
+                     law.dense_fp16)
 
 
 def generate(law: HybridLaw, seed: int, n: int | None = None, mean_nnz: float | None = None,
