@@ -120,9 +120,9 @@ class DeviceDataset:
 
     @classmethod
     def upload(cls, dataset: HybridDataset, device: int = 0, dense_fp16: bool = False):
-        s = sp.csr_matrix(dataset.sparse)
-        s.sort_indices()
+        s = sp.csr_matrix(dataset.sparse, copy=True)  # canonicalised here, not in place
         s.sum_duplicates()
+        s.sort_indices()
         indptr = nat.contig(s.indptr, np.int64)
         idx = nat.contig(s.indices, np.uint32)
         val = nat.contig(s.data, np.float32)
@@ -306,8 +306,9 @@ class GpuBuild:
         bits = np.unpackbits(s["dmask"].view(np.uint8), bitorder="little")[:m.nnz].astype(bool)
         eps = float(np.asarray(self.config.residual_threshold))
         keep = ~bits & (np.abs(m.data.astype(np.float64)) >= eps)
-        res = sp.csr_matrix((np.where(keep, m.data, 0).astype(np.float32), m.indices, m.indptr),
-                            shape=m.shape)
+        # (copies: eliminate_zeros compacts the index arrays in place)
+        res = sp.csr_matrix((np.where(keep, m.data, 0).astype(np.float32), m.indices.copy(),
+                             m.indptr.copy()), shape=m.shape)
         res.eliminate_zeros()
         res = res[s["order"]].tocsr()
         res.sort_indices()

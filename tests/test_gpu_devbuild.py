@@ -117,8 +117,8 @@ def test_upload_rejects_non_canonical_rows():
     from paper_1903_08690_b200 import devbuild
 
     h = ctypes.c_void_p()
-    args = [nat.ptr(np.array([0, 3], np.int64)), nat.ptr(np.array([5, 2, 7], np.uint32)),
-            nat.ptr(np.ones(3, np.float32)), None, 0, 0, ctypes.byref(h)]
+    keep = (np.array([0, 3], np.int64), np.array([5, 2, 7], np.uint32), np.ones(3, np.float32))
+    args = [nat.ptr(keep[0]), nat.ptr(keep[1]), nat.ptr(keep[2]), None, 0, 0, ctypes.byref(h)]
     with pytest.raises(ValueError, match="ascending"):
         nat.check(devbuild._lib().hs_builder_upload(1, 10, 0, *args))
     with pytest.raises(ValueError, match="out of range"):
