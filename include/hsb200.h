@@ -255,6 +255,11 @@ int hs_builder_dense_encode(hs_builder_t b, int32_t K, const int32_t* subdims,
                             const double* wh_fwd, const double* wh_inverse_t);
 int hs_builder_download_dense(hs_builder_t b, uint8_t* packed, float* sq_lo, float* sq_step,
                               uint8_t* sq_codes);
+/* Raw dataset rows of original ids (local to the index) — sampled checks of a
+ * GPU-built index whose dataset lives only on the device.  indptr [m+1]
+ * (relative); call with indices/data NULL first to size them; dense [m][d] f32. */
+int hs_index_gather_rows(hs_index_t index, const int64_t* ids, int64_t m, int64_t* indptr,
+                         uint32_t* indices, float* data, float* dense);
 /* move the products into a search index; the builder is consumed (destroyed,
  * also on failure) */
 int hs_builder_finish(hs_builder_t b, double sparse_weight, double dense_weight,

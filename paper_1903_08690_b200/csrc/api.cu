@@ -224,9 +224,12 @@ int run_search(DeviceIndex& ix, const hs_query_batch& qb, int64_t nnz, int max_q
   const char* ev_s = std::getenv("HSB200_FUSE_SAMPLE");
   const char* ev_c = std::getenv("HSB200_FUSE_CAP");
   const int64_t m_min = ev_s ? std::max<int64_t>(128, std::atoll(ev_s)) : 65536;
-  // sample ~ k1*n/6000 points (=> ~6000 expected dense candidates per query)
+  // sample ~ k1*n/E points (=> ~E expected dense candidates per query); E
+  // grows with k1 so that the sample stays a few percent of a large index
+  // (10^8 points, k1 = 1000: a 2M-point sample instead of 17M)
+  const double e_cand = std::max(6000.0, 50.0 * (double)sz.k1);
   const int64_t m_auto = std::max<int64_t>(
-      65536, (int64_t)((double)sz.k1 * (double)ix.n / 6000.0));
+      65536, (int64_t)((double)sz.k1 * (double)ix.n / e_cand));
   // (a whole number of stage-1 chunks, so the sample ends on a chunk boundary)
   const int64_t cpts = stage1_chunk_points();
   const int64_t m_s = std::min<int64_t>(
@@ -1184,6 +1187,43 @@ int hs_shard_merge_dev(const int64_t* d_ids, const double* d_scores, int64_t G, 
   launch_shard_merge(d_ids, d_scores, G, nq, kh, h, d_out_ids, d_out_scores,
                      static_cast<cudaStream_t>(stream));
   HS_CUDA(cudaGetLastError());
+  return HS_OK;
+}
+
+// Raw dataset rows of local original ids (sampled checks of indices whose
+// dataset lives only on the GPU).  indptr [m+1] relative offsets; pass
+// indices/data NULL first to size them.  dense [m][d] as f32.
+int hs_index_gather_rows(hs_index_t ix, const int64_t* ids, int64_t m, int64_t* indptr,
+                         uint32_t* indices, float* data, float* dense) {
+  if (!ix || (m > 0 && (!ids || !indptr))) HS_FAIL(HS_EINVAL, "null argument");
+  if (!ix->has_ds) HS_FAIL(HS_EINVAL, "index holds no dataset");
+  HS_CUDA(cudaSetDevice(ix->device));
+  const int64_t d = ix->d_dense;
+  indptr[0] = 0;
+  std::vector<__half> hrow(d > 0 ? d : 1);
+  for (int64_t i = 0; i < m; ++i) {
+    if (ids[i] < 0 || ids[i] >= ix->n) HS_FAIL(HS_EINVAL, "row id out of range");
+    int64_t be[2];
+    HS_CUDA(cudaMemcpy(be, ix->ds_indptr + ids[i], sizeof(int64_t) * 2, cudaMemcpyDeviceToHost));
+    const int64_t len = be[1] - be[0];
+    indptr[i + 1] = indptr[i] + len;
+    if (indices && len)
+      HS_CUDA(cudaMemcpy(indices + indptr[i], ix->ds_indices + be[0], sizeof(uint32_t) * len,
+                         cudaMemcpyDeviceToHost));
+    if (data && len)
+      HS_CUDA(cudaMemcpy(data + indptr[i], ix->ds_data + be[0], sizeof(float) * len,
+                         cudaMemcpyDeviceToHost));
+    if (dense && d > 0) {
+      if (ix->ds_dense_h) {
+        HS_CUDA(cudaMemcpy(hrow.data(), ix->ds_dense_h + ids[i] * d, sizeof(__half) * d,
+                           cudaMemcpyDeviceToHost));
+        for (int64_t j = 0; j < d; ++j) dense[i * d + j] = __half2float(hrow[j]);
+      } else {
+        HS_CUDA(cudaMemcpy(dense + i * d, ix->ds_dense + ids[i] * d, sizeof(float) * d,
+                           cudaMemcpyDeviceToHost));
+      }
+    }
+  }
   return HS_OK;
 }
 

@@ -78,6 +78,7 @@ def _lib():
         L.hs_builder_dense_encode.argtypes = [P, i32, P, P, i32, P, P, P]
         L.hs_builder_download_dense.argtypes = [P, P, P, P, P]
         L.hs_builder_finish.argtypes = [P, f64, f64, i64, ctypes.POINTER(P)]
+        L.hs_index_gather_rows.argtypes = [P, P, i64, P, P, P, P]
         L._hsb_builder_bound = True
     return L
 
@@ -385,3 +386,21 @@ class DeviceBuiltIndex:
 
     def memory_bytes(self) -> int:
         return self.handle.memory_bytes()
+
+    def gather_rows(self, ids) -> HybridDataset:
+        """Raw rows of local original ids (sampled checks; small m)."""
+        ids = nat.contig(ids, np.int64)
+        m = len(ids)
+        L = _lib()
+        indptr = np.zeros(m + 1, dtype=np.int64)
+        nat.check(L.hs_index_gather_rows(self.handle.handle, _p(ids), m, _p(indptr), None, None,
+                                         None))
+        nnz = int(indptr[-1])
+        idx = np.empty(max(nnz, 1), dtype=np.uint32)
+        val = np.empty(max(nnz, 1), dtype=np.float32)
+        dense = np.empty((m, self.d_dense), dtype=np.float32)
+        nat.check(L.hs_index_gather_rows(self.handle.handle, _p(ids), m, _p(indptr), _p(idx),
+                                         _p(val), _p(dense) if self.d_dense else None))
+        mat = sp.csr_matrix((val[:nnz], idx[:nnz].astype(np.int64), indptr),
+                            shape=(m, self.d_sparse))
+        return HybridDataset(mat, dense)
