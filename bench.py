@@ -1,26 +1,36 @@
 #!/usr/bin/env python
-"""Benchmark: hybrid search queries/sec at recall@10 on BASELINE configs[1] (cfg2).
+"""Benchmark: hybrid search queries/sec at recall@10 (BASELINE.json metric).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload cfg2] [--queries Q] [--top-t 128|none]
+                    [--workload cfg5|cfg2|cfg3|cfg4|cfg1] [--queries Q] [--n N]
 
-A step = one `search_batch` over the Q-query batch (the whole three-stage
-pipeline: LUT build, fused stage-1 scan + top-k1, SQ rerank, exact rerank).
-`value`  : Q*K / device time with queries already resident in HBM (max over
-           ranks; L2 flushed before every step, flush not timed).
-`e2e`    : same metric through the public API `search_batch(index, queries)`
-           with host buffers: H2D of the queries and D2H of the results inside
-           the timed region (wall clock around the call, which syncs).
-`roofline`: the fused stage-1 kernel (LUT16 scan + posting stream + per-tile
-           top-k): algorithmic bytes / its CUDA-event time vs MEASURED_PEAKS.
-`cpu_baseline`: the CPU oracle port (oracle/hybrid_oracle.py, a restatement of
-           the reference search path) on a bounded query sample, all host threads.
-`--impl reference`: that CPU path alone, printed as the reference arm.
+Default workload: BASELINE `configs[4]` (cfg5) — N=10^8 points, 10^9 sparse
+dims (Zipf 1.1, mean 50 nnz), 256 dense dims stored fp16, PQ 128x16, 10^4
+queries, top-100 after exact rerank of 1000 candidates per shard.  It fits one
+B200 (~150 GB resident), so N=1 runs it whole; with N ranks each GPU holds the
+id range [r*N/G, (r+1)*N/G) (scaling "strong": total work fixed).  Data are
+seeded synthetic with the BASELINE laws, generated ON THE GPU
+that searches them (rows keyed by global id) and indexed there
+(devbuild.py; the host cannot hold cfg5).  cfg1-cfg4 keep the host generator
+and host build (`--workload`).
 
-Multi-GPU (torchrun, N>1): the cfg2 dataset is split into N contiguous id-range
-shards, one per rank (each an independent index); every rank
-searches the same queries on its shard, per-shard top-h are all-gathered over
-NCCL and merged on device (K7).  Total work is fixed => scaling "strong".
+A step = one search of the whole Q-query batch through the three-stage
+pipeline (LUT build, tensor-core stage 1 + top-k1, SQ rerank, exact rerank)
+and, for N>1, the NCCL all-gather of per-shard top-h and the device merge.
+`value` : Q*K / device time (CUDA events on the search stream, max over
+          ranks), queries resident in HBM; L2 flushed (256 MiB write) before
+          every step, untimed.
+`e2e`   : same metric through the public API with host buffers: H2D of the
+          queries and D2H of the results inside the timed region.
+`roofline`: the dominant kernel (k_lut16_tc, tcgen05 kind::i8) vs the u8
+          tensor peak, plus the Qb=1 HBM view (single-query launches).
+`parity`: GPU results vs the CPU oracle (oracle/hybrid_oracle.py) on the
+          same inputs: for cfg5 a GPU-generated, GPU-built cfg5-law replica
+          searched by both (>= 200 queries) plus full-scale sampled checks of
+          the exact-rerank scores; for cfg1-4 the cpu_baseline sample.
+`cpu_baseline`: the oracle port on the box's host cores, on a bounded sample.
+`--impl reference`: the reference arm — the oracle port alone, on an index
+          built by oracle/build_oracle.py (numpy; no product library loaded).
 """
 
 from __future__ import annotations
@@ -29,6 +39,7 @@ import argparse
 import json
 import math
 import os
+import socket
 import subprocess
 import sys
 import threading
@@ -40,15 +51,17 @@ REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
 
 METRIC = "hybrid search queries/sec at recall@10 (1–8 GPU); scan HBM GB/s vs peak"
+REPLICA_N = 200_000      # cfg5-law replica for parity and the CPU baseline
+PARITY_QUERIES = 256
 
 
 def _peaks():
     try:
         with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
             p = json.load(f)
-        return float(p["hbm_gbs"]), "measured"
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     except Exception:
-        return 6650.0, "fallback"
+        return 6650.0, "fallback (B200_PROFILING.md)"
 
 
 def _tensor_peak():
@@ -77,6 +90,26 @@ def _traffic(workload):
         except Exception:
             continue
     return {}
+
+
+def _cpu_info():
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except Exception:
+        pass
+    blas = "unknown"
+    try:
+        cfg = np.show_config(mode="dicts")
+        b = cfg.get("Build Dependencies", {}).get("blas", {})
+        blas = f"{b.get('name', '?')} {b.get('version', '')}".strip()
+    except Exception:
+        pass
+    return {"cpu_model": model, "numpy": np.__version__, "blas": blas}
 
 
 class ClockSampler:
@@ -136,30 +169,110 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def build_workload(args, rank, world, device=None):
-    """Seeded cfg data (this rank's id-range shard) + queries + index."""
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _relaunch(args):
+    """`--gpus N` outside torchrun: start N ranks with torch.distributed.run."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    sys.exit(subprocess.call(cmd, env=env))
+
+
+# ---------------------------------------------------------------------------
+# workloads
+# ---------------------------------------------------------------------------
+class Work:
+    """Everything one rank needs: index, device handle, queries, settings."""
+
+
+def _gpu_query_law(cfg):
+    from paper_1903_08690_b200 import synth
+
+    L = cfg.data
+    return synth.HybridLaw(L.n, L.d_sparse, L.d_dense, cfg.query_mean_nnz, L.zipf_s, L.value_law,
+                           dense_fp16=False)
+
+
+def setup_gpu_built(args, rank, world, device):
+    """cfg5: this rank's id range generated and indexed on its GPU."""
+    import paper_1903_08690_b200 as hs
+    from paper_1903_08690_b200 import sharded, synth
+
+    cfg = synth.CONFIGS[args.workload]
+    n_total = args.n or cfg.data.n
+    law = cfg.data if n_total == cfg.data.n else synth.replica_law(cfg.data, n_total)
+    lo, hi = sharded.shard_bounds(n_total, rank, world)
+    w = Work()
+    w.cfg, w.law, w.n_total, w.lo, w.hi = cfg, law, n_total, lo, hi
+    t0 = time.time()
+    qlaw = synth.HybridLaw(law.n, law.d_sparse, law.d_dense, cfg.query_mean_nnz, law.zipf_s,
+                           law.value_law, dense_fp16=False)
+    w.qs = hs.DeviceDataset.generate(qlaw, seed=1, n=args.queries, device=device).download()
+    dd = hs.DeviceDataset.generate(law, seed=0, n=hi - lo, row0=lo, device=device)
+    w.t_gen = time.time() - t0
+    w.nnz = dd.nnz
+    t0 = time.time()
+    w.icfg = cfg.index_config()
+    b = dd.build(w.icfg)
+    w.index = b.finish(id_offset=lo)
+    w.t_build = time.time() - t0
+    w.build_timing = dict(w.index.build_timing)
+    w.dev = w.index.handle
+    w.gpu_built = True
+    w.postings = None
+    return w
+
+
+def setup_host_built(args, rank, world, device):
+    """cfg1-cfg4: host generator + host build (dense encode on the GPU)."""
+    import paper_1903_08690_b200 as hs
     from paper_1903_08690_b200 import build_index, sharded, synth
 
     cfg = synth.CONFIGS[args.workload]
     n_total = args.n or cfg.data.n
+    w = Work()
+    w.cfg, w.law, w.n_total = cfg, cfg.data, n_total
     t0 = time.time()
     ds_full = synth.generate(cfg.data, seed=0, n=n_total)
-    lo, _ = sharded.shard_bounds(n_total, rank, world)
+    w.lo, w.hi = sharded.shard_bounds(n_total, rank, world)
     ds = sharded.shard_dataset(ds_full, rank, world) if world > 1 else ds_full
-    qs = synth.generate(cfg.data, seed=1, n=args.queries, mean_nnz=cfg.query_mean_nnz)
-    t_gen = time.time() - t0
+    w.qs = synth.generate(cfg.data, seed=1, n=args.queries, mean_nnz=cfg.query_mean_nnz)
+    w.t_gen = time.time() - t0
     kw = {}
     if args.top_t is not None:
         kw["top_t"] = None if args.top_t == "none" else int(args.top_t)
-    icfg = cfg.index_config(**kw)
+    w.icfg = cfg.index_config(**kw)
     t0 = time.time()
     exact = cfg.search["exact_final_rerank"]
-    idx = build_index(ds, icfg, keep_dataset=exact, device=device)
+    idx = build_index(ds, w.icfg, keep_dataset=True, device=device)
     if cfg.search["overfetch"] == 1.0 and idx.dense_index is not None:
         # "no rerank" configs: the stage-1 composition (SURVEY §8(d), cfg 3)
         idx.dense_index.residual = None
-    t_build = time.time() - t0
-    return cfg, ds_full, ds, qs, idx, icfg, lo, t_gen, t_build
+    w.t_build = time.time() - t0
+    w.build_timing = {}
+    w.index, w.ds = idx, ds
+    w.nnz = int(ds.sparse.nnz)
+    w.dev = (hs.device_index(idx, device) if world == 1
+             else hs.DeviceIndex(idx, device=device, id_offset=w.lo))
+    del exact
+    w.gpu_built = False
+    sidx = idx.sparse_index
+    lens = np.diff(sidx.ptr)
+    if len(sidx.dims):
+        pos = np.minimum(np.searchsorted(sidx.dims, w.qs.sparse.indices), len(sidx.dims) - 1)
+        hit = sidx.dims[pos] == w.qs.sparse.indices
+        w.postings = int(lens[pos][hit].sum())
+    else:
+        w.postings = 0
+    return w
 
 
 def query_device_buffers(qs, d_dense, torch, dev):
@@ -184,95 +297,318 @@ def query_device_buffers(qs, d_dense, torch, dev):
     return b, hold, h2d
 
 
-def cpu_oracle_qps(idx, qs, sample, threads):
-    """The CPU port of the reference search path on `sample` queries."""
-    from oracle import hybrid_oracle as O
+def exact_truth(dev, qs, h):
+    """Exact top-h (GPU, f64) over this rank's shard, global ids."""
+    import ctypes
+
+    from paper_1903_08690_b200 import _native as nat
+    from paper_1903_08690_b200.search import query_arrays
+
+    q = query_arrays(qs, int(dev.d_dense))
+    kh = min(h, int(dev.n))
+    ids = np.empty((q.nq, kh), dtype=np.int64)
+    sc = np.empty((q.nq, kh), dtype=np.float64)
+    b = q.batch()
+    nat.check(nat.lib().hs_exact_topk(dev.handle, ctypes.byref(b), int(h), nat.ptr(ids),
+                                      nat.ptr(sc)))
+    return ids, sc
+
+
+def _sub(qs, a, b):
     from paper_1903_08690_b200 import HybridDataset
 
-    sub = HybridDataset(qs.sparse[:sample], qs.dense[:sample])
-    s = idx.config
-    O.search_batch(idx, HybridDataset(qs.sparse[:1], qs.dense[:1]), s.h, threads=1)  # warm
+    return HybridDataset(qs.sparse[a:b], qs.dense[a:b])
+
+
+def _time_oracle(index, qs, sample, threads, s):
+    """Oracle search over `sample` queries on `threads` host threads; also the
+    single-thread split between stage 1 (scales with N) and stages 2-3."""
+    from oracle import hybrid_oracle as O
+
+    kw = dict(overfetch=s["overfetch"], retain=s["retain"],
+              exact_final_rerank=s["exact_final_rerank"])
+    O.search_topk(index, *O.query_parts(qs, 0), s["h"], **kw)  # warm
     t0 = time.perf_counter()
-    O.search_batch(idx, sub, None, threads=threads)
+    res = O.search_batch(index, _sub(qs, 0, sample), s["h"], threads=threads, **kw)
     dt = time.perf_counter() - t0
-    return sample / dt, dt
+    # share of the per-query time that scales with N: stage-1 scoring +
+    # selection minus the query's LUT build (single thread, median of 3)
+    t1s, tall = [], []
+    for i in range(min(3, sample)):
+        parts = O.query_parts(qs, i)
+        a, b = [], []
+        for _ in range(3):
+            u0 = time.perf_counter()
+            sc = O.stage1_scores(index, *parts)
+            O.select_topk(sc, min(index.n, math.ceil(s["overfetch"] * s["h"])),
+                          tie_ids=np.asarray(index.order, dtype=np.int64))
+            u1 = time.perf_counter()
+            if index.dense_index is not None:
+                O.query_lut(index, parts[2])
+            u2 = time.perf_counter()
+            O.search_topk(index, *parts, s["h"], **kw)
+            u3 = time.perf_counter()
+            a.append((u1 - u0) - (u2 - u1))
+            b.append(u3 - u2)
+        t1s.append(float(np.median(a)))
+        tall.append(float(np.median(b)))
+    f1 = min(1.0, max(0.0, float(np.sum(t1s)) / max(float(np.sum(tall)), 1e-12)))
+    return res, dt, f1
 
 
+def replica_parity(args, device, s, want_cpu):
+    """cfg5-law replica generated and built on the GPU, searched on the GPU and
+    by the oracle on the downloaded index (same bytes, same queries)."""
+    import paper_1903_08690_b200 as hs
+    from paper_1903_08690_b200 import synth
+    from oracle import build_oracle as BO
+
+    cfg = synth.CONFIGS[args.workload]
+    law = synth.replica_law(cfg.data, args.replica_n)
+    qlaw = _gpu_query_law(cfg)
+    qlaw.d_sparse = law.d_sparse
+    t0 = time.time()
+    dd = hs.DeviceDataset.generate(law, seed=0, device=device)
+    qs = hs.DeviceDataset.generate(qlaw, seed=1, n=args.parity_queries, device=device).download()
+    icfg = cfg.index_config()
+    b = dd.build(icfg)
+    host = b.host_index()
+    # build parity: the oracle's numpy build of the downloaded dataset
+    ob = BO.build_index(host.dataset, icfg)
+    bp = {"order_equal": bool(np.array_equal(ob.order, host.order)),
+          "postings_equal": bool(np.array_equal(ob.sparse_index.ids, host.sparse_index.ids)
+                                 and np.array_equal(ob.sparse_index.w, host.sparse_index.w)
+                                 and np.array_equal(ob.sparse_index.ptr, host.sparse_index.ptr)),
+          "residual_equal": bool((ob.sparse_residual != host.sparse_residual).nnz == 0),
+          "pq_codes_agree": float(np.mean(ob.dense_index.codes.packed
+                                          == host.dense_index.codes.packed)),
+          "sq_codes_agree": float(np.mean(ob.dense_index.residual.codes
+                                          == host.dense_index.residual.codes))}
+    del ob
+    gidx = b.finish()
+    res = hs.search_batch(gidx, qs, s["h"], overfetch=s["overfetch"], retain=s["retain"],
+                          exact_final_rerank=s["exact_final_rerank"])
+    host.config.h = s["h"]
+    threads = os.cpu_count() or 1
+    ores, dt, f1 = _time_oracle(host, qs, qs.n, threads, s)
+    mism, worst = 0, 0.0
+    for r, (oi, osc, _) in zip(res, ores):
+        if r.ids.tolist() != oi.tolist():
+            mism += 1
+        if len(osc):
+            worst = max(worst, float(np.max(np.abs(r.scores - osc) / np.maximum(np.abs(osc),
+                                                                               1e-300))))
+    out = {"replica": f"cfg5 law at N={law.n}, d_sparse={law.d_sparse} (GPU-generated, "
+                      f"GPU-built, downloaded for the oracle)",
+           "queries": int(qs.n), "id_mismatch": int(mism), "max_rel_err": worst,
+           "build": bp, "seconds": round(time.time() - t0, 1)}
+    cpu = None
+    if want_cpu:
+        per_q = dt / qs.n
+        scale = cfg.data.n / law.n
+        est = per_q * (f1 * scale + (1.0 - f1))
+        cpu = {"value": 1.0 / est, "unit": "queries/s", "cores": threads, "kind": "port",
+               "sample": f"{qs.n} queries of the cfg5-law replica (N={law.n}), oracle "
+                         f"search_batch(threads={threads}) {dt:.1f} s; per-query time "
+                         f"extrapolated to N={cfg.data.n}: the share that scales with N "
+                         f"(stage-1 scan + select, {f1:.3f}, measured single-thread) x"
+                         f"{scale:.0f}, the rest (LUT build, stages 2-3) constant",
+               "replica_qps_measured": qs.n / dt}
+        cpu.update(_cpu_info())
+    gidx.handle.close()
+    return out, cpu
+
+
+def fullscale_checks(w, res_ids, res_sc, nq_check, s):
+    """Exact-rerank scores of the returned ids recomputed on the host from the
+    rows gathered out of the device index (rank-local ids)."""
+    from oracle import hybrid_oracle as O
+
+    worst, checked = 0.0, 0
+    for i in range(min(nq_check, res_ids.shape[0])):
+        ids = res_ids[i]
+        ids = ids[ids >= 0]
+        loc = ids - w.lo
+        mine = (loc >= 0) & (loc < w.hi - w.lo)
+        if not mine.any():
+            continue
+        rows = w.index.gather_rows(loc[mine])
+        qd, qv, qdense = O.query_parts(w.qs, i)
+        ex = O.exact_scores(rows, qd, qv, qdense, np.arange(rows.n),
+                            w.icfg.sparse_weight, w.icfg.dense_weight)
+        got = res_sc[i][: len(ids)][mine]
+        worst = max(worst, float(np.max(np.abs(got - ex) / np.maximum(np.abs(ex), 1e-300))))
+        checked += int(mine.sum())
+    return {"queries": int(min(nq_check, res_ids.shape[0])), "rows_checked": checked,
+            "max_rel_err_exact_scores": worst}
+
+
+# ---------------------------------------------------------------------------
+# reference arm
+# ---------------------------------------------------------------------------
 def run_reference_arm(args, rank, world):
-    """--impl reference: the CPU port of the reference path, rank 0 only."""
+    """--impl reference: the oracle port on the host cores (rank 0 only), on an
+    index built by oracle/build_oracle.py (no product library loaded)."""
     if rank != 0:
         return
-    cfg, ds_full, ds, qs, idx, icfg, lo, t_gen, t_build = build_workload(args, 0, 1)
-    s = cfg.search
-    idx.config.h = s["h"]
-    idx.config.overfetch = s["overfetch"]
-    idx.config.retain = s["retain"]
-    idx.config.exact_final_rerank = s["exact_final_rerank"]
-    threads = os.cpu_count() or 1
-    sample = min(args.cpu_sample, qs.n)
+    from oracle import build_oracle as BO
     from oracle import hybrid_oracle as O
-    from paper_1903_08690_b200 import HybridDataset
+    from types import SimpleNamespace
 
-    sub = HybridDataset(qs.sparse[:sample], qs.dense[:sample])
+    spec = _workload_spec(args.workload)
+    s = spec["search"]
+    gpu_built = args.workload == "cfg5"
+    n_full = args.n or spec["n"]
+    n_rep = min(n_full, args.replica_n) if gpu_built else n_full
+    scale_d = n_rep / spec["n"]
+    d_sparse = max(1000, int(round(spec["d_sparse"] * scale_d))) if spec["d_sparse"] else 0
+    t0 = time.time()
+    ds = BO.generate(n_rep, d_sparse, spec["d_dense"], spec["mean_nnz"], spec["zipf_s"],
+                     spec["value_law"], spec["dense_fp16"], seed=0)
+    qs = BO.generate(max(64, args.ref_queries), d_sparse, spec["d_dense"], spec["q_mean_nnz"],
+                     spec["zipf_s"], spec["value_law"], False, seed=1)
+    icfg = SimpleNamespace(**spec["index"])
+    index = BO.build_index(ds, icfg)
+    index.config.h = s["h"]
+    t_setup = time.time() - t0
+    threads = os.cpu_count() or 1
+    kw = dict(overfetch=s["overfetch"], retain=s["retain"],
+              exact_final_rerank=s["exact_final_rerank"])
+    # per-step sample: ~args.ref_step_seconds of work
+    u0 = time.perf_counter()
+    O.search_batch(index, _sub(qs, 0, 4), s["h"], threads=threads, **kw)
+    per = (time.perf_counter() - u0) / 4
+    sample = int(min(qs.n, max(8, args.ref_step_seconds / max(per, 1e-4) * min(threads, 8))))
     for _ in range(args.warmup):
-        O.search_batch(idx, HybridDataset(qs.sparse[:1], qs.dense[:1]), None, threads=1)
+        O.search_batch(index, _sub(qs, 0, min(4, sample)), s["h"], threads=threads, **kw)
     times = []
-    for _ in range(args.steps):
-        t0 = time.perf_counter()
-        O.search_batch(idx, sub, None, threads=threads)
-        times.append(time.perf_counter() - t0)
-    qps = sample * len(times) / sum(times)
+    for k in range(args.steps):
+        a = (k * sample) % max(1, qs.n - sample + 1)
+        t1 = time.perf_counter()
+        O.search_batch(index, _sub(qs, a, a + sample), s["h"], threads=threads, **kw)
+        times.append(time.perf_counter() - t1)
+    qps_rep = sample * len(times) / sum(times)
+    f1 = 1.0
+    note = ""
+    qps = qps_rep
+    if gpu_built and n_rep < n_full:
+        _, _, f1 = _time_oracle(index, qs, 4, 1, s)
+        scale = n_full / n_rep
+        qps = 1.0 / ((1.0 / qps_rep) * (f1 * scale + 1.0 - f1))
+        note = (f"; QPS extrapolated to N={n_full} from the N={n_rep} replica: the share "
+                f"that scales with N (stage-1 scan + select, {f1:.3f}) x{scale:.0f}, the rest "
+                f"(LUT build, stages 2-3) constant")
+    Q = args.queries or spec["queries"]
     line = {
         "impl": "reference", "metric": METRIC, "value": qps, "unit": "queries/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "u8+f64", "data": "synthetic",
-        "config": {"workload": f"{args.workload} ({cfg.note}), sample of {sample} queries/step",
-                   "n": int(ds.n), "queries_per_step": sample},
+        "ms_per_step": 1e3 * Q / qps, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "u8+f64", "data": "synthetic (seeded BASELINE-law "
+        "generator, numpy: oracle/build_oracle.py)",
+        "config": _config_dict(args.workload, spec, n_full, Q),
         "cpu_baseline": {"value": qps, "unit": "queries/s", "cores": threads, "kind": "port",
-                         "sample": f"{sample} queries of {args.workload} per step, "
-                                   f"oracle search_batch(threads={threads})"},
+                         "sample": f"{sample} queries per step of the {args.workload} law at "
+                                   f"N={n_rep}, oracle search_batch(threads={threads}), index "
+                                   f"from oracle/build_oracle.py{note}",
+                         "measured_qps_at_sample_n": qps_rep, "setup_s": round(t_setup, 1),
+                         **_cpu_info()},
         "e2e": {"value": qps, "unit": "queries/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
+def _workload_spec(name):
+    """Plain-data description of a BASELINE workload (no product import)."""
+    specs = {
+        "cfg1": dict(n=100_000, d_sparse=1_000_000, d_dense=128, mean_nnz=50.0, zipf_s=1.1,
+                     value_law="absnormal", dense_fp16=False, q_mean_nnz=50.0, queries=1000,
+                     index=dict(pq_subspaces=64, kmeans_iters=10),
+                     search=dict(h=10, overfetch=20.0, retain=20.0, exact_final_rerank=True)),
+        "cfg2": dict(n=1_000_000, d_sparse=10_000_000, d_dense=256, mean_nnz=100.0, zipf_s=1.1,
+                     value_law="lognormal", dense_fp16=False, q_mean_nnz=100.0, queries=1000,
+                     index=dict(pq_subspaces=128),
+                     search=dict(h=10, overfetch=50.0, retain=50.0, exact_final_rerank=True)),
+        "cfg3": dict(n=10_000_000, d_sparse=0, d_dense=128, mean_nnz=0.0, zipf_s=1.1,
+                     value_law="absnormal", dense_fp16=False, q_mean_nnz=0.0, queries=10_000,
+                     index=dict(pq_subspaces=64),
+                     search=dict(h=100, overfetch=1.0, retain=1.0, exact_final_rerank=False)),
+        "cfg4": dict(n=10_000_000, d_sparse=100_000_000, d_dense=0, mean_nnz=80.0, zipf_s=1.05,
+                     value_law="absnormal", dense_fp16=False, q_mean_nnz=30.0, queries=10_000,
+                     index=dict(top_t=None),
+                     search=dict(h=10, overfetch=1.0, retain=1.0, exact_final_rerank=False)),
+        "cfg5": dict(n=100_000_000, d_sparse=1_000_000_000, d_dense=256, mean_nnz=50.0,
+                     zipf_s=1.1, value_law="absnormal", dense_fp16=True, q_mean_nnz=50.0,
+                     queries=10_000, index=dict(pq_subspaces=128),
+                     search=dict(h=100, overfetch=10.0, retain=10.0, exact_final_rerank=True)),
+    }
+    sp_ = dict(specs[name])
+    base = dict(overfetch=10.0, retain=3.0, h=20, top_t=128, data_threshold=None,
+                residual_threshold=0.0, pq_subspaces=None, pq_centers=16, use_whitening=True,
+                exact_final_rerank=False, sparse_weight=1.0, dense_weight=1.0, kmeans_iters=25,
+                train_sample=50_000, line_capacity=16, seed=0)
+    base.update(sp_["index"])
+    sp_["index"] = base
+    return sp_
+
+
+def _config_dict(name, spec, n, Q):
+    s = spec["search"]
+    k1 = min(n, math.ceil(s["overfetch"] * s["h"]))
+    return {"workload": name, "n": int(n), "d_sparse": int(spec["d_sparse"]),
+            "d_dense": int(spec["d_dense"]), "pq_subspaces": spec["index"]["pq_subspaces"],
+            "queries_per_step": int(Q), "h": s["h"], "k1": int(k1),
+            "k2": int(min(k1, math.ceil(s["retain"] * s["h"]))),
+            "top_t": spec["index"]["top_t"], "exact_final_rerank": s["exact_final_rerank"]}
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="cfg2")
+    ap.add_argument("--workload", default="cfg5")
     ap.add_argument("--queries", type=int, default=None)
     ap.add_argument("--n", type=int, default=None)
     ap.add_argument("--top-t", default=None)
     ap.add_argument("--cpu-sample", type=int, default=None)
     ap.add_argument("--cpu-seconds", type=float, default=10.0,
-                    help="target CPU work of the cpu_baseline sample")
+                    help="target CPU work of the cpu_baseline sample (cfg1-4)")
     ap.add_argument("--truth-queries", type=int, default=None)
     ap.add_argument("--qb1", type=int, default=16,
                     help="single-query launches timed for the Qb=1 scan roofline")
+    ap.add_argument("--replica-n", type=int, default=REPLICA_N)
+    ap.add_argument("--parity-queries", type=int, default=PARITY_QUERIES)
+    ap.add_argument("--ref-queries", type=int, default=512)
+    ap.add_argument("--ref-step-seconds", type=float, default=3.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-parity", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        _relaunch(args)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference_arm(args, rank, world)
+        return
+
     from paper_1903_08690_b200 import synth
 
     if args.queries is None:
         args.queries = synth.CONFIGS[args.workload].n_queries
-    big = args.workload in ("cfg3", "cfg4")
+    gpu_built = args.workload == "cfg5"
+    big = args.workload in ("cfg3", "cfg4", "cfg5")
     if args.cpu_sample is None:
         args.cpu_sample = 8 if big else 24
     if args.truth_queries is None:
-        args.truth_queries = 200 if big else args.queries
-    if args.impl == "reference":
-        run_reference_arm(args, rank, world)
-        return
+        args.truth_queries = 100 if big else args.queries
 
     import torch
 
@@ -286,40 +622,58 @@ def main():
 
     import paper_1903_08690_b200 as hs
     from paper_1903_08690_b200 import _native as nat
+    from paper_1903_08690_b200 import sharded
 
-    cfg, ds_full, ds, qs, idx, icfg, id_lo, t_gen, t_build = build_workload(args, rank, world,
-                                                                            device=local)
+    cfg = synth.CONFIGS[args.workload]
     s = cfg.search
     h = s["h"]
-    dev_index = (hs.device_index(idx, local) if world == 1
-                 else hs.DeviceIndex(idx, device=local, id_offset=id_lo))
+
+    # parity replica first (small; freed before the full-size index is built)
+    parity, cpu = None, None
+    if gpu_built and rank == 0 and not args.no_parity:
+        parity, cpu = replica_parity(args, local, s, want_cpu=(world == 1 and not args.no_cpu))
+        torch.cuda.synchronize()
+
+    w = (setup_gpu_built if gpu_built else setup_host_built)(args, rank, world, local)
+    idx, dev_index, qs = w.index, w.dev, w.qs
     params = hs.search.resolve_params(idx, h, s["overfetch"], s["retain"], s["exact_final_rerank"])
     counts = np.zeros(3, dtype=np.int64)
     nat.check(nat.lib().hs_result_sizes(dev_index.handle, params, nat.ptr(counts)))
     k1, k2, kh = (int(x) for x in counts)
     nq = qs.n
+    if world > 1:  # ranks agree on the per-shard result width (pad to h)
+        t = torch.tensor([kh], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        kh_all = int(t.item())
+    else:
+        kh_all = kh
 
     qb, hold, h2d_bytes = query_device_buffers(qs, idx.d_dense, torch, dev)
-    out_ids = torch.empty((nq, kh), dtype=torch.int64, device=dev)
-    out_sc = torch.empty((nq, kh), dtype=torch.float64, device=dev)
+    out_ids = torch.full((nq, kh_all), -1, dtype=torch.int64, device=dev)
+    out_sc = torch.full((nq, kh_all), -math.inf, dtype=torch.float64, device=dev)
     if world > 1:
-        g_ids = torch.empty((world, nq, kh), dtype=torch.int64, device=dev)
-        g_sc = torch.empty((world, nq, kh), dtype=torch.float64, device=dev)
+        g_ids = torch.empty((world, nq, kh_all), dtype=torch.int64, device=dev)
+        g_sc = torch.empty((world, nq, kh_all), dtype=torch.float64, device=dev)
         m_ids = torch.empty((nq, h), dtype=torch.int64, device=dev)
         m_sc = torch.empty((nq, h), dtype=torch.float64, device=dev)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
     torch.cuda.synchronize()
     stream = torch.cuda.Stream(dev)
     torch.cuda.set_stream(stream)
+    # per-shard outputs are written into the first kh columns (row stride kh)
+    o_ids = out_ids if kh == kh_all else torch.empty((nq, kh), dtype=torch.int64, device=dev)
+    o_sc = out_sc if kh == kh_all else torch.empty((nq, kh), dtype=torch.float64, device=dev)
 
-    def step():
-        dev_index.search_dev(qb, params, out_ids.data_ptr(), out_sc.data_ptr(),
-                             stream.cuda_stream)
+    def step(qbuf=qb):
+        dev_index.search_dev(qbuf, params, o_ids.data_ptr(), o_sc.data_ptr(), stream.cuda_stream)
+        if kh != kh_all:
+            out_ids[:, :kh].copy_(o_ids)
+            out_sc[:, :kh].copy_(o_sc)
         if world > 1:
             dist.all_gather_into_tensor(g_ids.view(-1), out_ids.view(-1))
             dist.all_gather_into_tensor(g_sc.view(-1), out_sc.view(-1))
             nat.check(nat.lib().hs_shard_merge_dev(
-                g_ids.data_ptr(), g_sc.data_ptr(), world, nq, kh, h, m_ids.data_ptr(),
+                g_ids.data_ptr(), g_sc.data_ptr(), world, nq, kh_all, h, m_ids.data_ptr(),
                 m_sc.data_ptr(), stream.cuda_stream))
 
     for _ in range(args.warmup):
@@ -355,24 +709,54 @@ def main():
         t_total = float(tt.item())
     value = nq * args.steps / (t_total / 1e3)
 
-    # ---- e2e through the public API with host buffers (N=1) ----
-    e2e = None
+    # results of the last timed step (merged for N > 1)
+    torch.cuda.synchronize()
+    res_ids = (m_ids if world > 1 else out_ids).cpu().numpy()
+    res_sc = (m_sc if world > 1 else out_sc).cpu().numpy()
+    loc_ids, loc_sc = out_ids.cpu().numpy(), out_sc.cpu().numpy()
+
+    # ---- e2e through the public API with host buffers ----
+    e2e_steps = max(1, min(args.steps, 10))
     if world == 1:
+        kw = dict(overfetch=s["overfetch"], retain=s["retain"],
+                  exact_final_rerank=s["exact_final_rerank"])
         for _ in range(2):
-            hs.search_batch(idx, qs, h, overfetch=s["overfetch"], retain=s["retain"],
-                            exact_final_rerank=s["exact_final_rerank"])
+            hs.search_batch(idx, qs, h, **kw)
         et = []
-        for _ in range(args.steps):
+        for _ in range(e2e_steps):
             flush.zero_()
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            hs.search_batch(idx, qs, h, overfetch=s["overfetch"], retain=s["retain"],
-                            exact_final_rerank=s["exact_final_rerank"])
+            hs.search_batch(idx, qs, h, **kw)
             et.append(time.perf_counter() - t0)
         d2h = nq * kh * (8 + 8)
-        e2e = {"value": nq * len(et) / sum(et), "unit": "queries/s",
-               "h2d_bytes_per_step": int(h2d_bytes), "d2h_bytes_per_step": int(d2h),
-               "ms_per_step": 1e3 * sum(et) / len(et)}
+    else:
+        # host queries -> each GPU, shard search, all-gather, merge, merged
+        # result back to the host (every step, inside the timed region)
+        pin = [t.cpu().pin_memory() for t in hold]
+        et = []
+        for it in range(e2e_steps + 2):
+            flush.zero_()
+            torch.cuda.synchronize()
+            dist.barrier()
+            t0 = time.perf_counter()
+            with torch.cuda.stream(stream):
+                for dst, src in zip(hold, pin):
+                    dst.copy_(src, non_blocking=True)
+                step()
+                mi, ms = m_ids.to("cpu", non_blocking=False), m_sc.to("cpu", non_blocking=False)
+            stream.synchronize()
+            tt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            if it >= 2:
+                et.append(float(tt.item()))
+        d2h = nq * h * (8 + 8)
+        del mi, ms
+    e2e = {"value": nq * len(et) / sum(et), "unit": "queries/s",
+           "h2d_bytes_per_step": int(h2d_bytes), "d2h_bytes_per_step": int(d2h),
+           "ms_per_step": 1e3 * sum(et) / len(et),
+           "path": ("search_batch(index, queries) host buffers" if world == 1 else
+                    "host queries -> GPUs, shard search, NCCL all-gather, merge, D2H")}
 
     # ---- per-kernel breakdown (separate profiled steps; timing adds syncs) ----
     dev_index.set_timing(True)
@@ -380,24 +764,20 @@ def main():
     for _ in range(2):
         flush.zero_()
         torch.cuda.synchronize()
-        step()
+        dev_index.search_dev(qb, params, o_ids.data_ptr(), o_sc.data_ptr(), stream.cuda_stream)
         torch.cuda.synchronize()
         for k, v in dev_index.kernel_times().items():
             ktimes[k] = ktimes.get(k, 0.0) + v / 2
     qb1 = None
     if world == 1 and args.qb1 > 0:
-        # Qb=1: one query per launch, stage-1 kernel time per pass over the codes
-        from paper_1903_08690_b200 import HybridDataset
-
         t1 = []
         for i in range(min(args.qb1, nq)):
-            one = HybridDataset(qs.sparse[i:i + 1], qs.dense[i:i + 1])
-            b1, hold1, _ = query_device_buffers(one, idx.d_dense, torch, dev)
-            o_i = torch.empty((1, kh), dtype=torch.int64, device=dev)
-            o_s = torch.empty((1, kh), dtype=torch.float64, device=dev)
+            b1, hold1, _ = query_device_buffers(_sub(qs, i, i + 1), idx.d_dense, torch, dev)
+            oi = torch.empty((1, kh), dtype=torch.int64, device=dev)
+            os_ = torch.empty((1, kh), dtype=torch.float64, device=dev)
             flush.zero_()
             torch.cuda.synchronize()
-            dev_index.search_dev(b1, params, o_i.data_ptr(), o_s.data_ptr(), stream.cuda_stream)
+            dev_index.search_dev(b1, params, oi.data_ptr(), os_.data_ptr(), stream.cuda_stream)
             torch.cuda.synchronize()
             kt = dev_index.kernel_times()
             if i > 0:  # first launch warms the per-launch path
@@ -405,46 +785,64 @@ def main():
         qb1 = float(np.mean(t1)) if t1 else None
     dev_index.set_timing(False)
 
-    # ---- results (rank-local then merged) and recall@10 vs exact brute force ----
-    torch.cuda.synchronize()
+    # ---- recall@10 vs exact brute force (GPU f64 truth, merged over shards) ----
+    truth_q = min(nq, args.truth_queries)
+    qsub = _sub(qs, 0, truth_q)
+    t_ids, t_sc = exact_truth(dev_index, qsub, 10)
     if world > 1:
-        res_ids = m_ids.cpu().numpy()
-    else:
-        res_ids = out_ids.cpu().numpy()
-    recall = None
-    if rank == 0:
-        truth_q = min(nq, args.truth_queries)
-        from paper_1903_08690_b200 import HybridDataset
+        ti = torch.as_tensor(t_ids).to(dev)
+        ts = torch.as_tensor(t_sc).to(dev)
+        gi = [torch.empty_like(ti) for _ in range(world)]
+        gs = [torch.empty_like(ts) for _ in range(world)]
+        dist.all_gather(gi, ti)
+        dist.all_gather(gs, ts)
+        t_ids, _ = sharded.merge_host(torch.stack(gi).cpu().numpy(),
+                                      torch.stack(gs).cpu().numpy(), 10)
+    rec = [len(np.intersect1d(res_ids[i, :10], t_ids[i])) / 10 for i in range(truth_q)]
+    recall = float(np.mean(rec))
 
-        qsub = HybridDataset(qs.sparse[:truth_q], qs.dense[:truth_q])
-        t_ids, _ = hs.brute_force_batch(ds_full, qsub, 10, icfg.sparse_weight, icfg.dense_weight,
-                                        device=local)
-        rec = [len(np.intersect1d(res_ids[i, :10], t_ids[i])) / 10 for i in range(truth_q)]
-        recall = float(np.mean(rec))
+    # ---- full-scale sampled checks (exact scores of the returned rows) ----
+    full_check = None
+    if w.gpu_built and not args.no_parity:
+        full_check = fullscale_checks(w, loc_ids, loc_sc, 16, s)
+
+    # ---- parity (host-built workloads): the cpu_baseline sample vs the oracle ----
+    if not w.gpu_built and rank == 0 and world == 1 and not args.no_cpu:
+        threads = os.cpu_count() or 1
+        sample = min(args.cpu_sample, nq)
+        idx.config.h = h
+        ores, dt, _ = _time_oracle(idx, qs, sample, threads, s)
+        if dt < 0.5 * args.cpu_seconds and sample < nq:
+            sample = min(nq, max(sample + 1, int(sample * args.cpu_seconds / max(dt, 1e-3))))
+            ores, dt, _ = _time_oracle(idx, qs, sample, threads, s)
+        mism, worst = 0, 0.0
+        for i, (oi, osc, _) in enumerate(ores):
+            got = res_ids[i][res_ids[i] >= 0]
+            if got.tolist() != oi.tolist():
+                mism += 1
+            if len(osc):
+                worst = max(worst, float(np.max(np.abs(res_sc[i][:len(osc)] - osc)
+                                                / np.maximum(np.abs(osc), 1e-300))))
+        parity = {"queries": int(sample), "id_mismatch": int(mism), "max_rel_err": worst,
+                  "against": "oracle/hybrid_oracle.py on the same index and queries"}
+        cpu = {"value": sample / dt, "unit": "queries/s", "cores": threads, "kind": "port",
+               "sample": f"first {sample} of {nq} {args.workload} queries, oracle "
+                         f"search_batch(threads={threads}), {dt:.1f} s", **_cpu_info()}
+    if parity is not None and full_check is not None:
+        parity["full_scale"] = full_check
 
     # ---- roofline of the dominant kernel ----
-    # tensor-core path (cfg2/cfg3): k_lut16_tc, bound by the tensor cores:
-    #   algorithmic work = the one-hot LUT16 product, 2*N*Q*16K u8 ops per step
-    # posting-stream path (cfg4 / small batches): k_stage1, bound by HBM:
-    #   algorithmic bytes = 8 B per streamed posting (+ N*ceil(K/2) code bytes
-    #   per query when the CUDA-core LUT16 scan runs), SURVEY 8(d)
     di = idx.dense_index
-    npairs = (di.codes.n_subspaces + 1) // 2 if di is not None else 0
-    K = di.codes.n_subspaces if di is not None else 0
-    sidx = idx.sparse_index
-    # postings streamed per query: sum of list lengths over the query dims
-    lens = np.diff(sidx.ptr)
-    pos = np.searchsorted(sidx.dims, qs.sparse.indices)
-    pos = np.minimum(pos, max(len(sidx.dims) - 1, 0))
-    hit = (len(sidx.dims) > 0) & (sidx.dims[pos] == qs.sparse.indices) if len(sidx.dims) else \
-        np.zeros(qs.sparse.nnz, bool)
-    postings = int(lens[pos][hit].sum()) if len(sidx.dims) else 0
+    K = di.codebooks.n_subspaces if di is not None else 0
+    npairs = (K + 1) // 2
+    n_local = int(w.hi - w.lo)
     tc_ms = ktimes.get("lut16_tc")
     s1_ms = ktimes.get("stage1")
     roof = None
     traffic = _traffic(args.workload)
+    postings = w.postings
     if tc_ms and K:
-        ops = 2.0 * idx.n * nq * 16 * K
+        ops = 2.0 * n_local * nq * 16 * K
         tpeak, tkind = _tensor_peak()
         achieved = ops / (tc_ms / 1e3) / 1e12
         roof = {"bound": "tensor", "achieved": achieved, "peak": tpeak, "unit": "TFLOP/s",
@@ -456,7 +854,7 @@ def main():
                         "kernel writes only threshold-passing candidates, so its HBM "
                         "traffic is the code stream, not the N*Q score matrix"}
     elif s1_ms:
-        alg_bytes = 8 * postings + (nq * idx.n * npairs if K else 0)
+        alg_bytes = 8 * (postings or 0) + (nq * n_local * npairs if K else 0)
         peak, peak_kind = _peaks()
         achieved = alg_bytes / (s1_ms / 1e3) / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -468,50 +866,38 @@ def main():
                         + (" + N*ceil(K/2) code bytes per query" if K else "")}
     if roof is not None and qb1:
         peak, peak_kind = _peaks()
-        per_query_bytes = (idx.n * npairs + K * 16) + 8 * postings / max(nq, 1)
+        per_query_bytes = (n_local * npairs + K * 16) + 8 * (postings or 0) / max(nq, 1)
         a1 = per_query_bytes / (qb1 / 1e3) / 1e9
         roof["qb1"] = {"stage1_ms": qb1, "alg_bytes": per_query_bytes, "achieved_gbs": a1,
                        "peak_gbs": peak, "frac": a1 / peak,
                        "note": "latency path: one query per launch (CUDA-core LUT16 + "
-                               "posting stream, HBM-bound), L2 flushed before each launch"}
-
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
-        threads = os.cpu_count() or 1
-        sample = min(args.cpu_sample, nq)
-        idx.config.h = h
-        idx.config.overfetch = s["overfetch"]
-        idx.config.retain = s["retain"]
-        idx.config.exact_final_rerank = s["exact_final_rerank"]
-        qps_cpu, dt = cpu_oracle_qps(idx, qs, sample, threads)
-        if dt < 0.5 * args.cpu_seconds and sample < nq:
-            # the first sample sizes the real one: ~--cpu-seconds of CPU work
-            sample = min(nq, max(sample + 1, int(sample * args.cpu_seconds / max(dt, 1e-3))))
-            qps_cpu, dt = cpu_oracle_qps(idx, qs, sample, threads)
-        cpu = {"value": qps_cpu, "unit": "queries/s", "cores": threads, "kind": "port",
-               "sample": f"first {sample} of {nq} {args.workload} queries, oracle "
-                         f"search_batch(threads={threads}), {dt:.1f} s"}
+                               "posting stream, HBM-bound), L2 flushed before each launch"
+                               + ("" if postings is not None else "; code bytes only")}
 
     if rank == 0:
+        spec = _workload_spec(args.workload)
+        conf = _config_dict(args.workload, spec, w.n_total, nq)
+        conf.update({
+            "note": cfg.note, "recall_at_10": recall, "truth_queries": truth_q,
+            "l2": "flushed (256 MiB write) before every step, untimed",
+            "parallelism": f"id-range shards x{world}" if world > 1 else "single GPU",
+            "data_gen": "on-GPU generator (devbuild.cu)" if w.gpu_built else "host generator",
+            "index_build": "GPU (hs_builder_*)" if w.gpu_built else "host (+GPU dense encode)",
+            "nnz": int(w.nnz), "postings_per_query": (postings / max(nq, 1)
+                                                      if postings is not None else None),
+            "gen_s": round(w.t_gen, 1), "build_s": round(w.t_build, 1),
+            "build_phases_s": {k: round(v, 2) for k, v in w.build_timing.items()},
+            "index_bytes_rank0": int(dev_index.memory_bytes()),
+        })
         line = {
             "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_total / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "u8+f64",
             "data": "synthetic (seeded BASELINE-law generator, SURVEY App. B)",
-            "config": {
-                "workload": f"{args.workload}: {cfg.note}",
-                "n": int(idx.n * world if world > 1 else idx.n), "d_sparse": int(idx.d_sparse),
-                "d_dense": int(idx.d_dense), "pq_subspaces": K, "queries_per_step": nq,
-                "h": h, "k1": k1, "k2": k2, "top_t": icfg.top_t,
-                "exact_final_rerank": s["exact_final_rerank"],
-                "recall_at_10": recall, "l2": "flushed (256 MiB write) before every step, untimed",
-                "parallelism": f"id-range shards x{world}" if world > 1 else "single GPU",
-                "postings_per_query": postings / max(nq, 1),
-                "gen_s": round(t_gen, 1), "build_s": round(t_build, 1),
-            },
-            "e2e": e2e, "roofline": roof, "cpu_baseline": cpu, "clocks": clk.summary(),
-            "gpu_launches": int(launches),
+            "config": conf,
+            "e2e": e2e, "roofline": roof, "cpu_baseline": cpu, "parity": parity,
+            "clocks": clk.summary(), "gpu_launches": int(launches),
             "kernel_ms_per_step": {k: round(v, 4) for k, v in ktimes.items()},
         }
         print(json.dumps(line), flush=True)

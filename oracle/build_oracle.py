@@ -203,8 +203,16 @@ def train_codebooks(X, K, n_centers=16, n_iters=25, seed=0, sample=None):
     if sample is not None and n_centers <= sample < n:
         X = X[np.sort(np.random.default_rng(seqs[0]).choice(n, size=sample, replace=False))]
     edges = np.concatenate(([0], np.cumsum(widths)))
-    centers = [_lloyd(X[:, edges[k]:edges[k + 1]], n_centers, n_iters,
-                      np.random.default_rng(seqs[1 + k])).astype(np.float32) for k in range(K)]
+
+    def one(k):  # each subspace owns its RNG stream: thread order cannot matter
+        return _lloyd(np.ascontiguousarray(X[:, edges[k]:edges[k + 1]]), n_centers, n_iters,
+                      np.random.default_rng(seqs[1 + k])).astype(np.float32)
+
+    import os
+    from concurrent.futures import ThreadPoolExecutor
+
+    with ThreadPoolExecutor(max_workers=max(1, min(K, os.cpu_count() or 1))) as ex:
+        centers = list(ex.map(one, range(K)))
     return SimpleNamespace(subdims=widths, centers=centers, n_subspaces=K, n_centers=n_centers,
                            d_dense=d)
 
