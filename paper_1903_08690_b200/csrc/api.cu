@@ -442,7 +442,9 @@ int run_search(DeviceIndex& ix, const hs_query_batch& qb, int64_t nnz, int max_q
       }
       return HS_OK;
     };
-    const bool tc_chunk = use_tc && nqc >= kTcMinQueries;
+    // every chunk of a tensor-core batch stays on the tensor cores: a short
+    // last chunk gets a narrower query group (the MMA N shrinks with it)
+    const bool tc_chunk = use_tc;
     if (tc_chunk && use_fuse) {
       // 1. u16 totals of the first m_s points -> threshold
       HS_CHECK(launch_lut16_tc(ix, luts, nqc, P.tot_s, ld_s, st, m_s));
@@ -784,7 +786,7 @@ int hs_index_create(const hs_index_desc* ds, int device, hs_index_t* out) {
       HS_CUDA(cudaMalloc(&tmp, std::max<size_t>((size_t)ix->npairs * n, 1)));
       if (n) HS_CUDA(cudaMemcpy(tmp, ds->packed, (size_t)ix->npairs * n, cudaMemcpyHostToDevice));
       launch_to_vertical(tmp, n, K, ix->vstride, ix->vcodes, 0);
-      HS_CHECK(dalloc(*ix, &ix->hcodes, (size_t)ceil_div(K, 8) * n));
+      HS_CHECK(dalloc(*ix, &ix->hcodes, (size_t)hcodes_words(n, K)));
       launch_to_hcodes(tmp, n, K, ix->hcodes, 0);
       if (ds->n_active > 0) {  // point-major rows for the filtered stage 1's sparse part
         HS_CHECK(dalloc(*ix, &ix->pcodes, (size_t)pcodes_row(ix->npairs) * n));
@@ -1298,7 +1300,7 @@ int hs_builder_finish(hs_builder_t bp, double sparse_weight, double dense_weight
     ix->vstride = vertical_stride(n);
     HS_CHECK(dalloc(*ix, &ix->vcodes, (size_t)K * ix->vstride));
     launch_to_vertical(b->packed, n, K, ix->vstride, ix->vcodes, b->st);
-    HS_CHECK(dalloc(*ix, &ix->hcodes, (size_t)ceil_div(K, 8) * n));
+    HS_CHECK(dalloc(*ix, &ix->hcodes, (size_t)hcodes_words(n, K)));
     launch_to_hcodes(b->packed, n, K, ix->hcodes, b->st);
     HS_CUDA(cudaGetLastError());
     HS_CUDA(cudaStreamSynchronize(b->st));

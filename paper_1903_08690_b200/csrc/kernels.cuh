@@ -46,7 +46,7 @@ struct DeviceIndex {
   int32_t* cen_off = nullptr;  // [K] offset of centers[k] in `centers`
   float* centers = nullptr;
   uint32_t* vcodes = nullptr;  // [K][vstride] vertical nibble planes (stage1.cu)
-  uint32_t* hcodes = nullptr;  // [ceil(K/8)][n] 8 codes per point word (lut16_tc.cu)
+  uint32_t* hcodes = nullptr;  // blocked [n/128][ceil(K/8)][128] 8-code words (lut16_tc.cu)
   uint8_t* pcodes = nullptr;   // [n][pcodes_row] point-major packed codes (fuse.cu)
   int64_t vstride = 0;
   int has_sq = 0;
@@ -233,6 +233,7 @@ int64_t lut16_tc_group(const DeviceIndex& ix);  // queries per tensor-core group
 // the largest fraction of a query's points one segment (CTA) covers
 void lut16_filter_layout(const DeviceIndex& ix, int64_t nq, int64_t* nseg, double* frac);
 void launch_to_hcodes(const uint8_t* packed, int64_t n, int K, uint32_t* h, cudaStream_t st);
+int64_t hcodes_words(int64_t n, int K);
 // totals mode: u16 totals [nq][ld] of points [0, n_limit) (n_limit < 0: all)
 int launch_lut16_tc(const DeviceIndex& ix, const uint8_t* luts, int64_t nq, uint16_t* tot,
                     int64_t ld, cudaStream_t st, int64_t n_limit = -1);
