@@ -419,6 +419,45 @@ def replica_parity(args, device, s, want_cpu):
     return out, cpu
 
 
+def blas_recipe_check():
+    """The f64 dot recipe the kernels reproduce (common.cuh dot_recipe: the
+    OpenBLAS dgemv_t order) checked against THIS host's numpy/BLAS: the ADC
+    table (dense.py:212-220, widths 1-3) and the SQ residual dot
+    (dense.py:373-375, d = 256), GPU vs numpy on the same random inputs."""
+    import paper_1903_08690_b200 as hs
+    from oracle import hybrid_oracle as O
+
+    rng = np.random.default_rng(123)
+    out = {}
+    bad = tot = 0
+    for widths in ([2] * 128, [1] * 64, [3] * 40 + [2] * 4):
+        sub = np.asarray(widths, dtype=np.int64)
+        d = int(sub.sum())
+        cents = [rng.standard_normal((16, w)).astype(np.float32) for w in widths]
+        cb = hs.Codebooks(subdims=sub, centers=cents)
+        for _ in range(4):
+            q = rng.standard_normal(d)
+            g = hs.adc_table(q, cb)
+            o = O.adc_table(q, cents, sub)
+            bad += int(np.count_nonzero(g != o))
+            tot += g.size
+    out["adc_table"] = {"entries": tot, "mismatch": bad}
+    r = hs.ScalarQuantResidual(lo=rng.standard_normal(256).astype(np.float32),
+                               step=(rng.random(256) * 0.01).astype(np.float32),
+                               codes=rng.integers(0, 256, size=(4096, 256), dtype=np.uint8))
+    bad = tot = 0
+    for _ in range(4):
+        q = rng.standard_normal(256)
+        rows = rng.integers(0, 4096, size=1000)
+        g = r.dot(rows, q)
+        o = O.sq_residual_dot(r, rows, q)
+        bad += int(np.count_nonzero(g != o))
+        tot += g.size
+    out["sq_residual_dot"] = {"rows": tot, "mismatch": bad}
+    out["ok"] = out["adc_table"]["mismatch"] == 0 and bad == 0
+    return out
+
+
 def fullscale_checks(w, res_ids, res_sc, nq_check, s):
     """Exact-rerank scores of the returned ids recomputed on the host from the
     rows gathered out of the device index (rank-local ids)."""
@@ -830,6 +869,8 @@ def main():
                          f"search_batch(threads={threads}), {dt:.1f} s", **_cpu_info()}
     if parity is not None and full_check is not None:
         parity["full_scale"] = full_check
+    if parity is not None and rank == 0:
+        parity["blas_recipe"] = blas_recipe_check()
 
     # ---- roofline of the dominant kernel ----
     di = idx.dense_index

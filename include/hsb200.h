@@ -20,6 +20,9 @@
  *   hs_quantize_lut      <- quantize_lut + QuantizedLUT.bias_total dense.py:248-260, 243-245
  *   hs_lut16_scan        <- lut16_scan / lut16_scan_reference      dense.py:297-317, 263-281
  *   hs_sparse_scan       <- sparse_scan (Accumulator scores)       sparse.py:268-284
+ *   hs_sparse_scan_into  <- sparse_scan into a non-zero Accumulator sparse.py:277-282
+ *   hs_sq_decode         <- ScalarQuantResidual.decode, sq_decode dense.py:369-371, 393-394
+ *   hs_sq_residual_dot   <- ScalarQuantResidual.dot                dense.py:373-375
  *   hs_stage1_scores     <- _stage1_scores                         pipeline.py:192-203
  *   hs_select_topk       <- select_topk                            pipeline.py:165-189
  *   hs_exact_topk        <- brute_force_topk (_exact_scores)       harness.py:25-35, pipeline.py:313-322
@@ -156,6 +159,18 @@ int hs_lut16_scan(const uint8_t* packed, int64_t n, int32_t K, const uint8_t* qt
                   int32_t* totals, double* scores);
 /* f64 accumulator in layout order, weights NOT applied (sparse.py:268-284). */
 int hs_sparse_scan(hs_index_t index, const hs_query_batch* queries, double* acc);
+/* sparse_scan into a non-zero accumulator: acc [nq][n] holds the initial
+ * scores and receives acc + q_j*w added one query dim at a time in ascending
+ * dim order, each addition rounded (sparse.py:277-282, Accumulator sparse.py:239-258). */
+int hs_sparse_scan_into(hs_index_t index, const hs_query_batch* queries, double* acc);
+/* ScalarQuantResidual.decode(rows) / sq_decode (dense.py:369-371, 393-394):
+ * out [m][d] = lo + step*(codes[rows] + 0.5) in f64; rows NULL = all n (m == n). */
+int hs_sq_decode(const uint8_t* codes, int64_t n, int32_t d, const float* lo,
+                 const float* step, const int64_t* rows, int64_t m, double* out);
+/* ScalarQuantResidual.dot(rows, q) (dense.py:373-375): out [m] = decode(rows) @ q. */
+int hs_sq_residual_dot(const uint8_t* codes, int64_t n, int32_t d, const float* lo,
+                       const float* step, const int64_t* rows, int64_t m, const double* q,
+                       double* out);
 /* stage-1 scores in layout order with the index's weights (pipeline.py:192-203). */
 int hs_stage1_scores(hs_index_t index, const hs_query_batch* queries, double* scores);
 /* top-k positions per row by (score desc, tie asc); tie_ids NULL = positions. */

@@ -211,17 +211,20 @@ def _posting_list(sidx, dim):
     return sidx.ids[lo:hi], sidx.w[lo:hi]
 
 
-def sparse_scan(sidx, n, d_sparse, qdims, qvals):
+def sparse_scan(sidx, n, d_sparse, qdims, qvals, acc=None):
     """f64 accumulator in layout order (sparse.py:268-284).
 
     For each query dim in the order given (ascending), acc[ids] += f64(q) *
     f64(w).  Raises on an out-of-range dim like the reference (sparse.py:274-275).
+    `acc` (optional) is the initial accumulator (Accumulator.scores), updated
+    in place and returned.
     """
     qdims = np.asarray(qdims, dtype=np.int64)
     qvals = np.asarray(qvals, dtype=np.float32)
     if len(qdims) and int(qdims.max()) >= d_sparse:
         raise ValueError("query dimension out of range for this index")
-    acc = np.zeros(n, dtype=np.float64)
+    if acc is None:
+        acc = np.zeros(n, dtype=np.float64)
     for j, v in zip(qdims, qvals):
         entry = _posting_list(sidx, j)
         if entry is None:

@@ -77,6 +77,9 @@ def lib():
         L.hs_quantize_lut.argtypes = [P, i64, i32, i32, P, P, P, P]
         L.hs_lut16_scan.argtypes = [P, i64, i32, P, P, P, i64, P, P]
         L.hs_sparse_scan.argtypes = [P, ctypes.POINTER(QueryBatch), P]
+        L.hs_sparse_scan_into.argtypes = [P, ctypes.POINTER(QueryBatch), P]
+        L.hs_sq_decode.argtypes = [P, i64, i32, P, P, P, i64, P]
+        L.hs_sq_residual_dot.argtypes = [P, i64, i32, P, P, P, i64, P, P]
         L.hs_stage1_scores.argtypes = [P, ctypes.POINTER(QueryBatch), P]
         L.hs_select_topk.argtypes = [P, i64, i64, i64, P, P]
         L.hs_exact_topk.argtypes = [P, ctypes.POINTER(QueryBatch), i32, P, P]

@@ -641,6 +641,30 @@ static void free_index(hs_index* ix) {
 }
 }  // namespace hs
 
+namespace {
+// device buffers of a unit entry point, freed on every return path
+struct TmpBufs {
+  DeviceIndex ix;
+  std::vector<void*> ptrs;
+  template <typename T>
+  int alloc(T** p, size_t count) {
+    HS_CHECK(dalloc(ix, p, count));
+    ptrs.push_back(*p);
+    return HS_OK;
+  }
+  template <typename T>
+  int upload(T** p, const T* src, size_t count) {
+    HS_CHECK(dupload(ix, p, src, count));
+    ptrs.push_back(*p);
+    return HS_OK;
+  }
+  ~TmpBufs() {
+    for (void* p : ptrs)
+      if (p) cudaFree(p);
+  }
+};
+}  // namespace
+
 extern "C" {
 
 const char* hs_last_error(void) { return hs::last_error(); }
@@ -1104,6 +1128,98 @@ static int stage1_dump(hs_index_t index, const hs_query_batch* queries, double* 
 
 int hs_sparse_scan(hs_index_t index, const hs_query_batch* queries, double* acc) {
   return stage1_dump(index, queries, acc, true);
+}
+
+
+int hs_sparse_scan_into(hs_index_t index, const hs_query_batch* queries, double* acc) {
+  if (!index) HS_FAIL(HS_EINVAL, "null index");
+  std::lock_guard<std::mutex> lock(index->mu);
+  HS_CUDA(cudaSetDevice(index->device));
+  DevQueries dq;
+  HS_CHECK(upload_queries(*index, queries, &dq, true));
+  const int64_t nq = queries->nq, n = index->n;
+  if (nq == 0 || n == 0) return HS_OK;
+  TmpBufs t;
+  uint32_t *lb, *le;
+  double *qv, *dacc;
+  int32_t* lidx;
+  HS_CHECK(t.alloc(&lb, dq.nnz + 1));
+  HS_CHECK(t.alloc(&le, dq.nnz + 1));
+  HS_CHECK(t.alloc(&qv, dq.nnz + 1));
+  HS_CHECK(t.alloc(&lidx, dq.nnz + 1));
+  HS_CHECK(t.upload(&dacc, acc, (size_t)(nq * n)));
+  QueryView qvw;
+  qvw.nq = nq;
+  qvw.sp_indptr = dq.b.sp_indptr;
+  qvw.sp_dims = dq.b.sp_dims;
+  qvw.sp_vals = dq.b.sp_vals;
+  qvw.dense = dq.b.dense;
+  launch_map_dims(*index, qvw, dq.nnz, false, lb, le, qv, lidx, index->stream);
+  launch_scan_into(*index, qvw, dq.max_row, lb, le, qv, dacc, index->stream);
+  HS_CUDA(cudaGetLastError());
+  HS_CUDA(cudaStreamSynchronize(index->stream));
+  HS_CUDA(cudaMemcpy(acc, dacc, sizeof(double) * nq * n, cudaMemcpyDeviceToHost));
+  return HS_OK;
+}
+
+static int sq_args(const uint8_t* codes, int64_t n, int32_t d, const float* lo, const float* step,
+                   const int64_t* rows, int64_t m) {
+  if (n < 0 || d < 0 || m < 0) HS_FAIL(HS_EINVAL, "bad shape");
+  if (!lo || !step || (n * d > 0 && !codes)) HS_FAIL(HS_EINVAL, "null residual array");
+  if (rows) {
+    for (int64_t i = 0; i < m; ++i)
+      if (rows[i] < 0 || rows[i] >= n) HS_FAIL(HS_EINVAL, "row index out of range");
+  } else if (m != n) {
+    HS_FAIL(HS_EINVAL, "rows == NULL requires m == n");
+  }
+  return HS_OK;
+}
+
+int hs_sq_decode(const uint8_t* codes, int64_t n, int32_t d, const float* lo, const float* step,
+                 const int64_t* rows, int64_t m, double* out) {
+  HS_CHECK(sq_args(codes, n, d, lo, step, rows, m));
+  if (m == 0 || d == 0) return HS_OK;
+  TmpBufs t;
+  uint8_t* dc;
+  float *dlo, *dst;
+  int64_t* dr = nullptr;
+  double* dout;
+  HS_CHECK(t.upload(&dc, codes, (size_t)(n * d)));
+  HS_CHECK(t.upload(&dlo, lo, (size_t)d));
+  HS_CHECK(t.upload(&dst, step, (size_t)d));
+  if (rows) HS_CHECK(t.upload(&dr, rows, (size_t)m));
+  HS_CHECK(t.alloc(&dout, (size_t)(m * d)));
+  launch_sq_decode(dc, d, dlo, dst, dr, m, dout, 0);
+  HS_CUDA(cudaGetLastError());
+  HS_CUDA(cudaMemcpy(out, dout, sizeof(double) * m * d, cudaMemcpyDeviceToHost));
+  return HS_OK;
+}
+
+int hs_sq_residual_dot(const uint8_t* codes, int64_t n, int32_t d, const float* lo,
+                       const float* step, const int64_t* rows, int64_t m, const double* q,
+                       double* out) {
+  HS_CHECK(sq_args(codes, n, d, lo, step, rows, m));
+  if (m == 0) return HS_OK;
+  if (d == 0) {
+    for (int64_t i = 0; i < m; ++i) out[i] = 0.0;
+    return HS_OK;
+  }
+  if (!q) HS_FAIL(HS_EINVAL, "null query");
+  TmpBufs t;
+  uint8_t* dc;
+  float *dlo, *dst;
+  int64_t* dr = nullptr;
+  double *dq, *dout;
+  HS_CHECK(t.upload(&dc, codes, (size_t)(n * d)));
+  HS_CHECK(t.upload(&dlo, lo, (size_t)d));
+  HS_CHECK(t.upload(&dst, step, (size_t)d));
+  HS_CHECK(t.upload(&dq, q, (size_t)d));
+  if (rows) HS_CHECK(t.upload(&dr, rows, (size_t)m));
+  HS_CHECK(t.alloc(&dout, (size_t)m));
+  launch_sq_dot(dc, d, dlo, dst, dr, m, dq, dout, 0);
+  HS_CUDA(cudaGetLastError());
+  HS_CUDA(cudaMemcpy(out, dout, sizeof(double) * m, cudaMemcpyDeviceToHost));
+  return HS_OK;
 }
 
 int hs_stage1_scores(hs_index_t index, const hs_query_batch* queries, double* scores) {

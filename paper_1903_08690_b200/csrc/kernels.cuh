@@ -217,6 +217,9 @@ size_t stage1_smem_bytes(const DeviceIndex& ix, const Stage1Plan& p, bool ws);
 void launch_map_dims(const DeviceIndex& ix, const QueryView& q, int64_t nnz, bool use_weight,
                      uint32_t* lbeg, uint32_t* lend, double* qv, int32_t* lidx,
                      cudaStream_t st);
+void launch_scan_into(const DeviceIndex& ix, const QueryView& q, int max_row_nnz,
+                      const uint32_t* lbeg, const uint32_t* lend, const double* qv, double* acc,
+                      cudaStream_t st);
 int launch_stage1(const DeviceIndex& ix, const QueryView& q, const Stage1Plan& p,
                   const uint32_t* lbeg, const uint32_t* lend, const double* qv,
                   const int32_t* lidx, const uint8_t* luts, const double* bias_total, const double* scale,
@@ -286,5 +289,9 @@ void launch_exact_scores(const DeviceIndex& ix, const QueryView& q, int max_qnnz
                          const double* qd, Cand* out, cudaStream_t st);
 void launch_cands_to_ids(const Cand* c, int64_t total, int64_t id_offset, int64_t* ids,
                          double* scores, cudaStream_t st);
+void launch_sq_decode(const uint8_t* codes, int64_t d, const float* lo, const float* step,
+                      const int64_t* rows, int64_t m, double* out, cudaStream_t st);
+void launch_sq_dot(const uint8_t* codes, int64_t d, const float* lo, const float* step,
+                   const int64_t* rows, int64_t m, const double* q, double* out, cudaStream_t st);
 
 }  // namespace hs

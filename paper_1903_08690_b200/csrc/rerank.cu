@@ -507,11 +507,73 @@ void launch_exact_scores(const DeviceIndex& ix, const QueryView& q, int max_qnnz
                                                  out);
 }
 
+// ---------------------------------------------------------------------------
+// ScalarQuantResidual.decode / .dot / sq_decode (dense.py:369-375, 393-394) as
+// unit entry points.  decode: lo + step * (code + 0.5) in f64 (one rounding
+// per operation, like numpy's broadcast).  dot: decode(rows) @ q — numpy's
+// row-major matrix @ vector is the dgemv recipe (quarter-warp groups, the
+// same arithmetic as k_stage2); a single-row product goes through numpy's
+// ddot instead (not reproduced; within the north-star tolerance).
+// ---------------------------------------------------------------------------
+__global__ void k_sq_decode(const uint8_t* __restrict__ codes, int64_t d,
+                            const float* __restrict__ lo, const float* __restrict__ step,
+                            const int64_t* __restrict__ rows, int64_t m, double* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m * d) return;
+  const int64_t r = i / d, c = i - r * d;
+  const int64_t row = rows ? rows[r] : r;
+  const double code = (double)codes[row * d + c];
+  out[i] = __dadd_rn((double)lo[c], __dmul_rn((double)step[c], __dadd_rn(code, 0.5)));
+}
+
+__global__ void __launch_bounds__(kRrThreads) k_sq_dot(
+    const uint8_t* __restrict__ codes, int64_t d, const float* __restrict__ lo,
+    const float* __restrict__ step, const int64_t* __restrict__ rows, int64_t m,
+    const double* __restrict__ q, double* __restrict__ out) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* sq = reinterpret_cast<double*>(smem_raw);
+  double* slo = sq + d;
+  double* sstep = slo + d;
+  for (int64_t i = threadIdx.x; i < d; i += blockDim.x) {
+    sq[i] = q[i];
+    slo[i] = (double)lo[i];
+    sstep[i] = (double)step[i];
+  }
+  __syncthreads();
+  const int lane4 = threadIdx.x & 3;
+  const unsigned gmask = 0xFu << ((threadIdx.x & 31) & ~3);
+  const int64_t groups = (int64_t)gridDim.x * (blockDim.x / 4);
+  // uniform trip count per group: the group's shuffles stay converged
+  for (int64_t r = (int64_t)blockIdx.x * (blockDim.x / 4) + threadIdx.x / 4; r < m; r += groups) {
+    const uint8_t* row = codes + (rows ? rows[r] : r) * d;
+    auto elem = [&](int i) -> double {
+      return __dadd_rn(slo[i], __dmul_rn(sstep[i], (double)row[i] + 0.5));
+    };
+    const double dot = group4_dot_recipe(elem, sq, (int)d, lane4, gmask);
+    if (lane4 == 0) out[r] = dot;
+  }
+}
+
 void launch_cands_to_ids(const Cand* c, int64_t total, int64_t id_offset, int64_t* ids,
                          double* scores, cudaStream_t st) {
   if (total <= 0) return;
   k_cands_to_ids<<<(unsigned)ceil_div(total, 256), 256, 0, st>>>(c, total, id_offset, ids,
                                                                   scores);
+}
+
+void launch_sq_decode(const uint8_t* codes, int64_t d, const float* lo, const float* step,
+                      const int64_t* rows, int64_t m, double* out, cudaStream_t st) {
+  if (m * d <= 0) return;
+  k_sq_decode<<<(unsigned)ceil_div(m * d, 256), 256, 0, st>>>(codes, d, lo, step, rows, m, out);
+}
+
+void launch_sq_dot(const uint8_t* codes, int64_t d, const float* lo, const float* step,
+                   const int64_t* rows, int64_t m, const double* q, double* out, cudaStream_t st) {
+  if (m <= 0) return;
+  const size_t smem = 3 * sizeof(double) * (size_t)std::max<int64_t>(d, 1);
+  cudaFuncSetAttribute(k_sq_dot, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int64_t blocks = std::min<int64_t>(ceil_div(m, kRrThreads / 4), 148 * 8);
+  k_sq_dot<<<(unsigned)blocks, kRrThreads, smem, st>>>(codes, d, lo, step, rows, m, q, out);
 }
 
 }  // namespace hs

@@ -1167,6 +1167,26 @@ __global__ void k_map_dims(const uint32_t* __restrict__ dims_q, const float* __r
   qv[i] = (double)v;
 }
 
+// sparse_scan into a caller-supplied accumulator (sparse.py:277-282): the k-th
+// query dim of every query is one launch, so each point receives its
+// products one dim after another in the query's ascending dim order, each
+// `acc = acc + q_j * w` rounded like numpy's `acc.scores[ids] += qv * w`.
+// Within one dim the posting ids are distinct, so the scatter is race free.
+__global__ void k_scan_dim_into(const uint2* __restrict__ post, const int64_t* __restrict__ qptr,
+                                const uint32_t* __restrict__ lbeg, const uint32_t* __restrict__ lend,
+                                const double* __restrict__ qv, int k, int64_t n, double* acc) {
+  const int64_t q = blockIdx.y;
+  const int64_t i = qptr[q] + k;
+  if (i >= qptr[q + 1]) return;
+  const uint32_t b = lbeg[i], e = lend[i];
+  const double v = qv[i];
+  double* row = acc + q * n;
+  for (uint32_t p = b + blockIdx.x * blockDim.x + threadIdx.x; p < e; p += gridDim.x * blockDim.x) {
+    const uint2 pw = __ldg(post + p);
+    row[pw.x] = __dadd_rn(row[pw.x], __dmul_rn(v, (double)__uint_as_float(pw.y)));
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Sparse pre-pass: bucket one query's postings by 4096-slot chunk.
 // Counting sort on the chunk id; dims are scattered one after another (in the
@@ -1610,6 +1630,16 @@ void launch_map_dims(const DeviceIndex& ix, const QueryView& q, int64_t nnz, boo
       q.sp_dims, q.sp_vals, nnz, ix.post_dims, ix.n_active, ix.post_ptr,
       (float)ix.sparse_weight, use_weight && ix.sparse_weight != 1.0 ? 1 : 0, lbeg, lend, qv,
       lidx);
+}
+
+void launch_scan_into(const DeviceIndex& ix, const QueryView& q, int max_row_nnz,
+                      const uint32_t* lbeg, const uint32_t* lend, const double* qv, double* acc,
+                      cudaStream_t st) {
+  if (q.nq <= 0 || ix.n <= 0 || ix.nnz_post == 0) return;
+  for (int k = 0; k < max_row_nnz; ++k) {
+    dim3 grid(2 * 148, (unsigned)q.nq);
+    k_scan_dim_into<<<grid, 256, 0, st>>>(ix.post, q.sp_indptr, lbeg, lend, qv, k, ix.n, acc);
+  }
 }
 
 int launch_stage1(const DeviceIndex& ix, const QueryView& q, const Stage1Plan& p,

@@ -3,7 +3,9 @@ from .builder import (  # noqa: F401
     pack_codes, pq_encode, sq_encode, subspace_widths, train_codebooks, unpack_codes,
     whiten_apply, whiten_fit,
 )
-from .search import adc_table, lut16_scan, lut16_scan_reference, quantize_lut  # noqa: F401
+from .search import (  # noqa: F401
+    adc_table, lut16_scan, lut16_scan_reference, quantize_lut, sq_decode,
+)
 from .types import (  # noqa: F401
     LUT16_CENTERS, Codebooks, DenseIndex, PQCodes, QuantizedLUT, ScalarQuantResidual,
     WhiteningTransform,

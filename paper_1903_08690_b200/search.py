@@ -431,6 +431,50 @@ def adc_table(query_dense, codebooks) -> np.ndarray:
     return T
 
 
+def _sq_rows(r, rows):
+    codes = np.ascontiguousarray(r.codes, dtype=np.uint8)
+    if codes.ndim != 2:
+        raise ValueError("codes must be (n, d)")
+    n, d = codes.shape
+    if isinstance(rows, slice):
+        idx = np.arange(n, dtype=np.int64)[rows]
+    else:
+        idx = np.asarray(rows)
+        if idx.dtype == bool:
+            idx = np.flatnonzero(idx)
+        idx = np.where(idx < 0, idx + n, idx).astype(np.int64).reshape(-1)
+    return codes, n, d, nat.contig(r.lo, np.float32), nat.contig(r.step, np.float32), \
+        nat.contig(idx, np.int64)
+
+
+def sq_residual_decode(r, rows=slice(None)) -> np.ndarray:
+    """ScalarQuantResidual.decode (dense.py:369-371) on the GPU: f64 rows."""
+    codes, n, d, lo, step, idx = _sq_rows(r, rows)
+    nat.require_gpu()
+    out = np.empty((len(idx), d), dtype=np.float64)
+    nat.check(nat.lib().hs_sq_decode(nat.ptr(codes), n, d, nat.ptr(lo), nat.ptr(step),
+                                     nat.ptr(idx), len(idx), nat.ptr(out)))
+    return out
+
+
+def sq_residual_dot(r, rows, q) -> np.ndarray:
+    """ScalarQuantResidual.dot (dense.py:373-375) on the GPU: decode(rows) @ q."""
+    codes, n, d, lo, step, idx = _sq_rows(r, rows)
+    qv = nat.contig(np.asarray(q, dtype=np.float64).reshape(-1), np.float64)
+    if qv.shape[0] != d:
+        raise ValueError(f"shapes ({len(idx)},{d}) and ({qv.shape[0]},) not aligned")
+    nat.require_gpu()
+    out = np.empty(len(idx), dtype=np.float64)
+    nat.check(nat.lib().hs_sq_residual_dot(nat.ptr(codes), n, d, nat.ptr(lo), nat.ptr(step),
+                                           nat.ptr(idx), len(idx), nat.ptr(qv), nat.ptr(out)))
+    return out
+
+
+def sq_decode(r) -> np.ndarray:
+    """sq_decode (dense.py:393-394): every row decoded, on the GPU."""
+    return sq_residual_decode(r)
+
+
 def quantize_lut(table) -> QuantizedLUT:
     """Shared-scale 8-bit LUT (bias, scale, u8 table, bias_total) on the GPU."""
     T = nat.contig(table, np.float64)
@@ -513,13 +557,16 @@ def sparse_scan(index, query: SparseVector, acc: Accumulator, device: int = 0) -
             h = DeviceIndex(sparse_index=index, device=device)
             cache[("sparse", device)] = h
     qa = QueryArrays(np.array([0, dims.size]), dims, q.values, np.zeros((1, 0), np.float32))
-    out = np.empty((1, int(index.n)), dtype=np.float64)
     b = qa.batch()
-    nat.check(nat.lib().hs_sparse_scan(h.handle, ctypes.byref(b), nat.ptr(out)))
     if np.any(acc.scores):
-        acc.scores += out[0]  # exact only for a zero accumulator (the pipeline's case)
+        # non-zero accumulator: products added onto it one dim at a time, in
+        # the query's (ascending) dim order, like sparse.py:277-282
+        out = np.ascontiguousarray(acc.scores, dtype=np.float64).reshape(1, -1).copy()
+        nat.check(nat.lib().hs_sparse_scan_into(h.handle, ctypes.byref(b), nat.ptr(out)))
     else:
-        acc.scores[:] = out[0]
+        out = np.empty((1, int(index.n)), dtype=np.float64)
+        nat.check(nat.lib().hs_sparse_scan(h.handle, ctypes.byref(b), nat.ptr(out)))
+    acc.scores[:] = out[0]
     acc.lines_touched += _lines_touched(index, dims, acc.line_capacity)
     return acc
 

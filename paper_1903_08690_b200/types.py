@@ -334,8 +334,16 @@ class ScalarQuantResidual:
     codes: np.ndarray
 
     def decode(self, rows=slice(None)) -> np.ndarray:
-        c = self.codes[rows].astype(np.float64)
-        return self.lo.astype(np.float64) + self.step.astype(np.float64) * (c + 0.5)
+        """f64 rows lo + step * (code + 0.5), on the GPU (dense.py:369-371)."""
+        from .search import sq_residual_decode
+
+        return sq_residual_decode(self, rows)
+
+    def dot(self, rows, q) -> np.ndarray:
+        """decode(rows) @ q, on the GPU (dense.py:373-375)."""
+        from .search import sq_residual_dot
+
+        return sq_residual_dot(self, rows, q)
 
     def memory_bytes(self) -> int:
         return int(self.lo.nbytes + self.step.nbytes + self.codes.nbytes)
