@@ -295,6 +295,41 @@ def sq_residual_dot(residual, rows, qw):
     return dec @ np.asarray(qw, dtype=np.float64)
 
 
+def dot_recipe(x, y):
+    """One f64 dot product in the OpenBLAS `dgemv_t` order the kernels follow
+    (SURVEY Appendix A.1): four FMA lanes over blocks of 4 combined as
+    (L0+L2)+(L1+L3); a one-element tail is FMA'd onto that, a longer tail is
+    summed as fma(x0, y0, x1*y1) (+ fma for a third) and then added.  Exact
+    rational arithmetic stands in for the hardware FMA, so the result does not
+    depend on this host's BLAS, thread count or batch shape (numpy's own
+    `A @ v` rounds rows differently in the remainder kernels of a thread's
+    row block).  Small inputs only (pure Python)."""
+    from fractions import Fraction
+
+    x = [float(v) for v in x]
+    y = [float(v) for v in y]
+
+    def fma(a, b, c):
+        return float(Fraction(a) * Fraction(b) + Fraction(c))
+
+    w = len(x)
+    lanes = [0.0, 0.0, 0.0, 0.0]
+    m = w - (w % 4)
+    for i in range(0, m, 4):
+        for j in range(4):
+            lanes[j] = fma(x[i + j], y[i + j], lanes[j])
+    base = (lanes[0] + lanes[2]) + (lanes[1] + lanes[3])
+    rem = w - m
+    if rem == 0:
+        return base
+    if rem == 1:
+        return fma(x[m], y[m], base) if m else x[m] * y[m]
+    p = fma(x[m], y[m], x[m + 1] * y[m + 1])
+    for k in range(m + 2, w):
+        p = fma(x[k], y[k], p)
+    return base + p if m else p
+
+
 def sparse_residual_dot(index, layout_rows, qdims, qvals):
     """Stage-3 residual term (pipeline.py:303-310)."""
     res = index.sparse_residual

@@ -72,6 +72,9 @@ from .search import (  # noqa: F401
     stage1_scores,
 )
 
+from .search import sq_decode  # noqa: F401,E402
 from .devbuild import DeviceBuiltIndex, DeviceDataset, GpuBuild  # noqa: F401
+# the reference's submodule import paths (hybridsearch.dense, .sparse, ...)
+from . import data, dense, harness, pipeline, sparse  # noqa: F401,E402
 
 __version__ = "0.2.0"
