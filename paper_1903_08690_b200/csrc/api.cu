@@ -120,7 +120,13 @@ int resolve_sizes(const DeviceIndex& ix, const hs_search_params* p, Sizes* s) {
 }
 
 constexpr int64_t kMaxRerank = 8192;  // k1/k2 held in shared memory for stages 2-3
-constexpr int64_t kTcMinQueries = 64;  // batches at least this large use the tensor cores
+// batches at least this large use the tensor cores; smaller ones stream the
+// codes once per query (one tensor-core pass costs about as much as ten
+// streamed queries).  HSB200_TC_MIN: dev / test knob.
+int64_t tc_min_queries() {
+  const char* e = std::getenv("HSB200_TC_MIN");
+  return e ? std::max<int64_t>(1, std::atoll(e)) : 16;
+}
 
 // time accumulation helpers.  Two modes: FULL records an event after every
 // kernel (the bench's per-kernel breakdown; it serialises the aux-stream
@@ -204,14 +210,19 @@ int run_search(DeviceIndex& ix, const hs_query_batch& qb, int64_t nnz, int max_q
     HS_FAIL(HS_EUNSUPPORTED, "overfetch*h above 8192 candidates is not supported");
   if (max_qnnz > 8192) HS_FAIL(HS_EUNSUPPORTED, "queries with more than 8192 sparse nonzeros");
 
-  // tensor-core LUT16 for large batches (>= kTcMinQueries queries): either
+  // tensor-core LUT16 for large batches (>= tc_min_queries() queries): either
   // threshold-filtered (fuse.cu: sample -> threshold -> filtered tensor-core
   // pass -> candidate scoring) or, when that does not apply, u16 totals for
   // every point followed by the full stage-1 scan
   const int64_t d = ix.d_dense;
   const int64_t tc_ld = lut16_tc_ld(ix.n);
-  const bool use_tc = d > 0 && lut16_tc_supported(ix) && nq >= kTcMinQueries &&
+  const bool use_tc = d > 0 && lut16_tc_supported(ix) && nq >= tc_min_queries() &&
                       !getenv_flag("HSB200_NO_TC");
+  // smaller batches: the same threshold-filtered stage 1 with the HBM-bound
+  // CUDA-core scan (lut16_stream.cu) in place of the tensor-core pass — every
+  // query streams the codes once
+  const bool use_stream = d > 0 && !use_tc && lut16_stream_supported(ix) &&
+                          !getenv_flag("HSB200_NO_STREAM");
   const bool use_buckets = nnz > 0 && ix.nnz_post > 0 && !getenv_flag("HSB200_NO_BUCKETS");
   const bool sparse_part = nnz > 0 && ix.nnz_post > 0;
   // bucketing overlapped with the dense chain on the aux stream (not while
@@ -237,7 +248,7 @@ int run_search(DeviceIndex& ix, const hs_query_batch& qb, int64_t nnz, int max_q
   // threshold from the exact sample top-k1 (full stage-1 kernels) instead of
   // the sample's totals (dev / A-B knob)
   const bool exact_sample = getenv_flag("HSB200_EXACT_SAMPLE");
-  const bool use_fuse = use_tc && ix.K <= 256 && sz.k1 <= 4096 && ix.n >= 8 * m_s &&
+  const bool use_fuse = (use_tc || use_stream) && ix.K <= 256 && sz.k1 <= 4096 && ix.n >= 8 * m_s &&
                         (!sparse_part || (use_buckets && ix.pcodes != nullptr)) &&
                         !getenv_flag("HSB200_NO_FUSE");
   const int64_t expect = (int64_t)((double)sz.k1 * (double)ix.n / (double)m_s);
@@ -247,7 +258,8 @@ int run_search(DeviceIndex& ix, const hs_query_batch& qb, int64_t nnz, int max_q
   int64_t nseg = 0, Cf = 0;
   auto seg_cap = [&](int64_t qb) {
     double frac = 1.0;
-    lut16_filter_layout(ix, qb, &nseg, &frac);
+    if (use_tc) lut16_filter_layout(ix, qb, &nseg, &frac);
+    else lut16_stream_layout(ix, &nseg, &frac);
     Cf = ((int64_t)(4.0 * (double)expect * frac) + 64 + 31) / 32 * 32;
     if (ev_c) Cf = std::max<int64_t>(1, std::atoll(ev_c));
   };
@@ -259,8 +271,8 @@ int run_search(DeviceIndex& ix, const hs_query_batch& qb, int64_t nnz, int max_q
   const int64_t ld_s = lut16_tc_ld(m_s);
   const int64_t words = ceil_div(ix.n, 32);
   // query-chunk size bounded by scratch for the stage-1 per-tile outputs
-  if (use_tc) {
-    const int64_t grp = lut16_tc_group(ix);
+  if (use_tc || (use_stream && use_fuse)) {
+    const int64_t grp = use_tc ? lut16_tc_group(ix) : 1;
     const double per_q = use_fuse
         ? (double)Cf * nseg * 8 + (double)Mf * 16 + (double)ld_s * 2 +
               (sparse_part ? words * 4.0 : 0.0)
@@ -445,9 +457,10 @@ int run_search(DeviceIndex& ix, const hs_query_batch& qb, int64_t nnz, int max_q
     // every chunk of a tensor-core batch stays on the tensor cores: a short
     // last chunk gets a narrower query group (the MMA N shrinks with it)
     const bool tc_chunk = use_tc;
-    if (tc_chunk && use_fuse) {
+    if (use_fuse) {
       // 1. u16 totals of the first m_s points -> threshold
-      HS_CHECK(launch_lut16_tc(ix, luts, nqc, P.tot_s, ld_s, st, m_s));
+      if (tc_chunk) HS_CHECK(launch_lut16_tc(ix, luts, nqc, P.tot_s, ld_s, st, m_s));
+      else HS_CHECK(launch_lut16_stream_totals(ix, luts, nqc, P.tot_s, ld_s, st, m_s));
       ix.launches += 1;
       if (exact_sample) {
       HS_CHECK(join_sb());
@@ -466,14 +479,16 @@ int run_search(DeviceIndex& ix, const hs_query_batch& qb, int64_t nnz, int max_q
         ix.launches += 1;
       }
       if (tm) tm->mark("sample");
-      // 2. filtered tensor-core pass over every point
-      HS_CHECK(launch_lut16_filter(ix, luts, nqc, P.tlim, P.list, P.lcnt, Cf, st));
+      // 2. filtered pass over every point (tensor cores, or the streamed scan)
+      if (tc_chunk) HS_CHECK(launch_lut16_filter(ix, luts, nqc, P.tlim, P.list, P.lcnt, Cf, st));
+      else HS_CHECK(launch_lut16_stream_filter(ix, luts, nqc, P.tlim, P.list, P.lcnt, Cf, st));
       ix.launches += 1;
-      if (tm) tm->mark("lut16_tc");
+      if (tm) tm->mark(tc_chunk ? "lut16_tc" : "lut16_stream");
       // 3. candidate scoring (+ touched points) and exact top-k1
       int64_t nseg_c = 0;
       double frac_c = 1.0;
-      lut16_filter_layout(ix, nqc, &nseg_c, &frac_c);
+      if (tc_chunk) lut16_filter_layout(ix, nqc, &nseg_c, &frac_c);
+      else lut16_stream_layout(ix, &nseg_c, &frac_c);
       HS_CHECK(join_sb());
       HS_CHECK(launch_fuse_cands(ix, nqc, luts, btot, scl, off, P.list, P.lcnt, Cf, (int)nseg_c,
                                  sparse_part ? &sb : nullptr, P.bitmap, P.fout, Mf, P.fcnt,
@@ -804,12 +819,11 @@ int hs_index_create(const hs_index_desc* ds, int device, hs_index_t* out) {
     HS_CHECK(dupload(*ix, &ix->centers, ds->centers, csum));
     if (ds->n_centers == 16 && ds->packed) {
       // upload the reference pair-major layout, re-tile into vertical planes
-      ix->vstride = vertical_stride(n);
-      HS_CHECK(dalloc(*ix, &ix->vcodes, (size_t)K * ix->vstride));
+      HS_CHECK(dalloc(*ix, &ix->vcodes, (size_t)vertical_words(n, K)));
       uint8_t* tmp = nullptr;
       HS_CUDA(cudaMalloc(&tmp, std::max<size_t>((size_t)ix->npairs * n, 1)));
       if (n) HS_CUDA(cudaMemcpy(tmp, ds->packed, (size_t)ix->npairs * n, cudaMemcpyHostToDevice));
-      launch_to_vertical(tmp, n, K, ix->vstride, ix->vcodes, 0);
+      launch_to_vertical(tmp, n, K, ix->vcodes, 0);
       HS_CHECK(dalloc(*ix, &ix->hcodes, (size_t)hcodes_words(n, K)));
       launch_to_hcodes(tmp, n, K, ix->hcodes, 0);
       if (ds->n_active > 0) {  // point-major rows for the filtered stage 1's sparse part
@@ -1413,9 +1427,8 @@ int hs_builder_finish(hs_builder_t bp, double sparse_weight, double dense_weight
     HS_CHECK(dupload(*ix, &ix->dim_off, doff.data(), K));
     HS_CHECK(dupload(*ix, &ix->cen_off, coff.data(), K));
     HS_CHECK(dupload(*ix, &ix->centers, b->centers.data(), csum));
-    ix->vstride = vertical_stride(n);
-    HS_CHECK(dalloc(*ix, &ix->vcodes, (size_t)K * ix->vstride));
-    launch_to_vertical(b->packed, n, K, ix->vstride, ix->vcodes, b->st);
+    HS_CHECK(dalloc(*ix, &ix->vcodes, (size_t)vertical_words(n, K)));
+    launch_to_vertical(b->packed, n, K, ix->vcodes, b->st);
     HS_CHECK(dalloc(*ix, &ix->hcodes, (size_t)hcodes_words(n, K)));
     launch_to_hcodes(b->packed, n, K, ix->hcodes, b->st);
     HS_CUDA(cudaGetLastError());

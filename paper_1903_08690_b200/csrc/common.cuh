@@ -225,4 +225,31 @@ __device__ __forceinline__ void bitonic_sort_block(Cand* a, int n) {
   }
 }
 
+// --------------------------------------------------------------------------
+// In-register LUT16 (the GPU analogue of the paper's PSHUFB table,
+// PAPER.md:374-397): eight 16-entry u8 lookups with PRMT.
+// --------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t s) {
+  uint32_t r;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(s));
+  return r;
+}
+
+// w: nibble j = code of point j; T: the u8 table (entries 0..15 in the bytes
+// of T.x..T.w).  r0 = table bytes of points 0-3, r1 = points 4-7.  PRMT
+// selects among 8 bytes by the low 3 bits of a selector nibble (bit 3 set =
+// sign-replicate: garbage here, blended away), so entries 0-7 and 8-15 are
+// looked up separately and blended by a byte mask of the codes' bit 3.  The
+// mask is itself one PRMT in sign-replicate mode: the msb of byte j of w is
+// bit 3 of point 2j+1, the msb of byte j of w << 4 is bit 3 of point 2j.
+__device__ __forceinline__ void lut8(const uint4& T, uint32_t w, uint32_t& r0, uint32_t& r1) {
+  const uint32_t x = w ^ 0x88888888u;  // entries 8..15 become selectors 0..7
+  const uint32_t a0 = prmt(T.x, T.y, w), a1 = prmt(T.x, T.y, w >> 16);
+  const uint32_t b0 = prmt(T.z, T.w, x), b1 = prmt(T.z, T.w, x >> 16);
+  const uint32_t w4 = w << 4;
+  const uint32_t k0 = prmt(w, w4, 0x9D8Cu), k1 = prmt(w, w4, 0xBFAEu);
+  r0 = (b0 & k0) | (a0 & ~k0);
+  r1 = (b1 & k1) | (a1 & ~k1);
+}
+
 }  // namespace hs

@@ -33,6 +33,7 @@ namespace hs {
 namespace {
 
 constexpr int kFuseThreads = 256;
+constexpr int kMaxSeg = 2 * kNumSMs + 2;  // list segments per query (tensor-core pass: one per CTA; streamed scan: two per SM)
 
 __device__ __forceinline__ double dense_score(double btot, double scl, double off, uint32_t t) {
   return __dadd_rn(__dadd_rn(btot, __dmul_rn(scl, (double)t)), off);
@@ -185,13 +186,14 @@ __global__ void __launch_bounds__(kFuseThreads) k_fuse_cands(FuseArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   uint8_t* lut = smem_raw;  // [Kp][16]
   __shared__ uint32_t s_cnt;
-  __shared__ uint32_t s_pre[kNumSMs + 2];  // prefix of the segment counts
+  __shared__ uint32_t s_pre[kMaxSeg + 1];  // prefix of the segment counts
   __shared__ int s_over;
   const int64_t q = blockIdx.x;
   const int tid = threadIdx.x;
   if (tid == 0) s_over = 0;
   __syncthreads();
-  if (tid < a.nseg && a.cnt[q * a.nseg + tid] > (uint32_t)a.cap) s_over = 1;
+  for (int c = tid; c < a.nseg; c += blockDim.x)
+    if (a.cnt[q * a.nseg + c] > (uint32_t)a.cap) s_over = 1;
   if (tid == 0) {
     uint32_t run = 0;
     for (int c = 0; c < a.nseg; ++c) {
@@ -368,7 +370,7 @@ int launch_fuse_cands(const DeviceIndex& ix, int64_t nq, const uint8_t* luts, co
   a.cnt = cnt;
   a.cap = cap;
   a.nseg = nseg;
-  if (nseg > kNumSMs + 1) HS_FAIL(HS_EINVAL, "too many list segments");
+  if (nseg > kMaxSeg) HS_FAIL(HS_EINVAL, "too many list segments");
   a.bmode = sb ? sb->mode : nullptr;
   a.boff = sb ? sb->boff : nullptr;
   a.bslots = sb ? sb->slots : nullptr;

@@ -45,10 +45,9 @@ struct DeviceIndex {
   int32_t* dim_off = nullptr;  // [K] first dense dim of subspace k
   int32_t* cen_off = nullptr;  // [K] offset of centers[k] in `centers`
   float* centers = nullptr;
-  uint32_t* vcodes = nullptr;  // [K][vstride] vertical nibble planes (stage1.cu)
+  uint32_t* vcodes = nullptr;  // blocked [n/4096][K][512] vertical nibble planes (lut16_stream.cu, stage1.cu)
   uint32_t* hcodes = nullptr;  // blocked [n/128][ceil(K/8)][128] 8-code words (lut16_tc.cu)
   uint8_t* pcodes = nullptr;   // [n][pcodes_row] point-major packed codes (fuse.cu)
-  int64_t vstride = 0;
   int has_sq = 0;
   float *sq_lo = nullptr, *sq_step = nullptr;
   uint8_t* sq_codes = nullptr;  // [n][d_dense]
@@ -208,9 +207,6 @@ void launch_sparse_bucket(const DeviceIndex& ix, const QueryView& q, const uint3
                           const uint32_t* lend, const double* qv, const SparseBuckets& sb,
                           cudaStream_t st);
 int stage1_chunk_points();
-int64_t vertical_stride(int64_t n);
-void launch_to_vertical(const uint8_t* packed, int64_t n, int K, int64_t vstride, uint32_t* v,
-                        cudaStream_t st);
 Stage1Plan plan_stage1(const DeviceIndex& ix, int64_t nq, int64_t k, int max_qnnz, int mode,
                        int64_t n_limit = -1);
 size_t stage1_smem_bytes(const DeviceIndex& ix, const Stage1Plan& p, bool ws);
@@ -227,6 +223,21 @@ int launch_stage1(const DeviceIndex& ix, const QueryView& q, const Stage1Plan& p
                   uint32_t* dump_tot = nullptr, bool raw_dense = false,
                   const SparseBuckets* sb = nullptr, const uint16_t* tot16 = nullptr,
                   int64_t tot_ld = 0);
+
+// lut16_stream.cu (HBM-bound LUT16 scan for small batches; owns the vertical code layout)
+int64_t vertical_words(int64_t n, int K);
+void launch_to_vertical(const uint8_t* packed, int64_t n, int K, uint32_t* v, cudaStream_t st);
+bool lut16_stream_supported(const DeviceIndex& ix);
+// filter-mode list layout: one segment per CTA, each a contiguous range of
+// 4096-point code blocks; frac = the largest share of the points in one
+void lut16_stream_layout(const DeviceIndex& ix, int64_t* nseg, double* frac);
+// u16 totals [nq][ld] of points [0, n_limit) (n_limit < 0: all)
+int launch_lut16_stream_totals(const DeviceIndex& ix, const uint8_t* luts, int64_t nq,
+                               uint16_t* tot, int64_t ld, cudaStream_t st, int64_t n_limit = -1);
+// same contract as launch_lut16_filter, segments of lut16_stream_layout
+int launch_lut16_stream_filter(const DeviceIndex& ix, const uint8_t* luts, int64_t nq,
+                               const uint32_t* tlim, uint2* list, uint32_t* cnt, int64_t cap,
+                               cudaStream_t st);
 
 // lut16_tc.cu (tensor-core batched LUT16 totals)
 bool lut16_tc_supported(const DeviceIndex& ix);

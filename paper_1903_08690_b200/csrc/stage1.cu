@@ -72,8 +72,7 @@ struct Stage1Args {
   // dense
   int has_dense;
   int K, Kp;
-  const uint32_t* vcodes;  // [K][vstride] u32, nibble j = point 8*word + j
-  int64_t vstride;
+  const uint32_t* vcodes;  // [chunk][K][kChunk/8] u32, nibble j = point 8*word + j of the chunk
   const uint8_t* luts;
   const double* bias_total;
   const double* scale;
@@ -103,28 +102,6 @@ struct Stage1Args {
   const int* qmask;    // only queries with qmask[q] != 0 run (null: all)
   uint32_t ring_bytes; // WS: posting ring size (multiple of 16, >= 2 pieces)
 };
-
-__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t s) {
-  uint32_t r;
-  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(s));
-  return r;
-}
-
-// Eight 16-entry lookups.  w: nibble j = code of point j.  T: the u8 table
-// (entries 0..15 in bytes of T.x..T.w).  r0 = bytes for points 0-3, r1 = 4-7.
-__device__ __forceinline__ void lut8(const uint4& T, uint32_t w, uint32_t& r0, uint32_t& r1) {
-  const uint32_t x = w ^ 0x88888888u;             // entries 8..15 become selectors 0..7
-  const uint32_t a0 = prmt(T.x, T.y, w), a1 = prmt(T.x, T.y, w >> 16);
-  const uint32_t b0 = prmt(T.z, T.w, x), b1 = prmt(T.z, T.w, x >> 16);
-  // mask selector: nibble bit 3 = code bit 3, bit 0 = code bit 3 too (bits 1-2
-  // carry junk from the next code).  Bytes of 0x80008000: even 0x00, odd 0x80,
-  // so a clear bit 3 selects 0x00 and a set one sign-replicates 0x80 -> 0xFF.
-  const uint32_t s = (w & 0x88888888u) | ((w >> 3) & 0x77777777u);
-  const uint32_t k0 = prmt(0x80008000u, 0x80008000u, s);
-  const uint32_t k1 = prmt(0x80008000u, 0x80008000u, s >> 16);
-  r0 = (b0 & k0) | (a0 & ~k0);
-  r1 = (b1 & k1) | (a1 & ~k1);
-}
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -631,7 +608,7 @@ __global__ void __launch_bounds__(WS ? kThreads + 32 : kThreads, DM == 0 ? MINB0
     off = a.offset ? a.offset[q] : 0.0;
   }
   const uint2* vc = reinterpret_cast<const uint2*>(a.vcodes);
-  const int64_t vrow = a.vstride >> 1;  // uint2 per subspace row
+  constexpr int64_t vrow = kChunk / 16;  // uint2 per subspace row of a chunk's code block
   // u16 totals are prefetched two chunks ahead (tnext: next chunk, tnext2:
   // the one after)
   uint4 tnext0 = make_uint4(0u, 0u, 0u, 0u), tnext1 = tnext0, tnext20 = tnext0, tnext21 = tnext0;
@@ -699,7 +676,8 @@ __global__ void __launch_bounds__(WS ? kThreads + 32 : kThreads, DM == 0 ? MINB0
         tot[2 * j + 1] = w8[j] >> 16;
       }
     } else if (DM == 1 && p0 < ce && !(a.exp_flags & 1)) {
-      const uint2* col = vc + (p0 >> 4);
+      // blocked vertical planes (lut16_stream.cu): chunk cb/kChunk, row k, word pair tid
+      const uint2* col = vc + (cb / kChunk) * (int64_t)a.K * vrow + tid;
       uint32_t acc2[8];
 #pragma unroll
       for (int j = 0; j < 8; ++j) acc2[j] = 0;
@@ -1446,24 +1424,6 @@ __global__ void k_skip_rows(const uint2* __restrict__ post, const uint32_t* __re
   }
 }
 
-// pair-major packed codes (dense.py:156-170) -> vertical nibble planes
-__global__ void k_to_vertical(const uint8_t* __restrict__ packed, int64_t n, int K,
-                              int64_t vstride, uint32_t* __restrict__ v) {
-  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // word (8 points)
-  const int k = blockIdx.y;
-  if (g >= vstride) return;
-  const uint8_t* row = packed + (int64_t)(k >> 1) * n;
-  const int sh = (k & 1) ? 4 : 0;
-  uint32_t w = 0;
-#pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    const int64_t pt = g * 8 + j;
-    const uint32_t c = pt < n ? ((row[pt] >> sh) & 0xFu) : 0u;
-    w |= c << (4 * j);
-  }
-  v[(int64_t)k * vstride + g] = w;
-}
-
 }  // namespace
 
 int stage1_chunk_points() { return kChunk; }
@@ -1527,19 +1487,6 @@ void launch_sparse_bucket(const DeviceIndex& ix, const QueryView& q, const uint3
   const int ys = (int)std::min<int64_t>(ceil_div(sb.nchunks, kAggWarps), 8);
   k_bucket_aggregate<<<dim3((unsigned)q.nq, (unsigned)ys), kAggWarps * 32, asmem, st>>>(
       sb.mode, sb.boff, sb.nchunks, sb.capq, sb.slots, sb.vals);
-}
-
-int64_t vertical_stride(int64_t n) {
-  // u32 words per subspace row: 2 words per 16 points, padded to 64 B
-  const int64_t words = ((n + 15) / 16) * 2;
-  return ((words + 15) / 16) * 16;
-}
-
-void launch_to_vertical(const uint8_t* packed, int64_t n, int K, int64_t vstride, uint32_t* v,
-                        cudaStream_t st) {
-  if (K <= 0) return;
-  dim3 grid((unsigned)ceil_div(vstride, 256), (unsigned)K);
-  k_to_vertical<<<grid, 256, 0, st>>>(packed, n, K, vstride, v);
 }
 
 Stage1Plan plan_stage1(const DeviceIndex& ix, int64_t nq, int64_t k, int max_qnnz, int mode,
@@ -1668,7 +1615,6 @@ int launch_stage1(const DeviceIndex& ix, const QueryView& q, const Stage1Plan& p
   a.K = ix.K;
   a.Kp = ix.Kp;
   a.vcodes = ix.vcodes;
-  a.vstride = ix.vstride;
   a.luts = luts;
   a.bias_total = bias_total;
   a.scale = scale;

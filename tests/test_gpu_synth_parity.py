@@ -214,3 +214,37 @@ def test_filtered_stage1_negative_values_and_repeats(name, n, nq, top_t, negate,
         ids, sc, _ = O.search_topk(idx, *O.query_parts(qs, i), s["h"], **kw)
         assert fused[i].ids.tolist() == ids.tolist()
         np.testing.assert_allclose(fused[i].scores, sc, rtol=1e-9)
+
+
+@pytest.mark.parametrize("name,n,nq,sample,cap,over", [
+    ("cfg2", 60_000, 1, 4096, None, {}),      # single hybrid query (K=128)
+    ("cfg2", 60_000, 7, 4096, None, {}),
+    ("cfg3", 80_000, 5, 4096, None, {}),      # dense only (K=64)
+    ("cfg1", 50_000, 12, 4096, None, {"pq_subspaces": 25}),  # K not a multiple of the 8-row slice
+    ("cfg2", 60_000, 9, 2048, 1, {}),         # tiny list segments: overflow -> unfiltered rerun
+])
+def test_streamed_lut16_path_matches_unfiltered_and_oracle(name, n, nq, sample, cap, over,
+                                                           monkeypatch):
+    """Batches below the tensor-core minimum take the HBM-bound streamed LUT16
+    scan (k_lut16_stream: sample totals -> threshold -> filter) in the filtered
+    stage 1; it must select exactly what the unfiltered PRMT scan selects."""
+    ds, qs, cfg, idx = _scaled(name, n, nq, **over)
+    s = cfg.search
+    kw = dict(overfetch=s["overfetch"], retain=s["retain"],
+              exact_final_rerank=s["exact_final_rerank"])
+    monkeypatch.setenv("HSB200_FUSE_SAMPLE", str(sample))
+    if cap:
+        monkeypatch.setenv("HSB200_FUSE_CAP", str(cap))
+    dev = hs.device_index(idx)
+    dev.set_timing(True)
+    fused = hs.search_batch(idx, qs, s["h"], **kw)
+    assert "lut16_stream" in dev.kernel_times()  # the streamed filtered path ran
+    monkeypatch.setenv("HSB200_NO_FUSE", "1")
+    ref = hs.search_batch(idx, qs, s["h"], **kw)
+    for a, b in zip(fused, ref):
+        assert a.ids.tolist() == b.ids.tolist()
+        assert a.scores.tolist() == b.scores.tolist()
+    for i in range(qs.n):
+        ids, sc, _ = O.search_topk(idx, *O.query_parts(qs, i), s["h"], **kw)
+        assert fused[i].ids.tolist() == ids.tolist()
+        np.testing.assert_allclose(fused[i].scores, sc, rtol=1e-9)
