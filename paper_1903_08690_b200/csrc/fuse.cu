@@ -33,7 +33,7 @@ namespace hs {
 namespace {
 
 constexpr int kFuseThreads = 256;
-constexpr int kMaxSeg = 2 * kNumSMs + 2;  // list segments per query (tensor-core pass: one per CTA; streamed scan: two per SM)
+constexpr int kMaxSeg = 4 * kNumSMs + 2;  // list segments per query (tensor-core pass: one per CTA; streamed scan: a few per SM)
 
 __device__ __forceinline__ double dense_score(double btot, double scl, double off, uint32_t t) {
   return __dadd_rn(__dadd_rn(btot, __dmul_rn(scl, (double)t)), off);

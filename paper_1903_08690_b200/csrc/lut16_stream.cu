@@ -14,7 +14,11 @@
 // points each, pull their codes of a stage into registers (one LDS.64 per
 // row), release the stage, and look the codes up in the query's u8 tables
 // with PRMT (the GPU analogue of the paper's in-register PSHUFB LUT16,
-// PAPER.md:374-397).
+// PAPER.md:374-397).  Three CTAs per SM (4-stage rings, 12 x 16 KB in flight
+// per SM).  Blocks are handed out by ticket: a CTA starts on block blockIdx.x
+// and draws the following ones from a per-query counter (the next ticket is
+// in flight while the current block streams), so SMs that run ahead take
+// more blocks; the last CTA to finish re-arms the counter for the next launch.
 //
 // Accumulation: a PRMT result register holds 4 points' bytes.  `all` adds
 // the registers as plain 32-bit integers (a base-256 sum with carries), `odd`
@@ -41,11 +45,20 @@ constexpr int kRowWords = kSP / 8;    // u32 per subspace row of a block (2 KB)
 constexpr int kSlice = 8;             // subspace rows per ring stage
 constexpr int kStageBytes = kSlice * kRowWords * 4;  // 16 KB
 #ifndef HS_STREAM_STAGES
-#define HS_STREAM_STAGES 6
+#define HS_STREAM_STAGES 4
 #endif
 constexpr int kStages = HS_STREAM_STAGES;
 constexpr int kConsumers = 256;       // 16 points each
-constexpr int kCtasPerSM = 2;
+#ifndef HS_STREAM_CTAS
+#define HS_STREAM_CTAS 3
+#endif
+constexpr int kCtasPerSM = HS_STREAM_CTAS;
+constexpr int kSchedQueries = 4096;   // scheduler slots after the code planes
+
+bool env_flag(const char* name) {
+  const char* e = std::getenv(name);
+  return e && e[0] && e[0] != '0';
+}
 
 struct StreamArgs {
   const uint32_t* vcodes;
@@ -62,6 +75,13 @@ struct StreamArgs {
   uint2* list;
   uint32_t* cnt;
   int64_t cap;
+  // dynamic block scheduling: sched[2q] = next block of query q, sched[2q+1]
+  // = CTAs done (the last one re-arms both for the next launch)
+  uint32_t* sched;
+  // opaque multiplier (1): accumulator adds issue as IMAD on the FMA pipe,
+  // which the lookups leave idle (PRMT, LOP3, SHF and IADD3 all share the
+  // half-rate ALU pipe that bounds this kernel)
+  uint32_t one;
 };
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
@@ -96,6 +116,48 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
+// PRMT, LOP3, SHF and IADD3 all issue on the half-rate ALU pipe, which bounds
+// this kernel (ncu: ALU pipe 85% active, FMA pipe 17%, LSU 14%), so whatever
+// can issue elsewhere does: the accumulator adds are IMADs by an opaque 1 and
+// the << 4 an IMUL by an opaque 16 (FMA pipe; ptxas would turn literal
+// constants back into IADD3 / SHF).
+__device__ __forceinline__ uint32_t add_fma(uint32_t x, uint32_t acc, uint32_t one) {
+  uint32_t r;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(x), "r"(one), "r"(acc));
+  return r;
+}
+__device__ __forceinline__ uint32_t mul_fma(uint32_t x, uint32_t m) {
+  uint32_t r;
+  asm("mul.lo.u32 %0, %1, %2;" : "=r"(r) : "r"(x), "r"(m));
+  return r;
+}
+
+// One subspace row, 8 points (one code word w, nibble j = point j): the two
+// result registers (points 0-3, 4-7; byte = table entry) are added into the
+// base-256 sums all0/all1 and, bytes 1 and 3 only, into the u16 lanes of
+// odd0/odd1.  PRMT picks among 8 pool bytes by the low 3 bits of a selector
+// nibble, so entries 0-7 (T.x, T.y) and 8-15 (T.z, T.w) are both looked up
+// with the selector s = code & 7 and blended by a byte mask of the codes'
+// bit 3 — one more PRMT in sign-replicate mode: the msb of byte j of w is bit
+// 3 of point 2j+1, the msb of byte j of w << 4 that of point 2j.  12 ALU-pipe
+// instructions per 8 codes.
+__device__ __forceinline__ void row8(const uint4& T, uint32_t w, uint32_t one, uint32_t sixteen,
+                                     uint32_t& all0, uint32_t& all1, uint32_t& odd0,
+                                     uint32_t& odd1) {
+  const uint32_t s = w & 0x77777777u;
+  const uint32_t sh = s >> 16;
+  const uint32_t a0 = prmt(T.x, T.y, s), a1 = prmt(T.x, T.y, sh);
+  const uint32_t b0 = prmt(T.z, T.w, s), b1 = prmt(T.z, T.w, sh);
+  const uint32_t w4 = mul_fma(w, sixteen);
+  const uint32_t k0 = prmt(w, w4, 0x9D8Cu), k1 = prmt(w, w4, 0xBFAEu);
+  const uint32_t r0 = (b0 & k0) | (a0 & ~k0);
+  const uint32_t r1 = (b1 & k1) | (a1 & ~k1);
+  all0 = add_fma(r0, all0, one);
+  all1 = add_fma(r1, all1, one);
+  odd0 = add_fma(prmt(r0, 0u, 0x4341u), odd0, one);
+  odd1 = add_fma(prmt(r1, 0u, 0x4341u), odd1, one);
+}
+
 template <int MODE>  // 0 totals, 1 filter
 __global__ void __launch_bounds__(kConsumers + 32, kCtasPerSM) k_lut16_stream(StreamArgs a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -103,18 +165,13 @@ __global__ void __launch_bounds__(kConsumers + 32, kCtasPerSM) k_lut16_stream(St
   uint4* lut = reinterpret_cast<uint4*>(smem_raw + (size_t)kStages * kStageBytes);
   uint64_t* full = reinterpret_cast<uint64_t*>(lut + a.K8);
   uint64_t* empty = full + kStages;
-  uint32_t* s_cnt = reinterpret_cast<uint32_t*>(empty + kStages);
+  int32_t* s_blk = reinterpret_cast<int32_t*>(empty + kStages);  // [kStages] block of the stage
+  uint32_t* s_cnt = reinterpret_cast<uint32_t*>(s_blk + kStages);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t q = blockIdx.y;
   const int seg = blockIdx.x, nseg = gridDim.x;
-  const int64_t b0 = a.nblocks * seg / nseg, b1 = a.nblocks * (seg + 1) / nseg;
 
-  {
-    const uint4* src = reinterpret_cast<const uint4*>(a.luts + q * (int64_t)a.Kp * 16);
-    for (int i = tid; i < a.K8; i += blockDim.x)
-      lut[i] = i < a.K ? src[i] : make_uint4(0u, 0u, 0u, 0u);  // zero tables: rows past K add 0
-  }
   if (tid == 0) {
     for (int i = 0; i < kStages; ++i) {
       mbar_init(&full[i], 1);
@@ -127,17 +184,36 @@ __global__ void __launch_bounds__(kConsumers + 32, kCtasPerSM) k_lut16_stream(St
   __syncthreads();
 
   if (warp == kConsumers / 32) {
-    // ---- producer: one bulk copy per (block, slice of kSlice rows) ----
+    // ---- producer: one bulk copy per (block, slice of kSlice rows); starts
+    // streaming while the consumers stage the query's tables ----
     if (lane == 0) {
-      uint32_t it = 0;
-      for (int64_t b = b0; b < b1; ++b) {
+      uint32_t s = 0, ph = 1;  // stage, parity of its `empty` barrier (first pass: free)
+      const bool dyn = a.sched != nullptr;
+      // first block: the CTA's own index; then tickets nseg, nseg+1, ...
+      int64_t b = seg;
+      while (b < a.nblocks) {
+        // the next block's ticket is in flight while this block streams
+        const int64_t bn = dyn ? (int64_t)atomicAdd(&a.sched[2 * q], 1u) + nseg : b + nseg;
         const uint32_t* blk = a.vcodes + b * (int64_t)a.K * kRowWords;
-        for (int k0 = 0; k0 < a.K; k0 += kSlice, ++it) {
+        for (int k0 = 0; k0 < a.K; k0 += kSlice) {
           const uint32_t bytes = (uint32_t)min(kSlice, a.K - k0) * (kRowWords * 4);
-          const uint32_t s = it % kStages;
-          mbar_wait(&empty[s], ((it / kStages) & 1u) ^ 1u);
+          mbar_wait(&empty[s], ph);
+          s_blk[s] = (int32_t)b;
           mbar_arrive_tx(&full[s], bytes);
           bulk_g2s(ring + (size_t)s * kStageBytes, blk + (int64_t)k0 * kRowWords, bytes, &full[s]);
+          if (++s == kStages) s = 0, ph ^= 1u;
+        }
+        b = bn;
+      }
+      // end marker
+      mbar_wait(&empty[s], ph);
+      s_blk[s] = -1;
+      mbar_arrive(&full[s]);
+      if (dyn) {
+        __threadfence();
+        if (atomicAdd(&a.sched[2 * q + 1], 1u) == (uint32_t)nseg - 1u) {
+          a.sched[2 * q] = 0u;  // every CTA has drawn its last ticket: re-arm
+          a.sched[2 * q + 1] = 0u;
         }
       }
     }
@@ -145,37 +221,43 @@ __global__ void __launch_bounds__(kConsumers + 32, kCtasPerSM) k_lut16_stream(St
   }
 
   // ---- consumers ----
+  {
+    const uint4* src = reinterpret_cast<const uint4*>(a.luts + q * (int64_t)a.Kp * 16);
+    for (int i = tid; i < a.K8; i += kConsumers) {
+      lut[i] = i < a.K ? src[i] : make_uint4(0u, 0u, 0u, 0u);  // rows past K add 0
+    }
+  }
+  asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory");
   const uint32_t tl = MODE == 1 ? a.tlim[q] : 0u;
   uint2* seg_list = MODE == 1 ? a.list + (q * nseg + seg) * a.cap : nullptr;
-  uint32_t it = 0;
-  for (int64_t b = b0; b < b1; ++b) {
+  const uint32_t one = a.one, sixteen = a.one << 4;
+  uint32_t s = 0, ph = 0;  // stage, parity of its `full` barrier
+  for (;;) {
     uint32_t all[4] = {0u, 0u, 0u, 0u}, odd[4] = {0u, 0u, 0u, 0u};
-    for (int k0 = 0; k0 < a.K; k0 += kSlice, ++it) {
-      const int rows = min(kSlice, a.K - k0);
-      const uint32_t s = it % kStages;
-      mbar_wait(&full[s], (it / kStages) & 1u);
+    int64_t b = 0;
+    for (int k0 = 0; k0 < a.K; k0 += kSlice) {
+      mbar_wait(&full[s], ph);
+      if (k0 == 0) {
+        b = s_blk[s];
+        if (b < 0) break;
+      }
+      // every stage is read as kSlice rows: rows past K hold stale codes and
+      // look up all-zero tables
       const uint2* src = reinterpret_cast<const uint2*>(ring + (size_t)s * kStageBytes) + tid;
       uint2 w[kSlice];
 #pragma unroll
-      for (int r = 0; r < kSlice; ++r)
-        w[r] = r < rows ? src[r * (kRowWords / 2)] : make_uint2(0u, 0u);
+      for (int r = 0; r < kSlice; ++r) w[r] = src[r * (kRowWords / 2)];
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);  // codes are in registers: release the stage
 #pragma unroll
-      for (int r = 0; r < kSlice; r += 2) {
-        const uint4 T0 = lut[k0 + r], T1 = lut[k0 + r + 1];
-        uint32_t ra[4], rb[4];
-        lut8(T0, w[r].x, ra[0], ra[1]);
-        lut8(T0, w[r].y, ra[2], ra[3]);
-        lut8(T1, w[r + 1].x, rb[0], rb[1]);
-        lut8(T1, w[r + 1].y, rb[2], rb[3]);
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          all[i] += ra[i] + rb[i];
-          odd[i] += prmt(ra[i], 0u, 0x4341u) + prmt(rb[i], 0u, 0x4341u);  // bytes 1, 3
-        }
+      for (int r = 0; r < kSlice; ++r) {
+        const uint4 T = lut[k0 + r];
+        row8(T, w[r].x, one, sixteen, all[0], all[1], odd[0], odd[1]);
+        row8(T, w[r].y, one, sixteen, all[2], all[3], odd[2], odd[3]);
       }
+      if (++s == kStages) s = 0, ph ^= 1u;
     }
+    if (b < 0) break;
     // totals of this thread's 16 points: point 4i+j = S_j of register i
     uint32_t t[16];
 #pragma unroll
@@ -211,12 +293,17 @@ __global__ void __launch_bounds__(kConsumers + 32, kCtasPerSM) k_lut16_stream(St
       uint32_t mx = t[0];
 #pragma unroll
       for (int j = 1; j < 16; ++j) mx = max(mx, t[j]);
-      if (mx >= tl) {  // rare: ~k1 * n / sample passes per query in all
+      if (mx >= tl) {  // ~k1 * n / sample passes per query in all
+        const int lim = (int)min((int64_t)16, a.n - p0);  // < 16 in the last block only
+        uint32_t pm = 0u;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) pm |= (t[j] >= tl && j < lim) ? (1u << j) : 0u;
+        uint32_t pos = atomicAdd(s_cnt, (uint32_t)__popc(pm));  // one shared atomic per thread
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
-          if (t[j] >= tl && p0 + j < a.n) {
-            const uint32_t pos = atomicAdd(s_cnt, 1u);
+          if ((pm >> j) & 1u) {
             if (pos < (uint32_t)a.cap) seg_list[pos] = make_uint2((uint32_t)(p0 + j), t[j]);
+            ++pos;
           }
         }
       }
@@ -248,7 +335,8 @@ __global__ void k_to_vertical(const uint8_t* __restrict__ packed, int64_t n, int
 }
 
 size_t stream_smem(int K8) {
-  return (size_t)kStages * kStageBytes + (size_t)K8 * 16 + sizeof(uint64_t) * 2 * kStages + 16;
+  return (size_t)kStages * kStageBytes + (size_t)K8 * 16 + sizeof(uint64_t) * 2 * kStages +
+         sizeof(int32_t) * kStages + 16;
 }
 
 int launch_stream(const DeviceIndex& ix, int mode, StreamArgs& a, int64_t nq, int64_t nseg,
@@ -261,6 +349,11 @@ int launch_stream(const DeviceIndex& ix, int mode, StreamArgs& a, int64_t nq, in
   a.Kp = ix.Kp;
   a.nblocks = ceil_div(a.n, kSP);
   const size_t smem = stream_smem(a.K8);
+  a.one = 1u;
+  a.sched = env_flag("HSB200_STREAM_STATIC")
+                ? nullptr
+                : ix.vcodes + ceil_div(ix.n, kSP) * (int64_t)ix.K * kRowWords;
+  if (nq > kSchedQueries) a.sched = nullptr;
   auto kern = mode == 0 ? k_lut16_stream<0> : k_lut16_stream<1>;
   HS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   dim3 grid((unsigned)nseg, (unsigned)nq);
@@ -271,13 +364,18 @@ int launch_stream(const DeviceIndex& ix, int mode, StreamArgs& a, int64_t nq, in
 
 }  // namespace
 
-int64_t vertical_words(int64_t n, int K) { return ceil_div(n, kSP) * (int64_t)K * kRowWords; }
+// the code planes, then the scheduler words of k_lut16_stream (zeroed here,
+// re-armed by every launch)
+int64_t vertical_words(int64_t n, int K) {
+  return ceil_div(n, kSP) * (int64_t)K * kRowWords + 2 * kSchedQueries;
+}
 
 void launch_to_vertical(const uint8_t* packed, int64_t n, int K, uint32_t* v, cudaStream_t st) {
   if (K <= 0 || n <= 0) return;
   const int64_t nblocks = ceil_div(n, kSP);
   dim3 grid((unsigned)ceil_div(nblocks * kRowWords, 256), (unsigned)K);
   k_to_vertical<<<grid, 256, 0, st>>>(packed, n, K, nblocks, v);
+  cudaMemsetAsync(v + nblocks * (int64_t)K * kRowWords, 0, sizeof(uint32_t) * 2 * kSchedQueries, st);
 }
 
 bool lut16_stream_supported(const DeviceIndex& ix) {

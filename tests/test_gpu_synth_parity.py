@@ -248,3 +248,27 @@ def test_streamed_lut16_path_matches_unfiltered_and_oracle(name, n, nq, sample, 
         ids, sc, _ = O.search_topk(idx, *O.query_parts(qs, i), s["h"], **kw)
         assert fused[i].ids.tolist() == ids.tolist()
         np.testing.assert_allclose(fused[i].scores, sc, rtol=1e-9)
+
+
+@pytest.mark.parametrize("static", ["0", "1"])
+def test_streamed_lut16_block_scheduling(static, monkeypatch):
+    """k_lut16_stream hands out code blocks by ticket (HSB200_STREAM_STATIC=1:
+    a fixed stride); the assignment must not change results, launch after
+    launch (the ticket counter re-arms itself at the end of every launch)."""
+    ds, qs, cfg, idx = _scaled("cfg2", 70_000, 6)
+    s = cfg.search
+    kw = dict(overfetch=s["overfetch"], retain=s["retain"],
+              exact_final_rerank=s["exact_final_rerank"])
+    monkeypatch.setenv("HSB200_FUSE_SAMPLE", "4096")
+    dev = hs.device_index(idx)
+    dev.set_timing(True)
+    monkeypatch.setenv("HSB200_NO_FUSE", "1")
+    base = hs.search_batch(idx, qs, s["h"], **kw)
+    monkeypatch.delenv("HSB200_NO_FUSE")
+    monkeypatch.setenv("HSB200_STREAM_STATIC", static)
+    for _ in range(3):
+        got = hs.search_batch(idx, qs, s["h"], **kw)
+        assert "lut16_stream" in dev.kernel_times()
+        for a, b in zip(got, base):
+            assert a.ids.tolist() == b.ids.tolist()
+            assert a.scores.tolist() == b.scores.tolist()
