@@ -47,7 +47,7 @@ constexpr int kOfferRound = kThreads * kOfferPer;  // worst-case offers per inse
 #define MINB0 4
 #endif
 #ifndef KB0
-#define KB0 4
+#define KB0 3
 #endif
 constexpr int kSmallPostings = 512;        // below this a chunk's postings skip the barriers
 constexpr int kRingBytes = 24 * 1024;  // posting ring (bulk-copy staging), default size
@@ -908,10 +908,12 @@ __global__ void __launch_bounds__(WS ? kThreads + 32 : kThreads, DM == 0 ? MINB0
         uint2 nxt[kPre];
         {
           const uint32_t b = s.abase[0], c = s.acnt[0];
+          const uint2* p0 = a.post + b + tid;
 #pragma unroll
           for (int r = 0; r < kPre; ++r) {
-            const uint32_t j = tid + r * kThreads;
-            nxt[r] = j < c ? __ldg(&a.post[b + j]) : make_uint2(0xFFFFFFFFu, 0u);
+            if (r > 0 && (uint32_t)(r * kThreads) >= c) break;  // block-uniform
+            nxt[r] = (uint32_t)(tid + r * kThreads) < c ? __ldg(p0 + r * kThreads)
+                                                         : make_uint2(0xFFFFFFFFu, 0u);
           }
         }
         for (int i = 0; i < nact; ++i) {
@@ -922,45 +924,62 @@ __global__ void __launch_bounds__(WS ? kThreads + 32 : kThreads, DM == 0 ? MINB0
           for (int r = 0; r < kPre; ++r) cur[r] = nxt[r];
           if (i + 1 < nact) {
             const uint32_t b2 = s.abase[i + 1], c2 = s.acnt[i + 1];
+            const uint2* p2 = a.post + b2 + tid;
 #pragma unroll
             for (int r = 0; r < kPre; ++r) {
-              const uint32_t j = tid + r * kThreads;
-              nxt[r] = j < c2 ? __ldg(&a.post[b2 + j]) : make_uint2(0xFFFFFFFFu, 0u);
+              if (r > 0 && (uint32_t)(r * kThreads) >= c2) break;  // block-uniform
+              nxt[r] = (uint32_t)(tid + r * kThreads) < c2 ? __ldg(p2 + r * kThreads)
+                                                            : make_uint2(0xFFFFFFFFu, 0u);
             }
           }
 #pragma unroll
           for (int r = 0; r < kPre; ++r) {
+            if (r > 0 && (uint32_t)(r * kThreads) >= c) break;  // block-uniform
             if (cur[r].x == 0xFFFFFFFFu) continue;
             HS_DCHECK(cur[r].x >= cb && cur[r].x < ce);
             // f64(q) * f64(w) is exact, so contraction cannot change the sum
             s.acc[aix<DM>(cur[r].x - (uint32_t)cb)] += qv * (double)__uint_as_float(cur[r].y);
           }
-          // long slices: the rest in batches of kB loads per thread, the next
-          // batch in flight while this one adds
+          // long slices: whole batches of kB x kThreads postings with plain
+          // (unpredicated, immediate-offset) loads, two register sets
+          // alternating so the next batch is in flight while this one adds;
+          // then one predicated batch for the remainder
           constexpr int kB = DM == 0 ? KB0 : 4;  // (register budget of the dense variants)
+          constexpr uint32_t kBatch = kB * kThreads;
           if (c > (uint32_t)(kPre * kThreads)) {
-            uint2 v[kB];
+            const uint32_t rest = c - kPre * kThreads;
+            const uint32_t nfull = rest / kBatch;
+            const uint2* ptr = a.post + b + kPre * kThreads + tid;
+            auto load4 = [&](uint2* v, const uint2* p) {
 #pragma unroll
-            for (int r = 0; r < kB; ++r) {
-              const uint32_t j = kPre * kThreads + tid + r * kThreads;
-              v[r] = j < c ? __ldg(&a.post[b + j]) : make_uint2(0xFFFFFFFFu, 0u);
+              for (int r = 0; r < kB; ++r) v[r] = __ldg(p + r * kThreads);
+            };
+            auto add4 = [&](const uint2* v) {
+#pragma unroll
+              for (int r = 0; r < kB; ++r)
+                s.acc[aix<DM>(v[r].x - (uint32_t)cb)] += qv * (double)__uint_as_float(v[r].y);
+            };
+            uint2 v0[kB], v1[kB];
+            if (nfull > 0) load4(v0, ptr);
+            for (uint32_t k = 0; k < nfull; k += 2) {
+              if (k + 1 < nfull) load4(v1, ptr + kBatch);
+              add4(v0);
+              if (k + 2 < nfull) load4(v0, ptr + 2 * kBatch);
+              if (k + 1 < nfull) add4(v1);
+              ptr += 2 * kBatch;
             }
-            for (uint32_t j0 = kPre * kThreads; j0 < c; j0 += kB * kThreads) {
-              uint2 w[kB];
+            const uint32_t done = kPre * kThreads + nfull * kBatch;
+            if (done < c) {
+              const uint2* tp = a.post + b + done + tid;
 #pragma unroll
-              for (int r = 0; r < kB; ++r) w[r] = v[r];
-              if (j0 + kB * kThreads < c) {
-#pragma unroll
-                for (int r = 0; r < kB; ++r) {
-                  const uint32_t j = j0 + kB * kThreads + tid + r * kThreads;
-                  v[r] = j < c ? __ldg(&a.post[b + j]) : make_uint2(0xFFFFFFFFu, 0u);
-                }
-              }
+              for (int r = 0; r < kB; ++r)
+                v0[r] = done + tid + r * kThreads < c ? __ldg(tp + r * kThreads)
+                                                      : make_uint2(0xFFFFFFFFu, 0u);
 #pragma unroll
               for (int r = 0; r < kB; ++r) {
-                if (w[r].x == 0xFFFFFFFFu) continue;
-                HS_DCHECK(w[r].x >= cb && w[r].x < ce);
-                s.acc[aix<DM>(w[r].x - (uint32_t)cb)] += qv * (double)__uint_as_float(w[r].y);
+                if (v0[r].x == 0xFFFFFFFFu) continue;
+                HS_DCHECK(v0[r].x >= cb && v0[r].x < ce);
+                s.acc[aix<DM>(v0[r].x - (uint32_t)cb)] += qv * (double)__uint_as_float(v0[r].y);
               }
             }
           }
