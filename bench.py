@@ -402,8 +402,43 @@ def replica_parity(args, device, s, want_cpu):
                       f"GPU-built, downloaded for the oracle)",
            "queries": int(qs.n), "id_mismatch": int(mism), "max_rel_err": worst,
            "build": bp, "seconds": round(time.time() - t0, 1)}
+    # operating points on the replica: the reference defaults
+    # (top_t = 128) and the unpruned scan index (top_t = None), recall@10 of
+    # the GPU results against GPU exact truth
+    kw = dict(overfetch=s["overfetch"], retain=s["retain"],
+              exact_final_rerank=s["exact_final_rerank"])
+    t_ids, _ = exact_truth(gidx.handle, qs, 10)
+
+    def _recall(rr):
+        return float(np.mean([len(np.intersect1d(r.ids[:10], t_ids[i])) / 10
+                              for i, r in enumerate(rr)]))
+
+    ops = {f"top_t={icfg.top_t}": {"recall_at_10": _recall(res)}}
+    try:
+        b2 = dd.build(cfg.index_config(top_t=None))
+        g2 = b2.finish()
+        res2 = hs.search_batch(g2, qs, s["h"], **kw)
+        t0u = time.perf_counter()
+        hs.search_batch(g2, qs, s["h"], **kw)
+        ops["top_t=None"] = {"recall_at_10": _recall(res2),
+                             "gpu_qps_replica": qs.n / (time.perf_counter() - t0u)}
+        t0u = time.perf_counter()
+        hs.search_batch(gidx, qs, s["h"], **kw)
+        ops[f"top_t={icfg.top_t}"]["gpu_qps_replica"] = qs.n / (time.perf_counter() - t0u)
+        g2.handle.close()
+        del b2, g2
+    except Exception as e:  # noqa: BLE001
+        ops["top_t=None"] = {"error": repr(e)}
+    out["operating_points"] = ops
     cpu = None
     if want_cpu:
+        # single-thread figure (BASELINE.md §3 asks for threads=1 beside all cores)
+        n1 = min(qs.n, 24)
+        t0u = time.perf_counter()
+        from oracle import hybrid_oracle as O1
+
+        O1.search_batch(host, _sub(qs, 0, n1), s["h"], threads=1, **kw)
+        dt1 = time.perf_counter() - t0u
         per_q = dt / qs.n
         scale = cfg.data.n / law.n
         est = per_q * (f1 * scale + (1.0 - f1))
@@ -413,7 +448,9 @@ def replica_parity(args, device, s, want_cpu):
                          f"extrapolated to N={cfg.data.n}: the share that scales with N "
                          f"(stage-1 scan + select, {f1:.3f}, measured single-thread) x"
                          f"{scale:.0f}, the rest (LUT build, stages 2-3) constant",
-               "replica_qps_measured": qs.n / dt}
+               "replica_qps_measured": qs.n / dt,
+               "replica_qps_threads1": n1 / dt1,
+               "value_threads1": 1.0 / ((dt1 / n1) * (f1 * scale + (1.0 - f1)))}
         cpu.update(_cpu_info())
     gidx.handle.close()
     return out, cpu
@@ -845,6 +882,9 @@ def main():
                                       torch.stack(gs).cpu().numpy(), 10)
     rec = [len(np.intersect1d(res_ids[i, :10], t_ids[i])) / 10 for i in range(truth_q)]
     recall = float(np.mean(rec))
+    # true top-10 found anywhere in the returned top-h (cfg3's "10@100")
+    recall_10_at_h = float(np.mean([len(np.intersect1d(res_ids[i], t_ids[i])) / 10
+                                    for i in range(truth_q)]))
 
     # ---- full-scale sampled checks (exact scores of the returned rows) ----
     full_check = None
@@ -870,9 +910,19 @@ def main():
                                                 / np.maximum(np.abs(osc), 1e-300))))
         parity = {"queries": int(sample), "id_mismatch": int(mism), "max_rel_err": worst,
                   "against": "oracle/hybrid_oracle.py on the same index and queries"}
+        # single-thread figure beside the all-cores one
+        from oracle import hybrid_oracle as O1
+
+        n1 = max(1, min(sample, 4 if big else 12))
+        t0u = time.perf_counter()
+        O1.search_batch(idx, _sub(qs, 0, n1), h, threads=1, overfetch=s["overfetch"],
+                        retain=s["retain"], exact_final_rerank=s["exact_final_rerank"])
+        dt1 = time.perf_counter() - t0u
         cpu = {"value": sample / dt, "unit": "queries/s", "cores": threads, "kind": "port",
                "sample": f"first {sample} of {nq} {args.workload} queries, oracle "
-                         f"search_batch(threads={threads}), {dt:.1f} s", **_cpu_info()}
+                         f"search_batch(threads={threads}), {dt:.1f} s",
+               "value_threads1": n1 / dt1, "threads1_sample": f"first {n1} queries, {dt1:.1f} s",
+               **_cpu_info()}
     if parity is not None and full_check is not None:
         parity["full_scale"] = full_check
     if parity is not None and rank == 0:
@@ -900,6 +950,16 @@ def main():
                 "note": "u8 ops of the one-hot x LUT product (2*N*Q*16*K per step); the "
                         "kernel writes only threshold-passing candidates, so its HBM "
                         "traffic is the code stream, not the N*Q score matrix"}
+        # second denominator: the tcgen05 kind::i8 issue rate at the SM clock this
+        # run held (16384 u8 ops per SM per clock: one M=128, N=256, K=32 MMA per
+        # 128 cycles; tools/mma_bench2.cu measures exactly that floor) — cuBLAS
+        # bf16, the MEASURED_PEAKS figure behind `peak`, runs power-capped at a
+        # lower clock, so this one is the stricter of the two
+        mhz = (clk.summary() or {}).get("sm_mhz")
+        if mhz:
+            ipk = 148 * 16384 * float(mhz) * 1e6 / 1e12
+            roof["issue_peak"] = ipk
+            roof["frac_of_issue_peak"] = achieved / ipk
     elif s1_ms:
         alg_bytes = 8 * (postings or 0) + (nq * n_local * npairs if K else 0)
         peak, peak_kind = _peaks()
@@ -936,7 +996,8 @@ def main():
         spec = _workload_spec(args.workload)
         conf = _config_dict(args.workload, spec, w.n_total, nq)
         conf.update({
-            "note": cfg.note, "recall_at_10": recall, "truth_queries": truth_q,
+            "note": cfg.note, "recall_at_10": recall, "recall_10_at_h": recall_10_at_h,
+            "truth_queries": truth_q,
             "l2": "flushed (256 MiB write) before every step, untimed",
             "parallelism": f"id-range shards x{world}" if world > 1 else "single GPU",
             "data_gen": "on-GPU generator (devbuild.cu)" if w.gpu_built else "host generator",

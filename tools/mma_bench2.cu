@@ -2,7 +2,10 @@
 // tcgen05.mma kind::i8 with A from TMEM, single CTA (M=128) vs CTA pair
 // (cta_group::2, M=256), for the N values the LUT16 tensor-core kernel uses.
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o mma_bench2 tools/mma_bench2.cu
-// Prints cycles per MMA (operands resident, contents irrelevant).
+// Prints cycles per MMA (operands resident, contents irrelevant) and, timed
+// with CUDA events over all 148 SMs, the u8 op rate that issue cadence amounts
+// to (one JSON line per configuration): the tensor-pipe ceiling bench.py's
+// `roofline.issue_peak` restates analytically.
 #include <cstdint>
 #include <cstdio>
 
@@ -138,6 +141,21 @@ int main() {
     cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
     printf("cta_group::2 M=256 N=%3d acc=%d: %7.1f cycles/MMA (floor %5.1f) %s\n", c.N, c.nacc,
            (double)h / iters, 256.0 * c.N / 512.0, cudaGetErrorString(e));
+    // whole-chip rate: a longer launch between two events
+    const int long_iters = 1 << 18;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaLaunchKernelEx(&cfg, k_bench<true>, long_iters, c.N, c.nacc, d);  // warm
+    cudaEventRecord(e0);
+    cudaLaunchKernelEx(&cfg, k_bench<true>, long_iters, c.N, c.nacc, d);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    const double ops = 74.0 * long_iters * 2.0 * 256.0 * c.N * 32.0;
+    printf("{\"kind\": \"tcgen05.mma.cta_group::2.kind::i8\", \"M\": 256, \"N\": %d, \"acc_buffers\": %d, "
+           "\"ms\": %.3f, \"u8_tops\": %.1f}\n", c.N, c.nacc, ms, ops / (ms * 1e-3) / 1e12);
   }
   return 0;
 }
