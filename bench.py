@@ -149,7 +149,7 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
-        sm, mx, reasons = [], [], set()
+        sm, mx, pw, reasons = [], [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for ln in self.lines:
             f = [x.strip() for x in ln.split(",")]
@@ -160,12 +160,18 @@ class ClockSampler:
                 mx.append(float(f[2]))
             except ValueError:
                 continue
+            try:
+                pw.append(float(f[3]))
+            except ValueError:
+                pass
             for nm, v in zip(names, f[5:9]):
                 if v.lower() == "active":
                     reasons.add(nm)
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
         return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(mx)),
+                "sm_mhz_min": float(min(sm)), "power_w_median": float(np.median(pw)) if pw else None,
+                "power_w_max": float(max(pw)) if pw else None,
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
@@ -415,7 +421,9 @@ def replica_parity(args, device, s, want_cpu):
 
     ops = {f"top_t={icfg.top_t}": {"recall_at_10": _recall(res)}}
     try:
-        b2 = dd.build(cfg.index_config(top_t=None))
+        # (finish() moved the first builder's arrays into its index: generate again)
+        dd2 = hs.DeviceDataset.generate(law, seed=0, device=device)
+        b2 = dd2.build(cfg.index_config(top_t=None))
         g2 = b2.finish()
         res2 = hs.search_batch(g2, qs, s["h"], **kw)
         t0u = time.perf_counter()
@@ -426,7 +434,7 @@ def replica_parity(args, device, s, want_cpu):
         hs.search_batch(gidx, qs, s["h"], **kw)
         ops[f"top_t={icfg.top_t}"]["gpu_qps_replica"] = qs.n / (time.perf_counter() - t0u)
         g2.handle.close()
-        del b2, g2
+        del b2, g2, dd2
     except Exception as e:  # noqa: BLE001
         ops["top_t=None"] = {"error": repr(e)}
     out["operating_points"] = ops
@@ -1007,6 +1015,10 @@ def main():
             "gen_s": round(w.t_gen, 1), "build_s": round(w.t_build, 1),
             "build_phases_s": {k: round(v, 2) for k, v in w.build_timing.items()},
             "index_bytes_rank0": int(dev_index.memory_bytes()),
+            "index_postings_rank0": int(getattr(idx, "nnz_post", 0) or
+                                        (len(idx.sparse_index.ids)
+                                         if getattr(idx, "sparse_index", None) is not None
+                                         and hasattr(idx.sparse_index, "ids") else 0)),
         })
         line = {
             "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world,
