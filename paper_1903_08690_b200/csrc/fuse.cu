@@ -24,6 +24,7 @@
 //   5. the variable-length selection keeps the exact top-k1.
 // A query whose candidate list overflowed, or whose postings were not
 // bucketed, is flagged and rerun through the unfiltered stage 1.
+#include <algorithm>
 #include <cstdlib>
 
 #include "kernels.cuh"
@@ -72,17 +73,91 @@ __global__ void k_tlim(const Cand* __restrict__ cand_s, int64_t nq, int k,
 // lb == 0 (non-negative products: acc >= +0 exactly, and fl(acc + d) >= d)
 // T = dense(t_k) exactly; otherwise it is lowered by a relative guard that
 // covers the f64 rounding of the sums.
-constexpr int kTlThreads = 256;
-__global__ void __launch_bounds__(kTlThreads) k_sample_tlim(
-    const uint16_t* __restrict__ tot_s, int64_t ld, int64_t m, int k,
+//
+// The k points sit in the top ~k/m of the sample (0.05% at config 5), so the
+// two full passes skip almost every value: a first selection over a strided
+// sub-sample of ~64 K values gives L = its k-th largest total, a lower bound
+// of t_k (the sub-sample is part of the sample), and the full passes only
+// histogram totals >= L (a few percent) — they run at load speed instead of
+// one shared-memory atomic per value.
+constexpr int kTlThreads = 512;
+constexpr int kTlWarps = kTlThreads / 32;
+constexpr int kTlUnroll = 6;          // 16-byte groups in flight per thread
+
+struct TlSel {
+  uint32_t bin, rem;
+};
+
+// MODE 0: bin = v >> 8 for v >= lo;  MODE 1: bin = v & 255 for v >> 8 == hi8 and v >= lo.
+// Groups g*gstride (g = 0, 1, ...) of 8 totals each; returns the highest bin where the
+// count from the top reaches `rem`, and what is left to find inside it.
+template <int MODE>
+__device__ TlSel tl_pass(const uint16_t* __restrict__ t, int64_t m, int64_t gstride, uint32_t lo,
+                         uint32_t hi8, uint32_t rem, uint32_t (*hist)[256], uint32_t* s_sum,
+                         uint32_t* s_out) {
+  const int tid = threadIdx.x, warp = tid >> 5;
+  for (int i = tid; i < kTlWarps * 256; i += kTlThreads) (&hist[0][0])[i] = 0u;
+  __syncthreads();
+  const int64_t ngroups = (m + 7) / 8;
+  const int64_t nsel = (ngroups + gstride - 1) / gstride;  // groups visited
+  for (int64_t j0 = tid; j0 < nsel; j0 += (int64_t)kTlThreads * kTlUnroll) {
+    uint4 v4[kTlUnroll];
+#pragma unroll
+    for (int u = 0; u < kTlUnroll; ++u) {
+      const int64_t j = j0 + (int64_t)u * kTlThreads;
+      v4[u] = j < nsel ? __ldg(reinterpret_cast<const uint4*>(t + j * gstride * 8))
+                       : make_uint4(0u, 0u, 0u, 0u);
+    }
+#pragma unroll
+    for (int u = 0; u < kTlUnroll; ++u) {
+      const int64_t j = j0 + (int64_t)u * kTlThreads;
+      if (j >= nsel) break;
+      const int64_t p = j * gstride * 8;
+      const uint32_t w[4] = {v4[u].x, v4[u].y, v4[u].z, v4[u].w};
+#pragma unroll
+      for (int h = 0; h < 8; ++h) {
+        const uint32_t v = (w[h >> 1] >> (16 * (h & 1))) & 0xFFFFu;
+        if (v < lo || p + h >= m) continue;
+        if (MODE == 0) atomicAdd(&hist[warp][v >> 8], 1u);
+        else if ((v >> 8) == hi8) atomicAdd(&hist[warp][v & 0xFFu], 1u);
+      }
+    }
+  }
+  __syncthreads();
+  if (tid < 256) {
+    uint32_t c = 0;
+#pragma unroll
+    for (int w = 0; w < kTlWarps; ++w) c += hist[w][tid];
+    s_sum[tid] = c;
+  }
+  __syncthreads();
+  if (tid == 0) {  // highest bin where the running count from the top reaches rem
+    uint32_t run = 0;
+    int b = 255;
+    for (; b > 0; --b) {
+      if (run + s_sum[b] >= rem) break;
+      run += s_sum[b];
+    }
+    s_out[0] = (uint32_t)b;
+    s_out[1] = rem - run;
+  }
+  __syncthreads();
+  TlSel r;
+  r.bin = s_out[0];
+  r.rem = s_out[1];
+  __syncthreads();
+  return r;
+}
+
+__global__ void __launch_bounds__(kTlThreads, 2) k_sample_tlim(
+    const uint16_t* __restrict__ tot_s, int64_t ld, int64_t m, int k, int64_t sub_groups,
     const int64_t* __restrict__ qptr, const double* __restrict__ qv, double wmin, double wmax,
     const double* __restrict__ btot, const double* __restrict__ scl,
     const double* __restrict__ off, uint32_t* __restrict__ tlim, double* __restrict__ Tout) {
-  __shared__ uint32_t hist[kTlThreads / 32][256];
+  __shared__ uint32_t hist[kTlWarps][256];
   __shared__ uint32_t s_sum[256];
-  __shared__ double s_lb[kTlThreads / 32];
-  __shared__ int s_sel;
-  __shared__ uint32_t s_rem;
+  __shared__ double s_lb[kTlWarps];
+  __shared__ uint32_t s_out[2];
   const int64_t q = blockIdx.x;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint16_t* t = tot_s + q * ld;
@@ -97,52 +172,30 @@ __global__ void __launch_bounds__(kTlThreads) k_sample_tlim(
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) lb += __shfl_xor_sync(0xffffffffu, lb, o);
   if (lane == 0) s_lb[warp] = lb;
-  uint32_t prefix = 0, rem = (uint32_t)k;
-  bool none = m < k;  // fewer sample points than k: every total passes
-  for (int pass = 0; pass < 2 && !none; ++pass) {
-    for (int i = tid; i < (kTlThreads / 32) * 256; i += kTlThreads) (&hist[0][0])[i] = 0u;
-    __syncthreads();
-    for (int64_t p = (int64_t)tid * 8; p < m; p += (int64_t)kTlThreads * 8) {
-      const uint4 v4 = *reinterpret_cast<const uint4*>(t + p);
-      const uint32_t w[4] = {v4.x, v4.y, v4.z, v4.w};
-#pragma unroll
-      for (int h = 0; h < 8; ++h) {
-        if (p + h >= m) break;
-        const uint32_t v = (w[h >> 1] >> (16 * (h & 1))) & 0xFFFFu;
-        if (pass == 0) atomicAdd(&hist[warp][v >> 8], 1u);
-        else if ((v >> 8) == prefix) atomicAdd(&hist[warp][v & 0xFFu], 1u);
-      }
+  const bool none = m < k;  // fewer sample points than k: every total passes
+  uint32_t tk = 0;
+  if (!none) {
+    // lower bound L of t_k from a strided sub-sample holding at least k totals
+    uint32_t L = 0;
+    const int64_t ngroups = (m + 7) / 8;
+    const int64_t gstride = ngroups / sub_groups;
+    if (gstride >= 2 && (ngroups / gstride) * 8 - 8 >= (int64_t)k) {
+      // (every visited group but possibly the last is whole: >= k totals)
+      const TlSel a0 = tl_pass<0>(t, m, gstride, 0u, 0u, (uint32_t)k, hist, s_sum, s_out);
+      const TlSel a1 = tl_pass<1>(t, m, gstride, 0u, a0.bin, a0.rem, hist, s_sum, s_out);
+      L = (a0.bin << 8) | a1.bin;
     }
-    __syncthreads();
-    {
-      uint32_t c = 0;
-#pragma unroll
-      for (int w = 0; w < kTlThreads / 32; ++w) c += hist[w][tid];
-      s_sum[tid] = c;
-    }
-    __syncthreads();
-    if (tid == 0) {  // highest bin where the running count from the top reaches rem
-      uint32_t run = 0;
-      int b = 255;
-      for (; b > 0; --b) {
-        if (run + s_sum[b] >= rem) break;
-        run += s_sum[b];
-      }
-      s_sel = b;
-      s_rem = rem - run;
-    }
-    __syncthreads();
-    prefix = pass == 0 ? (uint32_t)s_sel : (prefix << 8) | (uint32_t)s_sel;
-    rem = s_rem;
-    __syncthreads();
+    const TlSel b0 = tl_pass<0>(t, m, 1, L, 0u, (uint32_t)k, hist, s_sum, s_out);
+    const TlSel b1 = tl_pass<1>(t, m, 1, L, b0.bin, b0.rem, hist, s_sum, s_out);
+    tk = (b0.bin << 8) | b1.bin;
   }
   if (tid == 0) {
     double l = 0.0;
-    for (int w = 0; w < kTlThreads / 32; ++w) l += s_lb[w];
+    for (int w = 0; w < kTlWarps; ++w) l += s_lb[w];
     const double b = btot[q], s = scl[q], o = off ? off[q] : 0.0;
     double T = -INFINITY;
     if (!none) {
-      const double dk = dense_score(b, s, o, prefix);
+      const double dk = dense_score(b, s, o, tk);
       T = l == 0.0 ? dk : (dk + l * (1.0 + 1e-6)) - 1e-9 * fabs(dk);
     }
     tlim[q] = tlim_of(T, b, s, o);
@@ -343,8 +396,12 @@ void launch_sample_tlim(const uint16_t* tot_s, int64_t ld, int64_t m, int64_t nq
                         const double* btot, const double* scl, const double* off,
                         uint32_t* tlim, double* T, cudaStream_t st) {
   if (nq <= 0) return;
-  k_sample_tlim<<<(unsigned)nq, kTlThreads, 0, st>>>(tot_s, ld, m, k, qptr, qv, wmin, wmax, btot,
-                                                     scl, off, tlim, T);
+  // sub-sample of the first selection, in 8-value groups (HSB200_TLIM_SUBGROUPS: test knob that
+  // lets small samples take the two-level path)
+  const char* e = std::getenv("HSB200_TLIM_SUBGROUPS");
+  const int64_t sub_groups = e ? std::max<int64_t>(1, std::atoll(e)) : 8192;
+  k_sample_tlim<<<(unsigned)nq, kTlThreads, 0, st>>>(tot_s, ld, m, k, sub_groups, qptr, qv, wmin,
+                                                     wmax, btot, scl, off, tlim, T);
 }
 
 int launch_fuse_cands(const DeviceIndex& ix, int64_t nq, const uint8_t* luts, const double* btot,

@@ -76,7 +76,10 @@ constexpr int kProd = HS_TC_WARP_ARRIVE ? 4 : 128;  // arrivals per A chunk (4 p
 #define HS_TC_NPAR 3
 #endif
 constexpr int kNPar = HS_TC_NPAR;  // producer warps per TMEM lane quadrant (round-robin over chunks)
-constexpr int kEpiPar = 2;     // epilogue warps per lane quadrant (alternate 32-column tiles)
+#ifndef HS_TC_EPIPAR
+#define HS_TC_EPIPAR 2
+#endif
+constexpr int kEpiPar = HS_TC_EPIPAR;  // epilogue warps per lane quadrant (alternate 32-column tiles)
 constexpr int kProdWarps = 4 * kNPar;
 constexpr int kEpiWarp0 = kProdWarps;      // a multiple of 4: warp & 3 = lane quadrant
 constexpr int kMmaWarp = kEpiWarp0 + 4 * kEpiPar;

@@ -272,3 +272,29 @@ def test_streamed_lut16_block_scheduling(static, monkeypatch):
         for a, b in zip(got, base):
             assert a.ids.tolist() == b.ids.tolist()
             assert a.scores.tolist() == b.scores.tolist()
+
+
+@pytest.mark.parametrize("name,n,nq,sub", [("cfg2", 70_000, 70, 64), ("cfg3", 80_000, 5, 32),
+                                           ("cfg2", 70_000, 3, 100000)])
+def test_sample_threshold_two_level_selection(name, n, nq, sub, monkeypatch):
+    """k_sample_tlim finds the k1-th largest sample total with a first selection
+    over a strided sub-sample (a lower bound) and two full passes that only
+    histogram totals at or above it.  HSB200_TLIM_SUBGROUPS shrinks the
+    sub-sample so the small test samples take that path (the last case: a
+    sub-sample larger than the sample, i.e. the direct path); results must
+    equal the unfiltered stage 1 for tensor-core and streamed batches."""
+    ds, qs, cfg, idx = _scaled(name, n, nq)
+    s = cfg.search
+    kw = dict(overfetch=s["overfetch"], retain=s["retain"],
+              exact_final_rerank=s["exact_final_rerank"])
+    monkeypatch.setenv("HSB200_FUSE_SAMPLE", "8192")
+    monkeypatch.setenv("HSB200_TLIM_SUBGROUPS", str(sub))
+    dev = hs.device_index(idx)
+    dev.set_timing(True)
+    fused = hs.search_batch(idx, qs, s["h"], **kw)
+    assert "fuse" in dev.kernel_times()
+    monkeypatch.setenv("HSB200_NO_FUSE", "1")
+    ref = hs.search_batch(idx, qs, s["h"], **kw)
+    for a, b in zip(fused, ref):
+        assert a.ids.tolist() == b.ids.tolist()
+        assert a.scores.tolist() == b.scores.tolist()
