@@ -179,7 +179,7 @@ __global__ void __launch_bounds__(kTlThreads, 2) k_sample_tlim(
     uint32_t L = 0;
     const int64_t ngroups = (m + 7) / 8;
     const int64_t gstride = ngroups / sub_groups;
-    if (gstride >= 2 && (ngroups / gstride) * 8 - 8 >= (int64_t)k) {
+    if (gstride >= 4 && (ngroups / gstride) * 8 - 8 >= (int64_t)k) {
       // (every visited group but possibly the last is whole: >= k totals)
       const TlSel a0 = tl_pass<0>(t, m, gstride, 0u, 0u, (uint32_t)k, hist, s_sum, s_out);
       const TlSel a1 = tl_pass<1>(t, m, gstride, 0u, a0.bin, a0.rem, hist, s_sum, s_out);

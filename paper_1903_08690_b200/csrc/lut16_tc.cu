@@ -64,6 +64,13 @@
 #ifndef HS_TC_PREGEN
 #define HS_TC_PREGEN 1       // producers generate a chunk's one-hot before waiting for its slot
 #endif
+#ifndef HS_TC_ASYNC
+#define HS_TC_ASYNC 1        // pair: the peer's producers signal the leader's `afull` with st.async
+                             // (transaction bytes, non-blocking) instead of forwarded remote arrives
+#endif
+#ifndef HS_TC_ROLLED
+#define HS_TC_ROLLED 1       // producers' chunk loop rolled (one copy of the chunk code)
+#endif
 
 namespace hs {
 
@@ -85,11 +92,17 @@ constexpr int kEpiWarp0 = kProdWarps;      // a multiple of 4: warp & 3 = lane q
 constexpr int kMmaWarp = kEpiWarp0 + 4 * kEpiPar;
 constexpr int kEpi = (HS_TC_WARP_ARRIVE ? 4 : 128) * kEpiPar;  // dempty arrivals per block
 constexpr int kThreadsTc = 32 * (kMmaWarp + 1);  // 12 producer, 8 epilogue, 1 MMA warps
-// pair mode: + forwarding warps.  A cluster-scope remote mbarrier arrive
-// blocks the issuing warp for ~1000 cycles (measured, HS_TCPROF); the peer's
-// producers therefore arrive locally and kFwd warps relay completed A slots
-// to the leader (slot s by warp s % kFwd), so those latencies overlap.
-constexpr int kFwd = HS_TC_FWD ? 4 : 0;
+// pair mode: the leader's `afull` / `dempty` barriers also count the peer
+// CTA's producers / epilogue.  A cluster-scope remote mbarrier arrive blocks
+// the issuing warp for ~1000 cycles (measured, HS_TCPROF), and relaying
+// through forwarding warps (HS_TC_ASYNC=0: kFwd warps, slot s by warp
+// s % kFwd) still left the relay latency in every slot's turnaround.  The
+// peer therefore signals with st.async (HS_TC_ASYNC=1): a 4-byte asynchronous
+// store into the leader's shared memory that completes 4 transaction bytes on
+// the leader's barrier — non-blocking — while the leader's own warp of the
+// same lane quadrant arrives with expect_tx(4).  cfg5-law filter pass 26.1 ->
+// 22.4 ms per 1920 queries x 10^7 points.
+constexpr int kFwd = (HS_TC_FWD && !HS_TC_ASYNC) ? 4 : 0;
 constexpr int kFwdWarp0 = kMmaWarp + 1;
 constexpr int kThreadsPair = 32 * (kFwdWarp0 + kFwd);
 static_assert(kEpiWarp0 % 4 == 0, "epilogue warps must start on a lane-quadrant boundary");
@@ -257,6 +270,23 @@ __device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
                : "memory");
 }
+// one arrival that also expects `bytes` of asynchronous-store transactions
+__device__ __forceinline__ void mbar_arrive_expect(uint64_t* bar, uint32_t bytes) {
+  asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n\t}" ::"r"(
+                   smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+// 4-byte asynchronous store into another CTA's shared memory that completes 4
+// transaction bytes on that CTA's mbarrier: a non-blocking remote signal (a
+// remote mbarrier.arrive.release.cluster stalls the issuing warp ~1000 cycles)
+__device__ __forceinline__ void st_async_signal(uint32_t cluster_dst, uint32_t cluster_bar) {
+  asm volatile(
+      "st.async.weak.shared::cluster.mbarrier::complete_tx::bytes.u32 [%0], %1, [%2];" ::"r"(
+          cluster_dst),
+      "r"(1u), "r"(cluster_bar)
+      : "memory");
+}
 
 // leader CTA only: D[256 x N] (+)= A[256 x 32 B] (TMEM, 128 rows per CTA) * B (smem,
 // N/2 columns per CTA)
@@ -406,6 +436,7 @@ __global__ void __launch_bounds__(PAIR ? kThreadsPair : kThreadsTc, 1)
   uint64_t* dfull = aempty + a.slots;  // [2]     MMA commit -> epilogue
   uint64_t* dempty = dfull + 2;        // [2]     epilogue -> MMA (count 128)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dempty + 2);
+  uint32_t* sink = tmem_slot + 4;  // [slots][4] + [2][kEpi] landing words of the peer's st.async signals
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t cta_item = PAIR ? (int64_t)(blockIdx.x >> 1) : (int64_t)blockIdx.x;
@@ -434,12 +465,12 @@ __global__ void __launch_bounds__(PAIR ? kThreadsPair : kThreadsTc, 1)
     for (int s = 0; s < a.slots; ++s) {
       // pair: the leader's afull counts its own producer warps plus either
       // the peer's (remote arrives) or the peer's forwarding warp (one)
-      mbar_init(&afull[s], PAIR && rank == 0 ? kProd + (HS_TC_FWD ? 1 : kProd) : kProd);
+      mbar_init(&afull[s], PAIR && rank == 0 && !HS_TC_ASYNC ? kProd + (HS_TC_FWD ? 1 : kProd) : kProd);
       mbar_init(&aempty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&dfull[b], 1);
-      mbar_init(&dempty[b], PAIR ? 2 * kEpi : kEpi);
+      mbar_init(&dempty[b], PAIR && !HS_TC_ASYNC ? 2 * kEpi : kEpi);
     }
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
@@ -450,6 +481,7 @@ __global__ void __launch_bounds__(PAIR ? kThreadsPair : kThreadsTc, 1)
   // where this CTA's producers / epilogue arrive: the leader's barriers
   const uint32_t afull_r = PAIR ? peer_addr(afull, 0) : 0u;
   const uint32_t dempty_r = PAIR ? peer_addr(dempty, 0) : 0u;
+  const uint32_t sink_r = PAIR ? peer_addr(sink, 0) : 0u;
   const bool remote = PAIR && rank != 0;
   const uint32_t tmem = *tmem_slot;
   const uint32_t tmem_a = tmem + 2u * (uint32_t)NQ;  // A ring after the two accumulators
@@ -577,6 +609,71 @@ __global__ void __launch_bounds__(PAIR ? kThreadsPair : kThreadsTc, 1)
         // (blocks so far) * nkc + c, slot = g mod slots, round = g / slots —
         // advanced incrementally over this warp's own chunks only
         const int64_t g0 = (blk_it + bi) * (int64_t)nkc;
+        if constexpr (NW == 1 && HS_TC_PREGEN && HS_TC_ROLLED) {
+          // This warp's own chunks c = par, par + kNPar, ... in a ROLLED loop:
+          // one copy of the chunk code.  (Unrolled over the 16 chunks of a
+          // block the producers' code ran to ~40 KB, each warp walking a
+          // different third of it — ncu showed as many instruction-fetch
+          // stalls as issued instructions.)  The chunk's code word is always
+          // cur[0]; the remaining words shift down.
+#pragma unroll 1
+          for (int c = par; c < nkc; c += kNPar) {
+            const uint32_t w = cur[0];
+#pragma unroll
+            for (int i = 0; i + 1 < OW; ++i) cur[i] = cur[i + 1];
+            const int64_t gch = g0 + c;
+            pslot += (int)(gch - pg);
+            pg = gch;
+            while (pslot >= a.slots) {
+              pslot -= a.slots;
+              ++pround;
+            }
+            const int slot = pslot;
+            const uint32_t round = pround;
+            uint32_t r[32];
+            {
+              TC_T0();
+              if (live && (c + 1) * kKC <= a.K) onehot8_full(w, r);
+              else onehot8(w, live ? min(kKC, a.K - c * kKC) : 0, r);
+#ifdef HS_TCPROF
+              uint32_t acc = 0;
+#pragma unroll
+              for (int i = 0; i < 32; ++i) acc ^= r[i];
+              if (acc == 0x12345678u) tw3 += 1;
+#endif
+              TC_ACC(tw3);
+            }
+            if (round > 0) {
+              TC_T0();
+              mbar_wait_sleep(&aempty[slot], (round - 1) & 1u, HS_TC_SLEEP_PROD);
+              TC_ACC(tw0);
+              asm volatile("tcgen05.fence::after_thread_sync;");
+            }
+            {
+              TC_T0();
+              if (!(a.exp & 2)) TMEM_ST32(tmem_a + lane_base + (uint32_t)(slot * SC), r);
+              if (!(a.exp & 2)) asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+              TC_ACC(tw1);
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;");
+            __syncwarp();  // the warp's stores are complete (wait::st is warp-wide): one arrive
+            {
+              TC_T0();
+              if (!HS_TC_WARP_ARRIVE || lane == 0) {
+                if (PAIR && HS_TC_ASYNC) {
+                  if (remote)
+                    st_async_signal(sink_r + 4u * (uint32_t)(slot * 4 + quad),
+                                    afull_r + 8u * (uint32_t)slot);
+                  else
+                    mbar_arrive_expect(&afull[slot], 4u);  // + the peer quadrant's 4 bytes
+                } else if (remote && !HS_TC_FWD) mbar_arrive_remote(afull_r + 8u * (uint32_t)slot);
+                else mbar_arrive(&afull[slot]);
+              }
+              __syncwarp();
+              TC_ACC(tw2);
+            }
+          }
+        } else {
 #pragma unroll
         for (int c = 0; c < NCH; ++c) {
           if (c >= nkc) break;
@@ -646,7 +743,13 @@ __global__ void __launch_bounds__(PAIR ? kThreadsPair : kThreadsTc, 1)
             {
               TC_T0();
               if (!HS_TC_WARP_ARRIVE || lane == 0) {
-                if (remote && !HS_TC_FWD) mbar_arrive_remote(afull_r + 8u * (uint32_t)slot);
+                if (PAIR && HS_TC_ASYNC) {
+                  if (remote)
+                    st_async_signal(sink_r + 4u * (uint32_t)(slot * 4 + quad),
+                                    afull_r + 8u * (uint32_t)slot);
+                  else
+                    mbar_arrive_expect(&afull[slot], 4u);  // + the peer quadrant's 4 bytes
+                } else if (remote && !HS_TC_FWD) mbar_arrive_remote(afull_r + 8u * (uint32_t)slot);
                 else mbar_arrive(&afull[slot]);
               }
               __syncwarp();
@@ -654,6 +757,7 @@ __global__ void __launch_bounds__(PAIR ? kThreadsPair : kThreadsTc, 1)
             }
           }
         }
+        }  // unrolled form (wide slots / no pre-generation)
       }
     } else if (warp < kMmaWarp) {
       // ---- epilogue: accumulator -> u16 totals [query][point] ----
@@ -677,7 +781,13 @@ __global__ void __launch_bounds__(PAIR ? kThreadsPair : kThreadsTc, 1)
           asm volatile("tcgen05.fence::before_thread_sync;");
           __syncwarp();
           if (!HS_TC_WARP_ARRIVE || lane == 0) {
-            if (remote) mbar_arrive_remote(dempty_r + 8u * (uint32_t)buf);
+            if (PAIR && HS_TC_ASYNC) {
+              if (remote)
+                st_async_signal(sink_r + 4u * (uint32_t)(4 * a.slots + buf * kEpi + (warp - kEpiWarp0)),
+                                dempty_r + 8u * (uint32_t)buf);
+              else
+                mbar_arrive_expect(&dempty[buf], 4u);  // + the peer warp's 4 bytes
+            } else if (remote) mbar_arrive_remote(dempty_r + 8u * (uint32_t)buf);
             else mbar_arrive(&dempty[buf]);
           }
         }
@@ -699,7 +809,13 @@ __global__ void __launch_bounds__(PAIR ? kThreadsPair : kThreadsTc, 1)
                 asm volatile("tcgen05.fence::before_thread_sync;");
                 __syncwarp();  // wait::ld is warp-wide: one arrive per warp
                 if (!HS_TC_WARP_ARRIVE || lane == 0) {
-                  if (remote) mbar_arrive_remote(dempty_r + 8u * (uint32_t)buf);
+                  if (PAIR && HS_TC_ASYNC) {
+                    if (remote)
+                      st_async_signal(sink_r + 4u * (uint32_t)(4 * a.slots + buf * kEpi + (warp - kEpiWarp0)),
+                                      dempty_r + 8u * (uint32_t)buf);
+                    else
+                      mbar_arrive_expect(&dempty[buf], 4u);  // + the peer warp's 4 bytes
+                  } else if (remote) mbar_arrive_remote(dempty_r + 8u * (uint32_t)buf);
                   else mbar_arrive(&dempty[buf]);
                 }
               }
@@ -750,7 +866,13 @@ __global__ void __launch_bounds__(PAIR ? kThreadsPair : kThreadsTc, 1)
             asm volatile("tcgen05.fence::before_thread_sync;");
             __syncwarp();  // wait::ld is warp-wide: one arrive per warp
             if (!HS_TC_WARP_ARRIVE || lane == 0) {
-              if (remote) mbar_arrive_remote(dempty_r + 8u * (uint32_t)buf);
+              if (PAIR && HS_TC_ASYNC) {
+                if (remote)
+                  st_async_signal(sink_r + 4u * (uint32_t)(4 * a.slots + buf * kEpi + (warp - kEpiWarp0)),
+                                  dempty_r + 8u * (uint32_t)buf);
+                else
+                  mbar_arrive_expect(&dempty[buf], 4u);  // + the peer warp's 4 bytes
+              } else if (remote) mbar_arrive_remote(dempty_r + 8u * (uint32_t)buf);
               else mbar_arrive(&dempty[buf]);
             }
           }
@@ -772,10 +894,11 @@ __global__ void __launch_bounds__(PAIR ? kThreadsPair : kThreadsTc, 1)
       }
     } else if (warp >= kFwdWarp0) {
       // ---- pair forwarders (peer only): relay this CTA's completed A slots ----
+      if constexpr (kFwd > 0)
       if (PAIR && rank != 0)
         for (int64_t bi = 0; bi < nblk; ++bi)
           for (int c = 0; c < nkc; ++c) {
-            if (slot % kFwd == warp - kFwdWarp0) {
+            if (slot % (kFwd > 0 ? kFwd : 1) == warp - kFwdWarp0) {
               mbar_wait(&afull[slot], round & 1u);
               if (lane == 0) mbar_arrive_remote(afull_r + 8u * (uint32_t)slot);
               __syncwarp();
@@ -1038,7 +1161,7 @@ int launch_tc(const DeviceIndex& ix, const uint8_t* luts, int64_t nq, int64_t n_
   const int NQL = L.pair ? NQ / 2 : NQ;
   const size_t smem =
       (size_t)a.Kp * NQL * 16 + kStageBytes + 2 * kMaxNQ * sizeof(uint32_t) +
-      (2 * a.slots + 4) * sizeof(uint64_t) + 16;
+      (2 * a.slots + 4) * sizeof(uint64_t) + 16 + 16 * (size_t)a.slots + 4 * 2 * kEpi;
   void (*kern)(TcArgs, const CUtensorMap);
   if (L.pair) {
     if (filter)
