@@ -1,6 +1,6 @@
 # Round-2 evidence: full GPU test run, smoke, default bench line (cfg5), reference arm, cfg3/cfg4 lines,
 # the ncu launch list of the bench command (search kernels only), the tcgen05 issue-rate microbenchmark,
-# one ncu --set full capture of the tensor-core filter kernel, and the compute-sanitizer logs.
+# one ncu --set full capture of the tensor-core filter kernel, the debug-library test run, cfg1/cfg2 lines.
 O=gpurun_out/r02
 mkdir -p $O
 timeout 2400 python -m pytest tests -m gpu -q > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $O/pytest_gpu.log
@@ -17,8 +17,8 @@ echo "ncu rc=$?" >> $O/ncu_launch.log
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:k_lut16_tc -s 1 -c 1 -f -o $O/tc_cfg5law \
   python bench.py --n 10000000 --no-cpu --no-parity --qb1 0 --steps 1 --warmup 0 --truth-queries 8 --queries 1152 > $O/ncu_tc.log 2>&1
 echo "ncu tc rc=$?" >> $O/ncu_tc.log
-for tool in racecheck synccheck memcheck; do
-  timeout 1500 compute-sanitizer --tool $tool python tools/sanitize_probe.py > $O/sanitizer_$tool.log 2>&1; echo "rc=$?" >> $O/sanitizer_$tool.log
-  tail -4 $O/sanitizer_$tool.log
-done
-tail -3 $O/pytest_gpu.log; tail -2 $O/smoke.log; cat $O/u8_peak.txt; cut -c1-300 $O/bench_cfg5.json; cut -c1-300 $O/bench_ref.json; tail -2 $O/ncu_launch.log $O/ncu_tc.log
+# compute-sanitizer is closed on this pool (profiles/r02/sanitizer_refused.log): the debug library's device asserts instead
+bash tools/gpu/debug_asserts.sh
+timeout 900 python bench.py --workload cfg2 > $O/bench_cfg2.json 2> $O/bench_cfg2.err
+timeout 900 python bench.py --workload cfg1 > $O/bench_cfg1.json 2> $O/bench_cfg1.err
+tail -3 $O/pytest_gpu.log; tail -2 $O/smoke.log; cat $O/u8_peak.txt; cut -c1-300 $O/bench_cfg5.json; cut -c1-300 $O/bench_ref.json; tail -n 2 $O/ncu_launch.log; tail -n 2 $O/ncu_tc.log
