@@ -60,6 +60,7 @@ __global__ void __launch_bounds__(kRsThreads) k_select_radix(const Cand* __restr
   Cand* buf = reinterpret_cast<Cand*>(smem_raw);  // [P] selected entries
   __shared__ unsigned hist[256];
   __shared__ int ctl[16];
+  __shared__ unsigned long long red[2 * (kRsThreads / 32)];
   const int64_t q = blockIdx.x;
   if (qmask && qmask[q] == 0) return;
   const int tid = threadIdx.x, warp = tid >> 5;
@@ -73,7 +74,52 @@ __global__ void __launch_bounds__(kRsThreads) k_select_radix(const Cand* __restr
   if (m > k) {
     int need = k;
     whole = false;
-    for (int shift = 56; shift >= 0; shift -= 8) {
+    // The keys of one query's candidates share their leading bytes (sign,
+    // exponent, often the top of the mantissa): a digit pass over such a byte
+    // puts every candidate into one bin — m atomics on one shared-memory word
+    // — and selects nothing.  One min/max reduction finds the first byte where
+    // the keys differ; the passes start there.
+    int shift0 = 56;
+    {
+      unsigned long long kmin = ~0ull, kmax = 0ull;
+      for (int64_t i = tid; i < m; i += blockDim.x) {
+        const unsigned long long key = score_key(src[i].s);
+        kmin = key < kmin ? key : kmin;
+        kmax = key > kmax ? key : kmax;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long a = __shfl_xor_sync(0xffffffffu, kmin, o);
+        const unsigned long long b = __shfl_xor_sync(0xffffffffu, kmax, o);
+        kmin = a < kmin ? a : kmin;
+        kmax = b > kmax ? b : kmax;
+      }
+      if ((tid & 31) == 0) {
+        red[2 * warp] = kmin;
+        red[2 * warp + 1] = kmax;
+      }
+      __syncthreads();
+      kmin = red[0];
+      kmax = red[1];
+      for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+        kmin = red[2 * w] < kmin ? red[2 * w] : kmin;
+        kmax = red[2 * w + 1] > kmax ? red[2 * w + 1] : kmax;
+      }
+      __syncthreads();
+      const unsigned long long diff = kmin ^ kmax;
+      if (diff == 0ull) {  // every key equal: only the tie ids select
+        prefix = kmax;
+        pmask = ~0ull;
+        shift0 = -8;
+      } else {
+        shift0 = ((63 - __clzll((long long)diff)) >> 3) << 3;  // first differing byte
+        if (shift0 < 56) {
+          pmask = ~0ull << (shift0 + 8);
+          prefix = kmax & pmask;
+        }
+      }
+    }
+    for (int shift = shift0; shift >= 0; shift -= 8) {
       for (int i = tid; i < 256; i += blockDim.x) hist[i] = 0;
       __syncthreads();
       for (int64_t i = tid; i < m; i += blockDim.x) {

@@ -116,6 +116,19 @@ def test_select_topk_known_answers_and_ties():
     s = rng.integers(0, 50, size=20000).astype(np.float64)
     assert hs.select_topk(s, 5000).tolist() == O.select_topk(s, 5000).tolist()
     assert hs.select_topk(s, 300).tolist() == O.select_topk(s, 300).tolist()
+    # keys that share their leading bytes (the radix select starts at the first
+    # differing byte), all-equal keys (tie ids only), signs and infinities mixed
+    for n, k in [(5000, 100), (70000, 1000), (3000, 2999)]:
+        t = rng.permutation(n)
+        near = 1.0 + rng.random(n) * 1e-9
+        near[rng.integers(0, n, size=n // 10)] = near[0]          # exact ties at many levels
+        assert hs.select_topk(near, k, tie_ids=t).tolist() == O.select_topk(near, k, t).tolist()
+        same = np.full(n, -0.375)
+        assert hs.select_topk(same, k, tie_ids=t).tolist() == O.select_topk(same, k, t).tolist()
+        mixed = rng.standard_normal(n) * 1e-3
+        mixed[::7] = -np.inf
+        mixed[3::11] = 0.0
+        assert hs.select_topk(mixed, k, tie_ids=t).tolist() == O.select_topk(mixed, k, t).tolist()
 
 
 def test_sparse_scan_bit_exact():
