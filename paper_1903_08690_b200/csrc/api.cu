@@ -7,6 +7,7 @@
 //   select (merge tiles to the top k1) -> stage2 -> stage3 -> outputs,
 // all enqueued on the index's stream with no host round trip between stages.
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
@@ -238,7 +239,16 @@ int run_search(DeviceIndex& ix, const hs_query_batch& qb, int64_t nnz, int max_q
   // sample ~ k1*n/E points (=> ~E expected dense candidates per query); E
   // grows with k1 so that the sample stays a few percent of a large index
   // (10^8 points, k1 = 1000: a 2M-point sample instead of 17M)
-  const double e_cand = std::max(6000.0, 50.0 * (double)sz.k1);
+  // ... scaled by sqrt(n / 10^8): the sample pass costs ~ n/E and the candidate
+  // scoring + selection ~ E per query, so the best E grows like sqrt(n) (at
+  // 10^8 points E = 50 k1 balances the two; an id-range shard of 1/8 of them
+  // wants ~18 k1)
+  // (HSB200_FUSE_ECAND: candidates per k1 at 10^8 points, a tuning knob)
+  static const double e_mult = std::getenv("HSB200_FUSE_ECAND")
+                                   ? std::max(1.0, std::atof(std::getenv("HSB200_FUSE_ECAND")))
+                                   : 50.0;
+  const double e_cand = std::max(
+      6000.0, e_mult * (double)sz.k1 * std::min(1.0, std::sqrt((double)ix.n / 1.0e8)));
   const int64_t m_auto = std::max<int64_t>(
       65536, (int64_t)((double)sz.k1 * (double)ix.n / e_cand));
   // (a whole number of stage-1 chunks, so the sample ends on a chunk boundary)

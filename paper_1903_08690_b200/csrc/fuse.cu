@@ -114,6 +114,13 @@ __device__ TlSel tl_pass(const uint16_t* __restrict__ t, int64_t m, int64_t gstr
       if (j >= nsel) break;
       const int64_t p = j * gstride * 8;
       const uint32_t w[4] = {v4[u].x, v4[u].y, v4[u].z, v4[u].w};
+      // group reject: the high half of a word is >= lo iff the word is >= lo << 16,
+      // the low half iff the word shifted up is (two compares per pair of totals)
+      const uint32_t ll = lo << 16;
+      bool any = false;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) any |= (w[i] >= ll) | ((w[i] << 16) >= ll);
+      if (!any) continue;
 #pragma unroll
       for (int h = 0; h < 8; ++h) {
         const uint32_t v = (w[h >> 1] >> (16 * (h & 1))) & 0xFFFFu;
