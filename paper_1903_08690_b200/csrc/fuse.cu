@@ -33,7 +33,10 @@ namespace hs {
 
 namespace {
 
-constexpr int kFuseThreads = 256;
+#ifndef HS_FUSE_THREADS
+#define HS_FUSE_THREADS 256
+#endif
+constexpr int kFuseThreads = HS_FUSE_THREADS;
 constexpr int kMaxSeg = 4 * kNumSMs + 2;  // list segments per query (tensor-core pass: one per CTA; streamed scan: a few per SM)
 
 __device__ __forceinline__ double dense_score(double btot, double scl, double off, uint32_t t) {

@@ -366,7 +366,7 @@ struct TcArgs {
   int64_t cap;
   int nseg;                // segment stride (>= grid size)
   int exp;                 // dev profiling knobs (HSB200_TC_EXP: 1 epilogue drain only, 2 no TMEM
-                           // stores, 8 no MMAs, 16 unused; build with -DHS_TCPROF for per-warp wait cycles), results invalid when set
+                           // stores, 8 no MMAs, 16 unused, 32 no code loads, 64 no pass appends; build with -DHS_TCPROF for per-warp wait cycles), results invalid when set
   uint32_t tmax;           // 255*K + 1: no total reaches it
   int64_t ngroups;
   int64_t nblocks;         // point blocks of 128
@@ -820,7 +820,7 @@ __global__ void __launch_bounds__(PAIR ? kThreadsPair : kThreadsTc, 1)
                 }
               }
               if (a.exp & 1) continue;  // profiling knob: drain only
-              uint32_t orr = 0u;
+              uint32_t og[4];  // per group of 4 columns: OR of the s_j
               const uint4* nt4 = reinterpret_cast<const uint4*>(sNt + c16);
 #pragma unroll
               for (int g = 0; g < 4; ++g) {
@@ -829,31 +829,28 @@ __global__ void __launch_bounds__(PAIR ? kThreadsPair : kThreadsTc, 1)
                 r[4 * g + 1] += t4.y;
                 r[4 * g + 2] += t4.z;
                 r[4 * g + 3] += t4.w;
-                orr |= (r[4 * g + 0] | r[4 * g + 1]) | (r[4 * g + 2] | r[4 * g + 3]);
+                og[g] = (r[4 * g + 0] | r[4 * g + 1]) | (r[4 * g + 2] | r[4 * g + 3]);
               }
-              if ((orr & 0x10000u) != 0u && p < a.n) {  // rare: this lane's passes
-                // totals into the lane's 64-byte row of the warp's staging
-                // area (16-byte chunks XOR-swizzled by lane), read back by
-                // column — no register-select chain
-                uint32_t* row = reinterpret_cast<uint32_t*>(stg) + lane * 16;
+              const uint32_t orr = (og[0] | og[1]) | (og[2] | og[3]);
+              if ((orr & 0x10000u) != 0u && p < a.n && !(a.exp & 64)) {  // rare: this lane's passes
+                // (a warp enters when any of its 32 lanes has a pass in these 16
+                // columns — a quarter of the time at config 5 — so the path is
+                // short: group ORs narrow the search to 4 columns, every
+                // register index is static, the total is s_j minus the staged
+                // 65536 - t_q)
+                const int64_t lstride = (int64_t)a.nseg * a.cap;  // list entries per query
+                uint2* lq = a.list + ((q0 + c16) * a.nseg + seg_id) * a.cap;
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                  const uint4 t4 = nt4[k];
-                  *reinterpret_cast<uint4*>(row + ((k ^ (lane & 3)) * 4)) =
-                      make_uint4(r[4 * k] - t4.x, r[4 * k + 1] - t4.y, r[4 * k + 2] - t4.z,
-                                 r[4 * k + 3] - t4.w);
-                }
-                uint32_t pm = 0u;
+                for (int g = 0; g < 4; ++g) {
+                  if (!(og[g] & 0x10000u)) continue;
 #pragma unroll
-                for (int j = 0; j < 16; ++j) pm |= (r[j] >> (16 - j)) & (1u << j);
-                while (pm) {
-                  const int j = __ffs(pm) - 1;
-                  pm &= pm - 1;
-                  const int64_t q = q0 + c16 + j;
-                  const uint32_t val = row[(((j >> 2) ^ (lane & 3)) * 4) + (j & 3)];
-                  const uint32_t pos = atomicAdd(sCnt + c16 + j, 1u);  // this CTA's segment of q
-                  if (pos < (uint32_t)a.cap)
-                    a.list[(q * a.nseg + seg_id) * a.cap + pos] = make_uint2((uint32_t)p, val);
+                  for (int i = 0; i < 4; ++i) {
+                    const int j = 4 * g + i;
+                    if (!(r[j] & 0x10000u)) continue;
+                    const uint32_t val = r[j] - sNt[c16 + j];
+                    const uint32_t pos = atomicAdd(sCnt + c16 + j, 1u);  // this CTA's segment of q
+                    if (pos < (uint32_t)a.cap) lq[j * lstride + pos] = make_uint2((uint32_t)p, val);
+                  }
                 }
               }
             }
