@@ -877,6 +877,7 @@ def main():
             ktimes[k] = ktimes.get(k, 0.0) + v / 2
     qb1 = None
     qb1_kernel = None
+    qb1_kt = {}
     t1_all = []
     if world == 1 and args.qb1 > 0:
         t1 = []
@@ -894,6 +895,7 @@ def main():
                 # filtered stage 1, or the fused k_stage1 where that does not apply
                 t1.append(kt.get("lut16_stream", kt.get("stage1", 0.0)))
                 t1_all.append(sum(kt.values()))
+                qb1_kt = dict(kt)
                 qb1_kernel = "k_lut16_stream" if "lut16_stream" in kt else "k_stage1"
         qb1 = float(np.mean(t1)) if t1 else None
     dev_index.set_timing(False)
@@ -1016,6 +1018,7 @@ def main():
         roof["qb1"] = {"scan_ms": qb1, "kernel": qb1_kernel, "alg_bytes": per_query_bytes,
                        "achieved_gbs": a1, "peak_gbs": peak, "frac": a1 / peak,
                        "query_ms_all_kernels": float(np.mean(t1_all)) if t1_all else None,
+                       "query_kernels_ms": {k: round(v, 4) for k, v in qb1_kt.items()},
                        "note": ("single-query path: one query per launch, L2 flushed before "
                                 "each launch; scan_ms = the code-stream kernel alone "
                                 "(k_lut16_stream filter pass: TMA-staged nibble codes, PRMT "
