@@ -287,7 +287,20 @@ int run_search(DeviceIndex& ix, const hs_query_batch& qb, int64_t nnz, int max_q
         ? (double)Cf * nseg * 8 + (double)Mf * 16 + (double)ld_s * 2 +
               (sparse_part ? words * 4.0 : 0.0)
         : 2.0 * (double)tc_ld;  // u16 totals [QB][tc_ld]
-    const int64_t cap = std::max<int64_t>(grp, (int64_t)(8.0e9 / per_q) / grp * grp);
+    // arena budget for the per-chunk stage-1 buffers: half of what the device
+    // has free (counting the arena already held), between 2 and 16 GB — larger
+    // chunks give the per-query kernels (one CTA per query) more CTAs per
+    // launch: cfg5 1236 -> 1197 ms per step from 8 to 16 GB, flat beyond
+    // (HSB200_SCRATCH_GB overrides)
+    double budget = 8.0e9;
+    if (const char* eb = std::getenv("HSB200_SCRATCH_GB")) {
+      budget = std::max(0.5, std::atof(eb)) * 1e9;
+    } else {
+      size_t free_b = 0, total_b = 0;
+      if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess)
+        budget = std::min(16.0e9, std::max(2.0e9, 0.5 * ((double)free_b + (double)ix.scratch_bytes)));
+    }
+    const int64_t cap = std::max<int64_t>(grp, (int64_t)(budget / per_q) / grp * grp);
     if (QB > cap) QB = cap;
   }
   if (use_fuse) {  // layout of the final chunk size (segments depend on it)
