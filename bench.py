@@ -427,10 +427,29 @@ def replica_parity(args, device, s, want_cpu):
         if len(osc):
             worst = max(worst, float(np.max(np.abs(r.scores - osc) / np.maximum(np.abs(osc),
                                                                                1e-300))))
+    # stage-1 scores of every point (whitening on): the one place where the GPU
+    # does not reproduce a BLAS call bit for bit (the ddot of the whitening
+    # offset, pipeline.py:223) — report how far that goes
+    s1 = None
+    try:
+        from oracle import hybrid_oracle as O2
+
+        nq1 = min(8, qs.n)
+        g1 = hs.stage1_scores(gidx, _sub(qs, 0, nq1))
+        worst1, neq = 0.0, 0
+        for i in range(nq1):
+            o1 = O2.stage1_scores(host, *O2.query_parts(qs, i))
+            neq += int(np.count_nonzero(g1[i] != o1))
+            worst1 = max(worst1, float(np.max(np.abs(g1[i] - o1) / np.maximum(np.abs(o1), 1e-300))))
+        s1 = {"queries": nq1, "points": int(law.n), "scores_not_bit_equal": neq,
+              "max_rel_err": worst1}
+        del g1
+    except Exception as e:  # noqa: BLE001
+        s1 = {"error": repr(e)}
     out = {"replica": f"cfg5 law at N={law.n}, d_sparse={law.d_sparse} (GPU-generated, "
                       f"GPU-built, downloaded for the oracle)",
            "queries": int(qs.n), "id_mismatch": int(mism), "max_rel_err": worst,
-           "build": bp, "seconds": round(time.time() - t0, 1)}
+           "build": bp, "stage1_scores": s1, "seconds": round(time.time() - t0, 1)}
     # operating points on the replica: the reference defaults
     # (top_t = 128) and the unpruned scan index (top_t = None), recall@10 of
     # the GPU results against GPU exact truth

@@ -77,12 +77,15 @@ __global__ void k_tlim(const Cand* __restrict__ cand_s, int64_t nq, int k,
 // T = dense(t_k) exactly; otherwise it is lowered by a relative guard that
 // covers the f64 rounding of the sums.
 //
-// The k points sit in the top ~k/m of the sample (0.05% at config 5), so the
-// two full passes skip almost every value: a first selection over a strided
+// The k points sit in the top ~k/m of the sample (0.05% at config 5), so a
+// full pass can skip almost every value: a first selection over a strided
 // sub-sample of ~64 K values gives L = its k-th largest total, a lower bound
-// of t_k (the sub-sample is part of the sample), and the full passes only
-// histogram totals >= L (a few percent) — they run at load speed instead of
-// one shared-memory atomic per value.
+// of t_k (the sub-sample is part of the sample); ONE full pass then builds a
+// direct histogram of (total - L) for the totals >= L (a few percent, within
+// a narrow range: 4096 bins, the last open-ended) and t_k is read off it.
+// It runs at load speed instead of one shared-memory atomic per value.  When
+// the sub-sample is too small, or t_k lands in the open bin, two 8-bit radix
+// passes over the totals >= L decide.
 constexpr int kTlThreads = 512;
 constexpr int kTlWarps = kTlThreads / 32;
 constexpr int kTlUnroll = 6;          // 16-byte groups in flight per thread
@@ -161,13 +164,16 @@ __device__ TlSel tl_pass(const uint16_t* __restrict__ t, int64_t m, int64_t gstr
 
 __global__ void __launch_bounds__(kTlThreads, 2) k_sample_tlim(
     const uint16_t* __restrict__ tot_s, int64_t ld, int64_t m, int k, int64_t sub_groups,
+    uint32_t direct_bins,
     const int64_t* __restrict__ qptr, const double* __restrict__ qv, double wmin, double wmax,
     const double* __restrict__ btot, const double* __restrict__ scl,
     const double* __restrict__ off, uint32_t* __restrict__ tlim, double* __restrict__ Tout) {
   __shared__ uint32_t hist[kTlWarps][256];
   __shared__ uint32_t s_sum[256];
+  __shared__ uint32_t s_part[kTlThreads];
   __shared__ double s_lb[kTlWarps];
   __shared__ uint32_t s_out[2];
+  static_assert(kTlWarps * 256 >= 4096 && kTlThreads * 8 == 4096, "direct histogram layout");
   const int64_t q = blockIdx.x;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint16_t* t = tot_s + q * ld;
@@ -195,9 +201,76 @@ __global__ void __launch_bounds__(kTlThreads, 2) k_sample_tlim(
       const TlSel a1 = tl_pass<1>(t, m, gstride, 0u, a0.bin, a0.rem, hist, s_sum, s_out);
       L = (a0.bin << 8) | a1.bin;
     }
-    const TlSel b0 = tl_pass<0>(t, m, 1, L, 0u, (uint32_t)k, hist, s_sum, s_out);
-    const TlSel b1 = tl_pass<1>(t, m, 1, L, b0.bin, b0.rem, hist, s_sum, s_out);
-    tk = (b0.bin << 8) | b1.bin;
+    bool found = false;
+    if (L > 0u) {
+      // one full pass: the totals >= L span a narrow range, so a direct
+      // histogram of (total - L) over 4096 bins (the last one open-ended)
+      // holds the k-th largest exactly unless it falls into the open bin
+      uint32_t* h12 = &hist[0][0];  // kTlWarps * 256 >= 4096 words
+      for (int i = tid; i < 4096; i += kTlThreads) h12[i] = 0u;
+      __syncthreads();
+      const int64_t ngroups = (m + 7) / 8;
+      const uint32_t ll = L << 16;
+      for (int64_t j0 = tid; j0 < ngroups; j0 += (int64_t)kTlThreads * kTlUnroll) {
+        uint4 v4[kTlUnroll];
+#pragma unroll
+        for (int u = 0; u < kTlUnroll; ++u) {
+          const int64_t j = j0 + (int64_t)u * kTlThreads;
+          v4[u] = j < ngroups ? __ldg(reinterpret_cast<const uint4*>(t + j * 8))
+                              : make_uint4(0u, 0u, 0u, 0u);
+        }
+#pragma unroll
+        for (int u = 0; u < kTlUnroll; ++u) {
+          const int64_t j = j0 + (int64_t)u * kTlThreads;
+          if (j >= ngroups) break;
+          const uint32_t w[4] = {v4[u].x, v4[u].y, v4[u].z, v4[u].w};
+          bool any = false;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) any |= (w[i] >= ll) | ((w[i] << 16) >= ll);
+          if (!any) continue;
+#pragma unroll
+          for (int h = 0; h < 8; ++h) {
+            const uint32_t v = (w[h >> 1] >> (16 * (h & 1))) & 0xFFFFu;
+            if (v < L || j * 8 + h >= m) continue;
+            atomicAdd(&h12[min(v - L, direct_bins - 1u)], 1u);
+          }
+        }
+      }
+      __syncthreads();
+      {  // thread i sums bins [8i, 8i + 8); thread 0 walks the 512 partial sums from the top
+        uint32_t c = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) c += h12[8 * tid + i];
+        s_part[tid] = c;
+      }
+      __syncthreads();
+      if (tid == 0) {
+        uint32_t run = 0;
+        int g = kTlThreads - 1;
+        for (; g > 0; --g) {
+          if (run + s_part[g] >= (uint32_t)k) break;
+          run += s_part[g];
+        }
+        int b = 8 * g + 7;
+        for (; b > 8 * g; --b) {
+          if (run + h12[b] >= (uint32_t)k) break;
+          run += h12[b];
+        }
+        s_out[0] = (uint32_t)b;
+      }
+      __syncthreads();
+      const uint32_t b = s_out[0];
+      __syncthreads();
+      if (b < direct_bins - 1u) {
+        tk = L + b;
+        found = true;
+      }
+    }
+    if (!found) {
+      const TlSel b0 = tl_pass<0>(t, m, 1, L, 0u, (uint32_t)k, hist, s_sum, s_out);
+      const TlSel b1 = tl_pass<1>(t, m, 1, L, b0.bin, b0.rem, hist, s_sum, s_out);
+      tk = (b0.bin << 8) | b1.bin;
+    }
   }
   if (tid == 0) {
     double l = 0.0;
@@ -410,8 +483,13 @@ void launch_sample_tlim(const uint16_t* tot_s, int64_t ld, int64_t m, int64_t nq
   // lets small samples take the two-level path)
   const char* e = std::getenv("HSB200_TLIM_SUBGROUPS");
   const int64_t sub_groups = e ? std::max<int64_t>(1, std::atoll(e)) : 8192;
-  k_sample_tlim<<<(unsigned)nq, kTlThreads, 0, st>>>(tot_s, ld, m, k, sub_groups, qptr, qv, wmin,
-                                                     wmax, btot, scl, off, tlim, T);
+  // bins of the direct histogram of the single full pass (the last one open-ended);
+  // HSB200_TLIM_DIRECT: test knob that makes the open bin, and the two-pass fallback, common
+  const char* e2 = std::getenv("HSB200_TLIM_DIRECT");
+  const uint32_t direct_bins =
+      e2 ? (uint32_t)std::min<int64_t>(4096, std::max<int64_t>(2, std::atoll(e2))) : 4096u;
+  k_sample_tlim<<<(unsigned)nq, kTlThreads, 0, st>>>(tot_s, ld, m, k, sub_groups, direct_bins, qptr,
+                                                     qv, wmin, wmax, btot, scl, off, tlim, T);
 }
 
 int launch_fuse_cands(const DeviceIndex& ix, int64_t nq, const uint8_t* luts, const double* btot,

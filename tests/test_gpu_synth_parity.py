@@ -274,12 +274,16 @@ def test_streamed_lut16_block_scheduling(static, monkeypatch):
             assert a.scores.tolist() == b.scores.tolist()
 
 
-@pytest.mark.parametrize("name,n,nq,sub", [("cfg2", 70_000, 70, 64), ("cfg3", 80_000, 5, 32),
-                                           ("cfg2", 70_000, 3, 100000)])
-def test_sample_threshold_two_level_selection(name, n, nq, sub, monkeypatch):
+@pytest.mark.parametrize("name,n,nq,sub,direct", [
+    ("cfg2", 70_000, 70, 64, None), ("cfg3", 80_000, 5, 32, None),
+    ("cfg2", 70_000, 3, 100000, None),
+    ("cfg2", 70_000, 70, 64, 16), ("cfg3", 80_000, 5, 32, 4)])  # open bin hit: two-pass fallback
+def test_sample_threshold_two_level_selection(name, n, nq, sub, direct, monkeypatch):
     """k_sample_tlim finds the k1-th largest sample total with a first selection
-    over a strided sub-sample (a lower bound) and two full passes that only
-    histogram totals at or above it.  HSB200_TLIM_SUBGROUPS shrinks the
+    over a strided sub-sample (a lower bound L) and one full pass with a direct
+    histogram of (total - L), falling back to two 8-bit passes when the k1-th
+    largest lands in the open-ended last bin (HSB200_TLIM_DIRECT shrinks the
+    histogram so that happens).  HSB200_TLIM_SUBGROUPS shrinks the
     sub-sample so the small test samples take that path (the last case: a
     sub-sample larger than the sample, i.e. the direct path); results must
     equal the unfiltered stage 1 for tensor-core and streamed batches."""
@@ -289,6 +293,8 @@ def test_sample_threshold_two_level_selection(name, n, nq, sub, monkeypatch):
               exact_final_rerank=s["exact_final_rerank"])
     monkeypatch.setenv("HSB200_FUSE_SAMPLE", "8192")
     monkeypatch.setenv("HSB200_TLIM_SUBGROUPS", str(sub))
+    if direct:
+        monkeypatch.setenv("HSB200_TLIM_DIRECT", str(direct))
     dev = hs.device_index(idx)
     dev.set_timing(True)
     fused = hs.search_batch(idx, qs, s["h"], **kw)
