@@ -19,6 +19,11 @@
 // and draws the following ones from a per-query counter (the next ticket is
 // in flight while the current block streams), so SMs that run ahead take
 // more blocks; the last CTA to finish re-arms the counter for the next launch.
+// (The kernel ends about half a block's time after the tickets run out —
+// ~6 of the 78 us a 320 MB query takes.  Half-block work units — ring stages
+// of 16 rows x 1 KB, one bulk copy per row, 8 points per thread — were
+// measured slower: 88 vs 80 us at 320 MB, 166 vs 145 us at 640 MB; the 1 KB
+// copies 2 KB apart stream at 4.1 instead of 5.0 TB/s.)
 //
 // Accumulation: a PRMT result register holds 4 points' bytes.  `all` adds
 // the registers as plain 32-bit integers (a base-256 sum with carries), `odd`
