@@ -304,3 +304,31 @@ def test_sample_threshold_two_level_selection(name, n, nq, sub, direct, monkeypa
     for a, b in zip(fused, ref):
         assert a.ids.tolist() == b.ids.tolist()
         assert a.scores.tolist() == b.scores.tolist()
+
+
+@pytest.mark.parametrize("K,nq", [(100, 193), (97, 70), (200, 100), (128, 385)])
+def test_tensor_core_group_shapes(K, nq, monkeypatch):
+    """Tensor-core scan shapes around the CTA-pair / single-CTA switch: K = 100
+    and 97 (pairs, 192-query groups, K not a multiple of the 8-subspace chunk,
+    odd K), K = 200 (single CTA, narrow groups), and batches that leave a
+    1-query or partial last group (193, 385) — filtered stage 1 against the
+    unfiltered scan and the oracle."""
+    ds, qs, cfg, idx = _scaled("cfg2", 70_000, nq, pq_subspaces=K)
+    s = cfg.search
+    kw = dict(overfetch=s["overfetch"], retain=s["retain"],
+              exact_final_rerank=s["exact_final_rerank"])
+    monkeypatch.setenv("HSB200_FUSE_SAMPLE", "4096")
+    dev = hs.device_index(idx)
+    dev.set_timing(True)
+    fused = hs.search_batch(idx, qs, s["h"], **kw)
+    assert "lut16_tc" in dev.kernel_times() and "fuse" in dev.kernel_times()
+    monkeypatch.setenv("HSB200_NO_FUSE", "1")
+    monkeypatch.setenv("HSB200_NO_TC", "1")
+    ref = hs.search_batch(idx, qs, s["h"], **kw)
+    for a, b in zip(fused, ref):
+        assert a.ids.tolist() == b.ids.tolist()
+        assert a.scores.tolist() == b.scores.tolist()
+    for i in range(0, qs.n, max(1, qs.n // 4)):
+        ids, sc, _ = O.search_topk(idx, *O.query_parts(qs, i), s["h"], **kw)
+        assert fused[i].ids.tolist() == ids.tolist()
+        np.testing.assert_allclose(fused[i].scores, sc, rtol=1e-9)
