@@ -292,14 +292,20 @@ int run_search(DeviceIndex& ix, const hs_query_batch& qb, int64_t nnz, int max_q
     // chunks give the per-query kernels (one CTA per query) more CTAs per
     // launch: cfg5 1236 -> 1197 ms per step from 8 to 16 GB, flat beyond
     // (HSB200_SCRATCH_GB overrides)
-    double budget = 8.0e9;
-    if (const char* eb = std::getenv("HSB200_SCRATCH_GB")) {
-      budget = std::max(0.5, std::atof(eb)) * 1e9;
-    } else {
-      size_t free_b = 0, total_b = 0;
-      if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess)
-        budget = std::min(16.0e9, std::max(2.0e9, 0.5 * ((double)free_b + (double)ix.scratch_bytes)));
+    // (decided once per index handle: cudaMemGetInfo is not free on a latency path)
+    if (ix.scratch_budget <= 0.0) {
+      double bud = 8.0e9;
+      if (const char* eb = std::getenv("HSB200_SCRATCH_GB")) {
+        bud = std::max(0.5, std::atof(eb)) * 1e9;
+      } else {
+        size_t free_b = 0, total_b = 0;
+        if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess)
+          bud = std::min(16.0e9,
+                         std::max(2.0e9, 0.5 * ((double)free_b + (double)ix.scratch_bytes)));
+      }
+      ix.scratch_budget = bud;
     }
+    const double budget = ix.scratch_budget;
     const int64_t cap = std::max<int64_t>(grp, (int64_t)(budget / per_q) / grp * grp);
     if (QB > cap) QB = cap;
   }

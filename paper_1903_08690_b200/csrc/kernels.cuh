@@ -84,6 +84,7 @@ struct DeviceIndex {
   // scratch arena (grown on demand, owned by the handle)
   void* scratch = nullptr;
   size_t scratch_bytes = 0;
+  double scratch_budget = 0.0;  // bytes the per-chunk stage-1 buffers may take (set on first search)
   // host entry point I/O staging (grown on demand): device query/result
   // buffers and a pinned host mirror, so a call does no cudaMalloc/cudaFree
   void* io_dev = nullptr;
