@@ -129,7 +129,7 @@ def test_bucketed_and_streamed_sparse_paths_agree(monkeypatch):
 @pytest.mark.parametrize("name,n,nq", [("cfg2", 40_000, 200), ("cfg3", 70_000, 150),
                                        ("cfg1", 30_000, 130)])
 def test_tensor_core_lut16_path_matches_oracle_and_prmt(name, n, nq, monkeypatch):
-    """Batches >= 64 queries take the tcgen05 kind::i8 LUT16 pass; results must be
+    """Batches >= 16 queries take the tcgen05 kind::i8 LUT16 pass; results must be
     identical to the PRMT CUDA-core path and to the oracle."""
     ds, qs, cfg, idx = _scaled(name, n, nq)
     s = cfg.search
