@@ -1012,6 +1012,9 @@ def main():
             ipk = 148 * 16384 * float(mhz) * 1e6 / 1e12
             roof["issue_peak"] = ipk
             roof["frac_of_issue_peak"] = achieved / ipk
+        # the algorithmic work behind those ops: one table lookup-add per (point, query,
+        # subspace); the one-hot product spends 32 u8 ops on each
+        roof["lookup_adds_per_s"] = float(n_local) * nq * K / (tc_ms / 1e3)
         b2 = _bf16x2_peak()
         if b2:
             roof["peak_2x_measured_bf16"] = b2
