@@ -565,8 +565,27 @@ def fullscale_checks(w, res_ids, res_sc, nq_check, s):
         got = res_sc[i][: len(ids)][mine]
         worst = max(worst, float(np.max(np.abs(got - ex) / np.maximum(np.abs(ex), 1e-300))))
         checked += int(mine.sum())
-    return {"queries": int(min(nq_check, res_ids.shape[0])), "rows_checked": checked,
-            "max_rel_err_exact_scores": worst}
+    out = {"queries": int(min(nq_check, res_ids.shape[0])), "rows_checked": checked,
+           "max_rel_err_exact_scores": worst}
+    # two independent scans at full scale: the same queries one at a time take the
+    # streamed PRMT scan (k_lut16_stream) instead of the tensor-core pass of the
+    # batch; ids and scores must be identical
+    try:
+        import paper_1903_08690_b200 as hs
+
+        kw = dict(overfetch=s["overfetch"], retain=s["retain"],
+                  exact_final_rerank=s["exact_final_rerank"])
+        nq1 = min(8, res_ids.shape[0])
+        bad_i = bad_s = 0
+        for i in range(nq1):
+            r = hs.search_batch(w.index, _sub(w.qs, i, i + 1), s["h"], **kw)[0]
+            ids = res_ids[i][res_ids[i] >= 0]
+            bad_i += int(r.ids.tolist() != ids.tolist())
+            bad_s += int(r.scores.tolist() != res_sc[i][: len(ids)].tolist())
+        out["tc_vs_streamed_scan"] = {"queries": nq1, "id_mismatch": bad_i, "score_mismatch": bad_s}
+    except Exception as e:  # noqa: BLE001
+        out["tc_vs_streamed_scan"] = {"error": repr(e)}
+    return out
 
 
 # ---------------------------------------------------------------------------
