@@ -1029,7 +1029,7 @@ int hs_quantize_lut(const double* T, int64_t nq, int32_t K, int32_t l, uint8_t* 
   HS_CUDA(cudaGetLastError());
   std::vector<int> hbad(nq);
   HS_CUDA(cudaMemcpy(hbad.data(), dbad, sizeof(int) * nq, cudaMemcpyDeviceToHost));
-  if (K * l) HS_CUDA(cudaMemcpy(table, dt, nq * K * l, cudaMemcpyDeviceToHost));
+  if (K > 0 && l > 0) HS_CUDA(cudaMemcpy(table, dt, nq * K * l, cudaMemcpyDeviceToHost));
   if (K) HS_CUDA(cudaMemcpy(bias, db, sizeof(double) * nq * K, cudaMemcpyDeviceToHost));
   HS_CUDA(cudaMemcpy(scale, ds, sizeof(double) * nq, cudaMemcpyDeviceToHost));
   HS_CUDA(cudaMemcpy(bias_total, dbt, sizeof(double) * nq, cudaMemcpyDeviceToHost));
