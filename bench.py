@@ -1031,6 +1031,16 @@ def main():
             ipk = 148 * 16384 * float(mhz) * 1e6 / 1e12
             roof["issue_peak"] = ipk
             roof["frac_of_issue_peak"] = achieved / ipk
+        # SURVEY 8(d)'s byte view of the same pass: one read of the code matrix per group
+        # of Qb queries (the pass is compute-bound by design, so this sits far below HBM)
+        # (query group of k_lut16_tc: CTA pairs hold 2 x 96 tables for K > 96, one CTA 160 below)
+        qb_grp = 192 if K > 96 else 160
+        hbm_pk, _ = _peaks()
+        passes = -(-nq // qb_grp)
+        cs_bytes = float(passes) * n_local * npairs
+        roof["code_stream"] = {"Qb": qb_grp, "passes_per_step": passes, "bytes_per_step": cs_bytes,
+                               "achieved_gbs": cs_bytes / (tc_ms / 1e3) / 1e9,
+                               "frac_of_hbm": cs_bytes / (tc_ms / 1e3) / 1e9 / hbm_pk}
         # the algorithmic work behind those ops: one table lookup-add per (point, query,
         # subspace); the one-hot product spends 32 u8 ops on each
         roof["lookup_adds_per_s"] = float(n_local) * nq * K / (tc_ms / 1e3)
