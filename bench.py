@@ -1054,6 +1054,7 @@ def main():
         achieved = alg_bytes / (s1_ms / 1e3) / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic.get("dram_bytes_per_launch"),
+                "frac_of_nominal_8tbs": achieved / 8000.0,
                 "kernel": "k_stage1 (posting stream + selection)", "peak_kind": peak_kind,
                 "alg_bytes_per_step": alg_bytes, "kernel_ms_per_step": s1_ms,
                 "traffic_source": traffic.get("source"),
@@ -1068,6 +1069,7 @@ def main():
         a1 = per_query_bytes / (qb1 / 1e3) / 1e9
         roof["qb1"] = {"scan_ms": qb1, "kernel": qb1_kernel, "alg_bytes": per_query_bytes,
                        "achieved_gbs": a1, "peak_gbs": peak, "frac": a1 / peak,
+                       "frac_of_nominal_8tbs": a1 / 8000.0,
                        "query_ms_all_kernels": float(np.mean(t1_all)) if t1_all else None,
                        "query_kernels_ms": {k: round(v, 4) for k, v in qb1_kt.items()},
                        "note": ("single-query path: one query per launch, L2 flushed before "
