@@ -306,12 +306,14 @@ def test_sample_threshold_two_level_selection(name, n, nq, sub, direct, monkeypa
         assert a.scores.tolist() == b.scores.tolist()
 
 
-@pytest.mark.parametrize("K,nq", [(100, 193), (97, 70), (200, 100), (128, 385)])
+@pytest.mark.parametrize("K,nq", [(100, 193), (97, 70), (200, 100), (128, 385), (128, 17), (128, 40),
+                                  (64, 16), (64, 33)])
 def test_tensor_core_group_shapes(K, nq, monkeypatch):
     """Tensor-core scan shapes around the CTA-pair / single-CTA switch: K = 100
     and 97 (pairs, 192-query groups, K not a multiple of the 8-subspace chunk,
-    odd K), K = 200 (single CTA, narrow groups), and batches that leave a
-    1-query or partial last group (193, 385) — filtered stage 1 against the
+    odd K), K = 200 (single CTA, narrow groups), batches that leave a 1-query
+    or partial last group (193, 385), and the smallest tensor-core batches
+    (16-40 queries: 32- and 64-query groups) — filtered stage 1 against the
     unfiltered scan and the oracle."""
     ds, qs, cfg, idx = _scaled("cfg2", 70_000, nq, pq_subspaces=K)
     s = cfg.search
