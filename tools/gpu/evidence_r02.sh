@@ -5,6 +5,7 @@ O=gpurun_out/r02
 mkdir -p $O
 timeout 2400 python -m pytest tests -m gpu -q > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $O/pytest_gpu.log
 timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc=$?" >> $O/smoke.log
+[ -x tools/mma_bench2 ] || nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/mma_bench2 tools/mma_bench2.cu
 nvidia-smi --query-gpu=clocks.sm,clocks.max.sm,power.draw --format=csv,noheader > $O/u8_peak.txt; ./tools/mma_bench2 >> $O/u8_peak.txt 2>&1; nvidia-smi --query-gpu=clocks.sm,clocks.max.sm,power.draw --format=csv,noheader >> $O/u8_peak.txt
 timeout 1200 python bench.py > $O/bench_cfg5.json 2> $O/bench_cfg5.err
 timeout 1200 python bench.py --impl reference > $O/bench_ref.json 2> $O/bench_ref.err
