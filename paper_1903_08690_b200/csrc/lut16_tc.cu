@@ -365,6 +365,7 @@ struct TcArgs {
   uint32_t* cnt;           // [nq][nseg]
   int64_t cap;
   int nseg;                // segment stride (>= grid size)
+  int rot;                 // producers take chunks by global index (see first_of)
   int exp;                 // dev profiling knobs (HSB200_TC_EXP: 1 epilogue drain only, 2 no TMEM
                            // stores, 8 no MMAs, 16 unused, 32 no code loads, 64 no pass appends; build with -DHS_TCPROF for per-warp wait cycles), results invalid when set
   uint32_t tmax;           // 255*K + 1: no total reaches it
@@ -555,12 +556,31 @@ __global__ void __launch_bounds__(PAIR ? kThreadsPair : kThreadsTc, 1)
       constexpr int NCH = (MAXC + NW - 1) / NW;              // max chunks per block
       constexpr int OW = ((NCH + kNPar - 1) / kNPar) * NW;   // words of this warp's chunks
       uint32_t nxt[OW];  // own chunk oc = c/kNPar: words oc*NW + h
+      // A quadrant's kNPar warps take the chunks c = par (mod kNPar) of every
+      // block.  The parity wait on a slot's `aempty` barrier is exact only
+      // while a warp revisits the ring at most `slots` chunks after its
+      // previous chunk; across a block boundary the fixed residue can leave a
+      // longer gap (14 chunks per block: chunks 11 -> 2 of the next block are
+      // 5 apart on a 4-slot ring).  For such shapes (a.rot, decided by the
+      // host) chunks go by their GLOBAL index (block * nkc + c) mod kNPar —
+      // always kNPar apart.  (Not by default: 2-3% slower at K = 128.)
+      // first_of(bi) = this warp's first chunk of block bi.
+      auto first_of = [&](int64_t bi) -> int {
+        if constexpr (NW == 1 && HS_TC_PREGEN && HS_TC_ROLLED) {
+          if (!a.rot) return par;  // the fixed residue is safe for this shape (and measured faster)
+          const int base = (int)(((blk_it + bi) * (int64_t)nkc) % kNPar);
+          return (par - base + kNPar) % kNPar;
+        } else {
+          return par;
+        }
+      };
       auto load_block = [&](int64_t bi) {
         const int64_t p = (b0 + bi) * PB + rank * kPM + quad * 32 + lane;
         const bool live = bi < nblk && p < a.n;
+        const int role = first_of(bi);
 #pragma unroll
         for (int i = 0; i < OW; ++i) {
-          const int w = (kNPar * (i / NW) + par) * NW + (i % NW);
+          const int w = (kNPar * (i / NW) + role) * NW + (i % NW);
           if (a.exp & 32) {
             nxt[i] = (uint32_t)(p * 2654435761u + w);
           } else {
@@ -617,7 +637,7 @@ __global__ void __launch_bounds__(PAIR ? kThreadsPair : kThreadsTc, 1)
           // stalls as issued instructions.)  The chunk's code word is always
           // cur[0]; the remaining words shift down.
 #pragma unroll 1
-          for (int c = par; c < nkc; c += kNPar) {
+          for (int c = first_of(bi); c < nkc; c += kNPar) {
             const uint32_t w = cur[0];
 #pragma unroll
             for (int i = 0; i + 1 < OW; ++i) cur[i] = cur[i + 1];
@@ -1016,7 +1036,9 @@ __global__ void k_to_hcodes(const uint8_t* __restrict__ packed, int64_t n, int n
 
 int pick_nq(int Kp, int64_t nq) {
   const int64_t by_smem = (int64_t)(kSmemBudget - 1024) / ((int64_t)Kp * 16);
-  int64_t v = std::min<int64_t>(kMaxNQ, by_smem) / 32 * 32;
+  // (<= 192: two accumulators of NQ columns must leave a ring of at least four
+  // 32-column A slots in the 512 TMEM columns)
+  int64_t v = std::min<int64_t>(192, std::min<int64_t>(kMaxNQ, by_smem)) / 32 * 32;
   const int64_t need = ceil_div(nq, 32) * 32;  // small batches: no idle columns
   if (need < v) v = need;
   return (int)std::max<int64_t>(v, 0);
@@ -1134,10 +1156,23 @@ int launch_tc(const DeviceIndex& ix, const uint8_t* luts, int64_t nq, int64_t n_
   // ring takes 4 narrow slots instead of 2 wide ones
   // (the pair keeps 32-column slots: with 64-column slots its ring is only
   // two deep, which hung in a dev run)
-  const int KCsel = L.pair ? 8 : kc_env == 8 ? 8 : kc_env == 16 ? 16
-                    : ((nw > 8 && nw <= 16) ? 16 : 8);
+  // (8-subspace slots everywhere: the rolled producer loop with the
+  // global-index chunk assignment serves them; HSB200_TC_KC=16 keeps the wide
+  // slots of the single-CTA form for A/B runs)
+  const int KCsel = L.pair ? 8 : kc_env == 16 ? 16 : 8;
   a.slots = std::min(slot_cap, (kTmemCols - 2 * NQ) / (4 * KCsel));
   if (a.slots < 3) HS_FAIL(HS_EUNSUPPORTED, "tensor-core LUT16: TMEM too small for the ring");
+  {
+    // largest distance between a producer warp's consecutive chunks under the
+    // fixed residue assignment (last chunk of a block -> first of the next)
+    const int nkc = (a.Kp + KCsel - 1) / KCsel;
+    int maxgap = 0;
+    for (int r = 0; r < kNPar && r < nkc; ++r) {
+      const int last = r + ((nkc - 1 - r) / kNPar) * kNPar;
+      maxgap = std::max(maxgap, (nkc - last) + r);
+    }
+    a.rot = (maxgap > a.slots || getenv("HSB200_TC_ROT")) ? 1 : 0;
+  }
   a.hcodes = ix.hcodes;
   a.luts = luts;
   a.tot = tot;

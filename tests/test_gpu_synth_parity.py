@@ -307,13 +307,16 @@ def test_sample_threshold_two_level_selection(name, n, nq, sub, direct, monkeypa
 
 
 @pytest.mark.parametrize("K,nq", [(100, 193), (97, 70), (200, 100), (128, 385), (128, 17), (128, 40),
-                                  (64, 16), (64, 33)])
+                                  (64, 16), (64, 33), (108, 200), (72, 150), (32, 300)])
 def test_tensor_core_group_shapes(K, nq, monkeypatch):
     """Tensor-core scan shapes around the CTA-pair / single-CTA switch: K = 100
     and 97 (pairs, 192-query groups, K not a multiple of the 8-subspace chunk,
     odd K), K = 200 (single CTA, narrow groups), batches that leave a 1-query
     or partial last group (193, 385), and the smallest tensor-core batches
-    (16-40 queries: 32- and 64-query groups) — filtered stage 1 against the
+    (16-40 queries: 32- and 64-query groups), K = 108 and 72 (chunk counts per
+    block whose fixed producer assignment would outrun the TMEM ring: chunks go
+    by global index there) and K = 32 with 300 queries (the group width is
+    capped so the ring keeps four slots) — filtered stage 1 against the
     unfiltered scan and the oracle."""
     ds, qs, cfg, idx = _scaled("cfg2", 70_000, nq, pq_subspaces=K)
     s = cfg.search
@@ -334,3 +337,19 @@ def test_tensor_core_group_shapes(K, nq, monkeypatch):
         ids, sc, _ = O.search_topk(idx, *O.query_parts(qs, i), s["h"], **kw)
         assert fused[i].ids.tolist() == ids.tolist()
         np.testing.assert_allclose(fused[i].scores, sc, rtol=1e-9)
+
+
+def test_tensor_core_global_chunk_assignment_forced(monkeypatch):
+    """HSB200_TC_ROT=1 forces the producers' global-index chunk assignment
+    (normally chosen only for shapes that need it) on the K = 128 pair kernel."""
+    ds, qs, cfg, idx = _scaled("cfg2", 70_000, 200)
+    s = cfg.search
+    kw = dict(overfetch=s["overfetch"], retain=s["retain"],
+              exact_final_rerank=s["exact_final_rerank"])
+    monkeypatch.setenv("HSB200_FUSE_SAMPLE", "4096")
+    base = hs.search_batch(idx, qs, s["h"], **kw)
+    monkeypatch.setenv("HSB200_TC_ROT", "1")
+    rot = hs.search_batch(idx, qs, s["h"], **kw)
+    for a, b in zip(rot, base):
+        assert a.ids.tolist() == b.ids.tolist()
+        assert a.scores.tolist() == b.scores.tolist()
