@@ -2,7 +2,7 @@
 (the chunk count per block, the group width and the ring depth all follow from
 them), filtered tensor-core results against the unfiltered CUDA-core scan.
 
-    python tools/tc_fuzz.py [trials] [seed]
+    python tools/tc_fuzz.py [trials] [seed] [small]      # small: batches of 1-15 queries (streamed scan)
 """
 import os
 import sys
@@ -16,10 +16,11 @@ from paper_1903_08690_b200 import synth  # noqa: E402
 
 trials = int(sys.argv[1]) if len(sys.argv) > 1 else 16
 rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 0)
+small = len(sys.argv) > 3 and sys.argv[3] == 'small'
 bad = 0
 for t in range(trials):
     K = int(rng.integers(4, 129))
-    nq = int(rng.choice([16, 31, 64, 97, 192, 193, 250, 385, 600]))
+    nq = int(rng.choice([1, 2, 5, 9, 15] if small else [16, 31, 64, 97, 192, 193, 250, 385, 600]))
     name = "cfg2" if K > 64 else "cfg1"
     ds, qs, cfg = synth.make_config(name, n=70_000, n_queries=nq)
     kw = dict(cfg.index)
@@ -31,7 +32,7 @@ for t in range(trials):
     dev.set_timing(True)
     for _ in range(2):  # twice: the second run reuses every ring / counter state
         a = hs.search_batch(idx, qs, s["h"], **skw)
-    used_tc = "lut16_tc" in dev.kernel_times()
+    used_tc = "lut16_tc" in dev.kernel_times() or "lut16_stream" in dev.kernel_times()
     os.environ["HSB200_NO_TC"] = "1"
     os.environ["HSB200_NO_FUSE"] = "1"
     b = hs.search_batch(idx, qs, s["h"], **skw)
